@@ -1,0 +1,225 @@
+"""Microsecond-stepped brute-force replay (second, independent implementation).
+
+Used only by tests on tiny instances (P <= 3, T <= 3, horizons of a few hundred
+µs).  It has no event queue: the clock advances one µs at a time, every timer is
+compared against the clock each µs, and a scheduling pass runs at every µs in
+which something fired while no iteration is in flight (R3).  Agreement
+with the event-driven oracle checks its next-event selection, the R1 order of
+same-instant events and the bookkeeping, by a different control structure.  EAGER expiry only.
+
+Semantics followed (C-5/C-6, Alg. 1 and §5.3):
+  * pin hit iff tool duration <= TTL (expiry checked as now > expiry)
+  * requests admitted at iteration boundaries; admission reserves all blocks
+  * program-level FCFS (pinned first) or request FCFS priority; HOL break
+  * victims: pinned programs with the largest index, only when nothing was admitted
+"""
+from __future__ import annotations
+
+import math
+
+from oracle import oracle as O  # the TTL formula itself is pinned separately
+
+
+def simulate(trace, gap_us, kv, pol, est, eng, fitted=None, horizon=200000):
+    P = trace.n_programs
+    progs = trace.programs
+    T = trace.turns
+    c0, cpf, ckv, ch2d, bs, maxb, dram_cap, max_it = [int(x) for x in eng]
+    prio, pause, dram, flags, t_pin, t_thresh = [int(x) for x in pol[:6]]
+    dram_on = dram != 0 and dram_cap > 0
+    victims_any = bool(flags & 1)
+    assert not (flags & 2), "brute force covers EAGER expiry only"
+
+    arr = [(int(progs["arr_q"][i]) * gap_us) >> 20 for i in range(P)]
+    t0 = [int(progs["turn0"][i]) for i in range(P)]
+    nt = [int(progs["nturns"][i]) for i in range(P)]
+
+    def rec(i, k):
+        return [int(x) for x in T[t0[i] + k]]
+
+    # per-program state as plain dicts
+    S = [dict(where="out", turn=0, ctx=0, blk=0, dblk=0, pin=None, waited_since=None,
+              tool_back=None, load_at=None, left=0, fresh=0, done_at=None) for _ in range(P)]
+    free = kv
+    dfree = dram_cap if dram_on else 0
+    chan = 0
+    stats = {"g": [0, 0, 0]}
+    n_done = 0
+    turns_done = 0
+    cnt = dict(iters=0, busy=0, bubble=0, prefill=0, recompute=0, hits=0, exp=0, vict=0, reload=0)
+    engine_until = None  # end time of the iteration in flight
+    batch = []
+
+    def drop(i):  # free GPU blocks, write through to DRAM
+        nonlocal free, dfree
+        free += S[i]["blk"]
+        S[i]["blk"] = 0
+        if dram_on:
+            dfree += S[i]["dblk"]
+            S[i]["dblk"] = 0
+            need = -(-S[i]["ctx"] // bs)
+            if 0 < need <= dfree:
+                S[i]["dblk"] = need
+                dfree -= need
+
+    def row(key):
+        return stats.get(key, [0, 0, 0])
+
+    def as_row(r):
+        n, s1, s2 = r
+        return [n, s1, s2 & (2**64 - 1), s2 >> 64]
+
+    def pause_ttl(i):
+        k = S[i]["turn"]
+        f = rec(i, k)[2]
+        if pause == 0:
+            return 0
+        if pause == 1:
+            return O.simplified(as_row(row("g")), as_row(row(f)), est, t_pin, t_thresh)
+        if pause == 2:
+            return O.calc_ttl(as_row(row("g")), as_row(row(f)), est, n_done, turns_done)
+        return int(fitted[f][min(k, fitted.shape[1] - 1)])
+
+    now = 0
+    while now <= horizon:
+        fired = False
+        # 1) pins that became stale this µs (first instant with now > expiry)
+        for i in range(P):
+            s = S[i]
+            if s["where"] == "tool" and s["pin"] is not None and now == s["pin"] + 1:
+                drop(i)
+                s["pin"] = None
+                cnt["exp"] += 1
+                fired = True
+        # 2) tool results come back: the program re-enters the queue, stats update
+        for i in range(P):
+            s = S[i]
+            if s["where"] == "tool" and s["tool_back"] == now:
+                f, d = rec(i, s["turn"])[2:4]
+                t = min(d, int(est[1]))
+                for key in ("g", f):
+                    r = stats.setdefault(key, [0, 0, 0])
+                    r[0] += 1
+                    r[1] += t
+                    r[2] += t * t
+                s["turn"] += 1
+                s["where"] = "queue"
+                s["waited_since"] = now
+                fired = True
+        # 3) KV loads complete
+        for i in range(P):
+            if S[i]["where"] == "loading" and S[i]["load_at"] == now:
+                S[i]["where"] = "loaded"
+                fired = True
+        # 4) new programs
+        for i in range(P):
+            if S[i]["where"] == "out" and arr[i] == now:
+                S[i].update(where="queue", turn=0, ctx=0, waited_since=now)
+                fired = True
+        # 5) the iteration in flight ends
+        if engine_until == now:
+            engine_until = None
+            fired = True
+            for i in sorted(batch):
+                s = S[i]
+                s["left"] -= 1
+                if s["left"] == 0:
+                    new, dec, f, d = rec(i, s["turn"])
+                    s["ctx"] += new + dec
+                    batch.remove(i)
+                    if s["turn"] == nt[i] - 1:
+                        free += s["blk"]
+                        s["blk"] = 0
+                        dfree += s["dblk"]
+                        s["dblk"] = 0
+                        s["where"] = "done"
+                        s["done_at"] = now
+                        n_done += 1
+                        turns_done += nt[i]
+                    else:
+                        ttl = pause_ttl(i)
+                        if ttl > 0:
+                            s["pin"] = now + ttl
+                        else:
+                            drop(i)
+                        s["tool_back"] = now + d
+                        s["where"] = "tool"
+        # 6) scheduling pass at an event instant with no iteration in flight (R3)
+        if engine_until is None and fired:
+            for i in range(P):
+                if S[i]["where"] == "loaded":
+                    S[i]["where"] = "run"
+                    batch.append(i)
+            admitted = 0
+            while True:
+                waiting = [i for i in range(P) if S[i]["where"] == "queue"]
+                busy = len(batch) + sum(1 for i in range(P) if S[i]["where"] == "loading")
+                if not waiting or busy >= maxb:
+                    break
+                if prio == 0:
+                    pinned_w = [i for i in waiting if S[i]["pin"] is not None]
+                    h = min(pinned_w) if pinned_w else min(waiting)
+                else:
+                    h = min(waiting, key=lambda i: (S[i]["waited_since"], i))
+                s = S[h]
+                new, dec, _, _ = rec(h, s["turn"])
+                total = -(-(s["ctx"] + new + dec) // bs)
+                need = total - s["blk"]
+                if need > free and (admitted == 0 or victims_any):
+                    for v in sorted((i for i in range(P) if S[i]["pin"] is not None and i != h),
+                                    reverse=True):
+                        if need <= free:
+                            break
+                        drop(v)
+                        S[v]["pin"] = None
+                        cnt["vict"] += 1
+                if need > free:
+                    break
+                free -= need
+                s["blk"] = total
+                cnt["bubble"] += now - s["waited_since"]
+                if s["pin"] is not None:
+                    cached = s["ctx"]
+                    s["pin"] = None
+                    cnt["hits"] += 1
+                    s["where"] = "run"
+                elif dram_on and s["dblk"] > 0 and s["dblk"] == -(-s["ctx"] // bs):
+                    cached = s["ctx"]
+                    start = max(now, chan)
+                    s["load_at"] = start + math.ceil(s["dblk"] * ch2d / 10**6)
+                    chan = s["load_at"]
+                    cnt["reload"] += 1
+                    s["where"] = "loading"
+                else:
+                    cached = 0
+                    cnt["recompute"] += s["ctx"]
+                    s["where"] = "run"
+                s["fresh"] = s["ctx"] + new - cached
+                cnt["prefill"] += s["fresh"]
+                s["left"] = dec
+                if s["where"] == "run":
+                    batch.append(h)
+                admitted += 1
+            waiting = [i for i in range(P) if S[i]["where"] == "queue"]
+            loading = [i for i in range(P) if S[i]["where"] == "loading"]
+            if waiting and admitted == 0 and not batch and not loading:
+                return "unschedulable", None, None
+            if batch:
+                if cnt["iters"] >= max_it:
+                    return "budget", None, None
+                ps = c0 + ckv * bs * sum(S[i]["blk"] for i in batch)
+                for i in batch:
+                    ps += cpf * S[i]["fresh"]
+                    S[i]["fresh"] = 0
+                dur = -(-ps // 10**6)
+                engine_until = now + dur
+                cnt["iters"] += 1
+                cnt["busy"] += dur
+        if n_done == P:
+            break
+        now += 1
+    if n_done != P:
+        return "horizon", None, None
+    jct = [S[i]["done_at"] - arr[i] for i in range(P)]
+    makespan = max(S[i]["done_at"] for i in range(P)) - min(arr)
+    return "ok", jct, dict(cnt, makespan=makespan, turns=turns_done)
