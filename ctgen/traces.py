@@ -261,3 +261,26 @@ def synthetic_samples(n: int, n_tools: int, seed: int = 0) -> tuple[np.ndarray, 
             z = _normal(_key(7, seed, f, idx, 1), _key(7, seed, f, idx, 2)).astype(np.float32)
             out[a:b] = np.clip(np.rint(np.float32(med) * np.exp(np.float32(sig) * z)), 1, mx).astype(np.int32)
     return out, off
+
+
+def synthetic_samples_torch(log2n: int, n_tools: int = 32, seed: int = 1234, device="cuda"):
+    """2^log2n duration samples (CSR by tool) generated on a torch device (bandwidth run).
+
+    Tool f has weight and median of catalog entry f % 12, lognormal sigma 0.8, clamped to
+    [1 µs, 120 s].  Returns (dur int32 tensor on `device`, tool_off int64 numpy [F+1]).
+    """
+    import torch
+    n = 1 << log2n
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    w = torch.tensor([TOOLS[f % N_TOOLS][2] for f in range(n_tools)], dtype=torch.float64)
+    cnt = (w / w.sum() * n).floor().long()
+    cnt[0] += n - int(cnt.sum())
+    off = np.concatenate([[0], np.cumsum(cnt.numpy())]).astype(np.int64)
+    dur = torch.empty(n, dtype=torch.int32, device=device)
+    for f in range(n_tools):
+        a, b = int(off[f]), int(off[f + 1])
+        z = torch.randn(b - a, generator=g, device=device)
+        med = float(TOOLS[f % N_TOOLS][3])
+        dur[a:b] = torch.clamp(med * torch.exp(0.8 * z), 1, 1.2e8).to(torch.int32)
+    return dur, off

@@ -1,0 +1,245 @@
+/* continuum.h — C ABI of libcontinuum: batched trace-replay evaluation of Continuum's
+ * tool-call-aware KV-cache TTL scheduling (arXiv 2511.02230) on B200 (sm_100a).
+ *
+ * Three calls make up the hot path:
+ *   ct_fit_ttl         TTL tables from per-tool duration samples        (§8(a) A-2)
+ *   ct_simulate_batch  replay of independent agent workloads            (§8(a) A-1, A-3..A-8)
+ *   ct_jct_stats       per-sweep-cell reduction of replica summaries    (§8(a) A-8)
+ * Citations are PAPER.md line numbers (the paper's LaTeX source) and DESIGN.md readings.
+ *
+ * Conventions
+ *   - Time is integer microseconds (int64); cost constants are integer picoseconds; an
+ *     iteration lasts ceil(sum_ps / 1e6) µs.  Statistics are exact integers (int64 / 128-bit).
+ *   - Pointers marked [dev] are CUDA device pointers, [host] are host pointers.  The caller
+ *     owns every input and output buffer; the library never frees caller memory.  A ct_ctx
+ *     owns only its own scratch.
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).  Calls are
+ *     asynchronous on that stream unless stated otherwise; results are valid after the stream
+ *     is synchronised.
+ *   - Every call returns CT_OK (0) or a negative CT_E* code; ct_last_error() returns a
+ *     thread-local message for the last failure.  No C++ exception crosses this boundary.
+ *   - Per-replica outcomes are reported in ct_replica_summary.status, not as return codes.
+ *   - Outputs are a pure function of the inputs: sharding the replica range over ranks, the
+ *     launch configuration and the stream do not change a single byte.
+ */
+#ifndef CONTINUUM_H
+#define CONTINUUM_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CT_ABI_VERSION 1
+
+/* return codes */
+#define CT_OK 0
+#define CT_EINVAL (-1)        /* an argument violates a documented precondition */
+#define CT_ENOMEM (-2)        /* device or host allocation failed */
+#define CT_ECUDA (-3)         /* a CUDA runtime call failed (message in ct_last_error) */
+#define CT_EUNSUPPORTED (-4)  /* device is not compute capability 10.0 (B200, sm_100a) */
+
+/* replica status (ct_replica_summary.status) */
+#define CT_R_OK 0
+#define CT_R_UNSCHEDULABLE 1  /* the head request can never fit (C-5 step 5c) */
+#define CT_R_EVENT_BUDGET 2   /* more than max_iters engine iterations would be needed */
+
+/* priority (PAPER.md:535-551 for PROG_FCFS; vanilla vLLM request FCFS PAPER.md:272) */
+#define CT_PRIO_PROG_FCFS 0   /* key (not pinned, program index): pinned first, then FCFS */
+#define CT_PRIO_REQ_FCFS 1    /* key (request arrival time, program index) */
+
+/* pause action on a non-final finish */
+#define CT_PAUSE_EVICT 0      /* free KV at once (vanilla vLLM) */
+#define CT_PAUSE_FIXED 1      /* §4.5 simplified: pin T_pin iff mean < T_thresh */
+#define CT_PAUSE_PAPER 2      /* Alg. 1 CalcTTL with the online empirical-Bernstein bound */
+#define CT_PAUSE_FITTED 3     /* table lookup ttl[tool][turn bucket] from ct_fit_ttl */
+
+#define CT_FLAG_VICTIMS_ANY 1 /* DESIGN.md R13 alternative: victims whenever the head misses */
+#define CT_FLAG_STEP_EXPIRY 2 /* DESIGN.md R4 alternative: release only at scheduling points */
+#define CT_ALWAYS INT64_MAX   /* t_thresh_us sentinel: pin unconditionally (TTL grid) */
+
+#define CT_MAX_PROGRAMS 256   /* programs per replica */
+#define CT_MAX_TOOLS 64
+#define CT_MAX_K 1024         /* TTL grid points */
+#define CT_MAX_J 64           /* turn buckets */
+
+typedef struct ct_ctx ct_ctx;
+
+/* ---- trace set ------------------------------------------------ */
+typedef struct {            /* 16 B, one per program, seeds back to back */
+  int64_t arr_q;            /* cumulative unit-rate Exp(1) arrival in Q20; non-decreasing in a
+                               seed.  arrival_us = floor(arr_q * gap_us / 2^20), < 2^62 */
+  int32_t turn0;            /* index of the program's first turn record */
+  int32_t nturns;           /* >= 1 */
+} ct_program;
+
+typedef struct {            /* 16 B, one per turn */
+  int32_t new_tokens;       /* tokens appended to the context this turn (>= 0) */
+  int32_t decode_tokens;    /* >= 1 */
+  int32_t tool;             /* tool called after this turn, 0..n_tools-1; -1 on the final turn */
+  int32_t dur_us;           /* tool duration = Δ_obs of PAPER.md:622-626, >= 1 (R25); 0 on final */
+} ct_turn;
+
+typedef struct {
+  const ct_program* programs;  /* [dev] n_seeds * n_programs records */
+  const ct_turn* turns;        /* [dev] n_turns records */
+  int64_t n_turns;
+  int32_t n_seeds;
+  int32_t n_programs;          /* P, programs per replica, 1..CT_MAX_PROGRAMS */
+  int32_t n_tools;             /* F, 1..CT_MAX_TOOLS */
+  int32_t reserved;
+} ct_trace_set;
+
+/* ---- parameters ---------------------------------------------------------------------- */
+typedef struct {            /* Continuum tunables, C-1/C-2 */
+  uint64_t lq;              /* round(ln(3/delta) * 2^32), delta in (0,1) => lq > 0 */
+  int64_t b_us;             /* upper bound b of a tool interval, > 0 */
+  int64_t t_default_us;     /* T_default, > 0 */
+  int64_t n_min;            /* threshold N, >= 1 */
+  int64_t a_num, a_den;     /* alpha = a_num / a_den, a_num >= 0, a_den >= 1 */
+  int64_t ttl_max_us;       /* clamp (reading R8); 0 disables */
+  int64_t reserved;
+} ct_estimator_params;
+
+typedef struct {            /* linear engine cost model (R16) */
+  int64_t c0_ps;            /* per iteration, >= 1 */
+  int64_t c_pf_ps;          /* per uncached prefill token in a request's first iteration */
+  int64_t c_kv_ps;          /* per resident token (bs * blocks) per iteration */
+  int64_t c_h2d_ps;         /* per block reloaded from DRAM, >= 1 when any policy uses DRAM */
+  int64_t bs;               /* tokens per KV block, >= 1 */
+  int64_t max_batch;        /* running + loading requests, >= 1 */
+  int64_t dram_blocks;      /* DRAM tier capacity in blocks, 0 = no tier */
+  int64_t max_iters;        /* engine-iteration budget per replica (CT_R_EVENT_BUDGET) */
+} ct_engine_params;
+
+typedef struct {            /* 48 B */
+  int32_t priority;         /* CT_PRIO_* */
+  int32_t pause;            /* CT_PAUSE_* */
+  int32_t dram;             /* 1 = evictions write through to the DRAM tier */
+  int32_t flags;            /* CT_FLAG_* */
+  int64_t t_pin_us;         /* FIXED: pin length */
+  int64_t t_thresh_us;      /* FIXED: pin iff mean < t_thresh (CT_ALWAYS = always) */
+  int64_t reserved[2];
+} ct_policy;
+
+/* Sweep: replica r -> (seed, rate, kv, policy) in mixed radix, policy fastest:
+ *   pol = r % n_policies; kv = (r / n_policies) % n_kv; rate = (r / (n_policies n_kv)) % n_rates;
+ *   seed = r / (n_policies n_kv n_rates).  Seed s replays programs [s P, (s+1) P). */
+typedef struct {
+  int32_t n_seeds, n_rates, n_kv, n_policies;
+  const int64_t* gap_us;      /* [host] n_rates mean inter-arrival gaps (lambda = 1e6/gap JPS) */
+  const int64_t* kv_blocks;   /* [host] n_kv GPU KV pool sizes in blocks */
+  const ct_policy* policies;  /* [host] n_policies */
+  ct_estimator_params est;
+  const int64_t* fitted_ttl;  /* [dev] n_tools x fitted_j table for CT_PAUSE_FITTED, or NULL */
+  int32_t fitted_j;
+  int32_t reserved;
+} ct_sweep;
+
+/* ---- outputs --------------------------------------------------------------------------- */
+typedef struct {            /* 128 B per replica; all zero except status when status != OK */
+  int32_t status;           /* CT_R_* */
+  int32_t n_done;           /* completed programs */
+  int64_t turns_done;
+  int64_t sum_jct_us, max_jct_us, p50_jct_us, p99_jct_us;  /* nearest rank (R20) */
+  int64_t sum_bubble_us;    /* waiting-queue time before admission */
+  int64_t makespan_us;      /* max completion - min arrival (R19) */
+  int64_t iterations;       /* engine iterations */
+  int64_t busy_us;          /* engine busy time */
+  int64_t prefill_tokens;   /* uncached tokens prefilled */
+  int64_t recompute_tokens; /* context tokens recomputed after eviction */
+  int64_t pin_hits, pin_expiries, victims, reloads;
+} ct_replica_summary;
+
+typedef struct {            /* 64 B per sweep cell (rate, kv, policy): sums over seeds */
+  int64_t n_ok, n_bad, sum_done, sum_turns, sum_jct_us, max_jct_us, sum_bubble_us, sum_makespan_us;
+} ct_cell_stats;
+
+/* ---- TTL fit ----------------------------------------------------------------------------- */
+typedef struct {
+  const int32_t* dur_us;      /* [dev] n samples grouped by tool (CSR), each >= 0 */
+  const int64_t* tool_off;    /* [host] n_tools + 1 non-decreasing offsets, tool_off[0] = 0 */
+  int64_t n;
+  int32_t n_tools;            /* F, 1..CT_MAX_TOOLS */
+  int32_t reserved;
+} ct_samples;
+
+typedef struct {            /* extension C-4 (not in PAPER.md; motivated by PAPER.md:323-338) */
+  int64_t c_pf_ps;          /* prefill ps per token saved on a hit */
+  int64_t c_pin_ps;         /* opportunity cost, ps per pinned block per µs */
+  int64_t bs;
+  int64_t a_num, a_den;     /* turn factor (1 + alpha w_j), alpha = a_num / a_den */
+  int64_t grid_step_us;     /* tau_k = k * grid_step_us, k = 0..K-1 */
+  int32_t K;                /* 1..CT_MAX_K */
+  int32_t J;                /* turn buckets, 1..CT_MAX_J */
+  int64_t ctx_tokens[CT_MAX_J];   /* expected context at turn bucket j */
+  int64_t turn_weight[CT_MAX_J];  /* w_j, default j + 1 = m(r) */
+  int64_t avg_turns_num;    /* paper mode: AvgTurns = num / den (turns_done / n_done), */
+  int64_t avg_turns_den;    /* den = 0 => AvgTurns factor 1 (reading R7) */
+} ct_cost_params;
+
+typedef struct {
+  int64_t* ttl_argmax;      /* [dev] (F+1) x J: tau* per tool row (row F = pooled samples) */
+  int64_t* ttl_paper;       /* [dev] F+1: CalcTTL offset per row */
+  int64_t* stats;           /* [dev] (F+1) x 4 {n, sum t~, sum t~^2 lo, hi}, t~ = min(t, b); or NULL */
+} ct_ttl_table;
+
+/* ---- calls ------------------------------------------------------------------------------- */
+int ct_version(void);
+const char* ct_last_error(void);
+
+/* Create a context on `device`.  Fails with CT_EUNSUPPORTED unless the device is sm_100. */
+int ct_ctx_create(int device, ct_ctx** out);
+int ct_ctx_destroy(ct_ctx* ctx);
+
+/* TTL fit, one HBM pass over the samples:
+ *  - paper mode: per tool f the statistics (n, sum t~, sum t~^2) of t~ = min(t, b) (R5), and
+ *    ttl_paper[f] = CalcTTL offset with 𝓑 selected by PAPER.md:515-521 and the caller's AvgTurns;
+ *  - argmax mode (extension C-4): n U(k) = V_j cnt_le(k) - C_j (sum_le(k) + tau_k (n - cnt_le(k))),
+ *    V_j = floor(c_pf ctx_j (a_den + a_num w_j) / a_den), C_j = c_pin ceil(ctx_j / bs); tau* is the
+ *    smallest maximiser over k >= 1 with U > 0, else 0.  Tools with n_f < N take the pooled row.
+ * Preconditions (else CT_EINVAL): samples within [0, 2^31); every product bounded so that the
+ * 128-bit arithmetic cannot overflow (checked against the sample count and the maxima).
+ * Errors: CT_EINVAL, CT_ENOMEM, CT_ECUDA. */
+int ct_fit_ttl(ct_ctx* ctx, const ct_samples* samples, const ct_cost_params* cost,
+               const ct_estimator_params* est, ct_ttl_table* out, void* stream);
+
+/* Replay replicas [replica_begin, replica_end) of the sweep:
+ * Alg. 1 with §5.3 pin/unpin/victims inside an
+ * integer discrete-event continuous-batching engine (C-5/C-6).
+ * out[i] (and jct_us[i*P .. i*P+P-1] when jct_us != NULL) belongs to replica
+ * replica_begin + i.  jct_us = completion - arrival per program, -1 when status != OK.
+ * Preconditions (else CT_EINVAL): 1 <= P <= CT_MAX_PROGRAMS; turns valid (decode >= 1, tool in
+ * range and dur >= 1 except on final turns); c0 >= 1, bs >= 1, max_batch >= 1; c_h2d >= 1 when a
+ * policy has dram = 1; fitted_ttl != NULL when a policy is FITTED; estimator valid when a policy
+ * is PAPER or FIXED with a threshold.  Errors: CT_EINVAL, CT_ENOMEM, CT_ECUDA. */
+int ct_simulate_batch(ct_ctx* ctx, const ct_trace_set* traces, const ct_sweep* sweep,
+                      const ct_engine_params* eng, int64_t replica_begin, int64_t replica_end,
+                      ct_replica_summary* out, int64_t* jct_us, void* stream);
+
+/* Same as ct_simulate_batch but with HOST buffers: programs/turns in traces->programs/turns are
+ * host pointers, out/jct_us are host pointers.  Copies in, runs, copies out and synchronises the
+ * stream before returning (end-to-end path; pinned host memory recommended). */
+int ct_simulate_batch_host(ct_ctx* ctx, const ct_trace_set* host_traces, const ct_sweep* sweep,
+                           const ct_engine_params* eng, int64_t replica_begin,
+                           int64_t replica_end, ct_replica_summary* host_out,
+                           int64_t* host_jct_us, void* stream);
+
+/* Per sweep cell (rate, kv, policy) sums over seeds of a full sweep's summaries (R19, R21).
+ * n_replicas must be a multiple of n_cells; replica r belongs to cell r % n_cells.
+ * summaries [dev] n_replicas, out [dev] n_cells.  Errors: CT_EINVAL, CT_ECUDA. */
+int ct_jct_stats(ct_ctx* ctx, const ct_replica_summary* summaries, int64_t n_replicas,
+                 int32_t n_cells, ct_cell_stats* out, void* stream);
+
+/* Launch statistics of the last ct_simulate_batch on this context (for bench accounting). */
+typedef struct {
+  int32_t grid, block, warps_per_block, slots_per_lane;
+  int64_t smem_per_block;
+  int64_t launches;         /* kernels launched by the last call */
+} ct_launch_info;
+int ct_last_launch(ct_ctx* ctx, ct_launch_info* info);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,10 @@
+"""libcontinuum: B200-native batched trace-replay of Continuum's KV-cache TTL scheduler.
+
+Product path only: C ABI in include/continuum.h, CUDA kernels in csrc/, ctypes binding
+in api.py.  No CPU fallback.
+"""
+from .api import (Context, DeviceTrace, ct_fit_ttl, ct_jct_stats, ct_simulate_batch,  # noqa: F401
+                  ct_simulate_batch_host, cost_params, status, SUMMARY_FIELDS)
+
+__all__ = ["Context", "DeviceTrace", "ct_fit_ttl", "ct_jct_stats", "ct_simulate_batch",
+           "ct_simulate_batch_host", "cost_params", "status", "SUMMARY_FIELDS"]

@@ -1,0 +1,226 @@
+"""Python binding of libcontinuum: same names as the C ABI, argument marshalling only.
+
+Every step of the hot path runs in the library's CUDA kernels; this module only turns
+torch tensors (device memory), streams and the ctgen parameter objects into the C structs of
+include/continuum.h.  There is no CPU fallback: without a CUDA device or without the built
+library every call raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+import torch
+
+from . import _lib as L
+
+SUMMARY_FIELDS = ["status_ndone", "turns_done", "sum_jct", "max_jct", "p50_jct", "p99_jct",
+                  "sum_bubble", "makespan", "iterations", "busy_us", "prefill_tokens",
+                  "recompute_tokens", "pin_hits", "pin_expiries", "victims", "reloads"]
+
+
+def _stream_ptr(stream) -> int | None:
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return stream.cuda_stream
+
+
+class Context:
+    """Owns a ct_ctx (scratch only) on one CUDA device."""
+
+    def __init__(self, device: int | None = None):
+        if not torch.cuda.is_available():
+            raise L.CtError("libcontinuum needs a CUDA device (no CPU fallback)")
+        self.device = torch.cuda.current_device() if device is None else int(device)
+        self._h = C.c_void_p()
+        with torch.cuda.device(self.device):
+            L.check(L.lib().ct_ctx_create(self.device, C.byref(self._h)), "ct_ctx_create")
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            try:
+                L.lib().ct_ctx_destroy(h)
+            except Exception:
+                pass
+            self._h = None
+
+    @property
+    def handle(self):
+        return self._h
+
+    def last_launch(self) -> dict:
+        info = L.LaunchInfo()
+        L.check(L.lib().ct_last_launch(self._h, C.byref(info)), "ct_last_launch")
+        return {k: getattr(info, k) for k, _ in L.LaunchInfo._fields_}
+
+
+# ---- parameter conversion -----------------------------------------------------------------
+def estimator_params(est) -> L.EstimatorParams:
+    a = [int(x) for x in est.as_array()]
+    return L.EstimatorParams(a[0], a[1], a[2], a[3], a[4], a[5], a[6], 0)
+
+
+def engine_params(eng) -> L.EngineParams:
+    return L.EngineParams(*[int(x) for x in eng.as_array()])
+
+
+class DeviceTrace:
+    """A ctgen TraceSet resident in HBM (programs: 16-B records, turns: int32[T, 4])."""
+
+    def __init__(self, trace, device=None):
+        dev = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+        self.trace = trace
+        self.programs = torch.from_numpy(np.ascontiguousarray(trace.programs).view(np.uint8)).to(dev)
+        self.turns = torch.from_numpy(np.ascontiguousarray(trace.turns, dtype=np.int32)).to(dev)
+        self.n_seeds, self.n_programs, self.n_tools = trace.n_seeds, trace.n_programs, trace.n_tools
+
+    @property
+    def bytes(self) -> int:
+        return self.programs.numel() + 4 * self.turns.numel()
+
+    def struct(self) -> L.TraceSet:
+        return L.TraceSet(self.programs.data_ptr(), self.turns.data_ptr(), int(self.turns.shape[0]),
+                          self.n_seeds, self.n_programs, self.n_tools, 0)
+
+
+class _SweepStruct:
+    """Keeps the host axis arrays alive for the duration of a call."""
+
+    def __init__(self, sweep, fitted: torch.Tensor | None = None):
+        self.gap = np.ascontiguousarray(sweep.gap_us, dtype=np.int64)
+        self.kv = np.ascontiguousarray(sweep.kv_blocks, dtype=np.int64)
+        pols = (L.Policy * len(sweep.policies))()
+        for i, p in enumerate(sweep.policies):
+            pols[i] = L.Policy(p.priority, p.pause, p.dram, p.flags, p.t_pin_us, p.t_thresh_us, (0, 0))
+        self.pols = pols
+        self.fitted = fitted
+        fptr, fj = 0, 0
+        if fitted is not None:
+            assert fitted.is_cuda and fitted.dtype == torch.int64 and fitted.is_contiguous()
+            fptr, fj = fitted.data_ptr(), int(fitted.shape[1])
+        self.s = L.Sweep(sweep.n_seeds, len(self.gap), len(self.kv), len(sweep.policies),
+                         self.gap.ctypes.data, self.kv.ctypes.data, C.addressof(pols),
+                         estimator_params(sweep.estimator), fptr, fj, 0)
+
+
+def _fitted_tensor(sweep, device):
+    if sweep.fitted is None:
+        return None
+    f = sweep.fitted
+    if isinstance(f, torch.Tensor):
+        return f.to(device=device, dtype=torch.int64).contiguous()
+    return torch.from_numpy(np.ascontiguousarray(f, dtype=np.int64)).to(device)
+
+
+# ---- the three calls ----------------------------------------------------------------------
+def ct_simulate_batch(ctx: Context, trace: DeviceTrace, sweep, engine, replica_begin: int = 0,
+                      replica_end: int | None = None, out: torch.Tensor | None = None,
+                      jct: torch.Tensor | bool | None = None, stream=None):
+    """Replay replicas [replica_begin, replica_end) on the GPU.
+
+    Returns (summary int64[R, 16] device tensor, jct int64[R, P] device tensor or None).
+    """
+    if replica_end is None:
+        replica_end = sweep.n_replicas
+    R = replica_end - replica_begin
+    dev = trace.turns.device
+    if out is None:
+        out = torch.empty((max(R, 0), 16), dtype=torch.int64, device=dev)
+    if jct is True:
+        jct = torch.empty((max(R, 0), trace.n_programs), dtype=torch.int64, device=dev)
+    elif jct is False:
+        jct = None
+    sw = _SweepStruct(sweep, _fitted_tensor(sweep, dev))
+    ts = trace.struct()
+    eng = engine_params(engine)
+    rc = L.lib().ct_simulate_batch(ctx.handle, C.byref(ts), C.byref(sw.s), C.byref(eng),
+                                   int(replica_begin), int(replica_end), out.data_ptr(),
+                                   jct.data_ptr() if jct is not None else None,
+                                   _stream_ptr(stream))
+    L.check(rc, "ct_simulate_batch")
+    return out, jct
+
+
+def ct_simulate_batch_host(ctx: Context, trace, sweep, engine, replica_begin: int = 0,
+                           replica_end: int | None = None, out: torch.Tensor | None = None,
+                           jct: torch.Tensor | None = None, stream=None,
+                           programs: torch.Tensor | None = None, turns: torch.Tensor | None = None):
+    """End-to-end call with HOST buffers (pinned torch tensors recommended).
+
+    programs (uint8 [S*P*16]) and turns (int32 [T, 4]) default to pinned copies of `trace`;
+    out (int64 [R, 16]) and jct (int64 [R, P] or None) are host tensors.  Synchronises.
+    """
+    if replica_end is None:
+        replica_end = sweep.n_replicas
+    R = replica_end - replica_begin
+    if programs is None:
+        programs = torch.from_numpy(np.ascontiguousarray(trace.programs).view(np.uint8)).pin_memory()
+    if turns is None:
+        turns = torch.from_numpy(np.ascontiguousarray(trace.turns, dtype=np.int32)).pin_memory()
+    if out is None:
+        out = torch.empty((R, 16), dtype=torch.int64).pin_memory()
+    dev = torch.device("cuda", ctx.device)
+    sw = _SweepStruct(sweep, _fitted_tensor(sweep, dev))
+    ts = L.TraceSet(programs.data_ptr(), turns.data_ptr(), int(turns.shape[0]), trace.n_seeds,
+                    trace.n_programs, trace.n_tools, 0)
+    eng = engine_params(engine)
+    rc = L.lib().ct_simulate_batch_host(ctx.handle, C.byref(ts), C.byref(sw.s), C.byref(eng),
+                                        int(replica_begin), int(replica_end), out.data_ptr(),
+                                        jct.data_ptr() if jct is not None else None,
+                                        _stream_ptr(stream))
+    L.check(rc, "ct_simulate_batch_host")
+    return out, jct
+
+
+def cost_params(c_pf_ps: int, c_pin_ps: int, bs: int, a_num: int, a_den: int, grid_step_us: int,
+                K: int, ctx_tokens, turn_weight, avg_turns=(0, 0)) -> L.CostParams:
+    J = len(ctx_tokens)
+    assert J == len(turn_weight) and 1 <= J <= L.MAX_J
+    cp = L.CostParams()
+    cp.c_pf_ps, cp.c_pin_ps, cp.bs, cp.a_num, cp.a_den = c_pf_ps, c_pin_ps, bs, a_num, a_den
+    cp.grid_step_us, cp.K, cp.J = grid_step_us, K, J
+    for j in range(J):
+        cp.ctx_tokens[j] = int(ctx_tokens[j])
+        cp.turn_weight[j] = int(turn_weight[j])
+    cp.avg_turns_num, cp.avg_turns_den = int(avg_turns[0]), int(avg_turns[1])
+    return cp
+
+
+def ct_fit_ttl(ctx: Context, dur_us: torch.Tensor, tool_off, cost: L.CostParams, est, stream=None,
+               want_stats: bool = True):
+    """TTL fit over device samples grouped by tool.
+
+    dur_us: int32 device tensor [n]; tool_off: host int64 [F+1].
+    Returns (ttl_argmax int64[F+1, J], ttl_paper int64[F+1], stats int64[F+1, 4] or None).
+    """
+    assert dur_us.is_cuda and dur_us.dtype == torch.int32 and dur_us.is_contiguous()
+    off = np.ascontiguousarray(tool_off, dtype=np.int64)
+    F = off.shape[0] - 1
+    J = cost.J
+    dev = dur_us.device
+    arg = torch.empty((F + 1, J), dtype=torch.int64, device=dev)
+    pap = torch.empty(F + 1, dtype=torch.int64, device=dev)
+    st = torch.empty((F + 1, 4), dtype=torch.int64, device=dev) if want_stats else None
+    sm = L.Samples(dur_us.data_ptr(), off.ctypes.data, int(off[-1]), F, 0)
+    tab = L.TtlTable(arg.data_ptr(), pap.data_ptr(), st.data_ptr() if st is not None else None)
+    e = estimator_params(est)
+    rc = L.lib().ct_fit_ttl(ctx.handle, C.byref(sm), C.byref(cost), C.byref(e), C.byref(tab),
+                            _stream_ptr(stream))
+    L.check(rc, "ct_fit_ttl")
+    return arg, pap, st
+
+
+def ct_jct_stats(ctx: Context, summary: torch.Tensor, n_cells: int, out: torch.Tensor | None = None,
+                 stream=None) -> torch.Tensor:
+    assert summary.is_cuda and summary.dtype == torch.int64 and summary.shape[1] == 16
+    if out is None:
+        out = torch.empty((n_cells, 8), dtype=torch.int64, device=summary.device)
+    rc = L.lib().ct_jct_stats(ctx.handle, summary.data_ptr(), int(summary.shape[0]), int(n_cells),
+                              out.data_ptr(), _stream_ptr(stream))
+    L.check(rc, "ct_jct_stats")
+    return out
+
+
+def status(summary: torch.Tensor | np.ndarray):
+    return summary[:, 0] & 0xFFFFFFFF

@@ -1,0 +1,370 @@
+// api.cu — libcontinuum host runtime: the C ABI of include/continuum.h.
+// Validation, launch planning (occupancy-sized persistent grids), scratch ownership and the
+// host-buffer end-to-end path.  No compute happens here: every step of the hot path runs in
+// the kernels of replay.cu, ttl_fit.cu and jct_stats.cu.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "ct_internal.h"
+
+struct ct_ctx {
+  int device = 0;
+  int sm_count = 0;
+  unsigned long long* counter = nullptr;
+  void* axes = nullptr;
+  size_t axes_cap = 0;
+  void* fit = nullptr;
+  size_t fit_cap = 0;
+  void* chunks = nullptr;
+  size_t chunks_cap = 0;
+  void* h_progs = nullptr;
+  size_t h_progs_cap = 0;
+  void* h_turns = nullptr;
+  size_t h_turns_cap = 0;
+  void* h_out = nullptr;
+  size_t h_out_cap = 0;
+  void* h_jct = nullptr;
+  size_t h_jct_cap = 0;
+  ct_launch_info last{};
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) __attribute__((format(printf, 2, 3)));
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+  return fail(CT_ECUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+#define CT_CUDA(call)                                        \
+  do {                                                       \
+    cudaError_t _e = (call);                                 \
+    if (_e != cudaSuccess) return cuda_fail(_e, #call);      \
+  } while (0)
+
+int ensure(void** p, size_t* cap, size_t need) {
+  if (*cap >= need && *p) return CT_OK;
+  if (*p) cudaFree(*p);
+  *p = nullptr;
+  *cap = 0;
+  size_t n = std::max<size_t>(need, 256);
+  cudaError_t e = cudaMalloc(p, n);
+  if (e != cudaSuccess) return fail(CT_ENOMEM, "cudaMalloc(%zu): %s", n, cudaGetErrorString(e));
+  *cap = n;
+  return CT_OK;
+}
+
+bool est_valid(const ct_estimator_params& e) {
+  return e.lq > 0 && e.b_us > 0 && e.t_default_us > 0 && e.n_min >= 1 && e.a_num >= 0 &&
+         e.a_den >= 1 && e.ttl_max_us >= 0 && e.b_us < (1ll << 40) &&
+         e.t_default_us < (1ll << 40) && e.lq < (1ull << 40);
+}
+
+typedef __int128 i128;
+
+}  // namespace
+
+extern "C" {
+
+int ct_version(void) { return CT_ABI_VERSION; }
+const char* ct_last_error(void) { return g_err.c_str(); }
+
+int ct_ctx_create(int device, ct_ctx** out) {
+  if (!out) return fail(CT_EINVAL, "out is NULL");
+  *out = nullptr;
+  cudaDeviceProp prop;
+  cudaError_t e = cudaGetDeviceProperties(&prop, device);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDeviceProperties");
+  if (prop.major != 10 || prop.minor != 0)
+    return fail(CT_EUNSUPPORTED, "device %d is sm_%d%d; libcontinuum is built for sm_100a", device,
+                prop.major, prop.minor);
+  CT_CUDA(cudaSetDevice(device));
+  ct_ctx* c = new ct_ctx();
+  c->device = device;
+  c->sm_count = prop.multiProcessorCount;
+  e = cudaMalloc((void**)&c->counter, 64);
+  if (e != cudaSuccess) {
+    delete c;
+    return fail(CT_ENOMEM, "cudaMalloc counter: %s", cudaGetErrorString(e));
+  }
+  *out = c;
+  return CT_OK;
+}
+
+int ct_ctx_destroy(ct_ctx* c) {
+  if (!c) return CT_OK;
+  void* ps[] = {c->counter, c->axes, c->fit, c->chunks, c->h_progs, c->h_turns, c->h_out, c->h_jct};
+  for (void* p : ps)
+    if (p) cudaFree(p);
+  delete c;
+  return CT_OK;
+}
+
+int ct_last_launch(ct_ctx* c, ct_launch_info* info) {
+  if (!c || !info) return fail(CT_EINVAL, "NULL argument");
+  *info = c->last;
+  return CT_OK;
+}
+
+// ---------------------------------------------------------------------------------------------
+int ct_simulate_batch(ct_ctx* c, const ct_trace_set* tr, const ct_sweep* sw,
+                      const ct_engine_params* eng, int64_t rb, int64_t re,
+                      ct_replica_summary* out, int64_t* jct, void* stream) {
+  if (!c || !tr || !sw || !eng) return fail(CT_EINVAL, "NULL argument");
+  const int P = tr->n_programs, F = tr->n_tools;
+  if (P < 1 || P > CT_MAX_PROGRAMS) return fail(CT_EINVAL, "n_programs %d not in [1, %d]", P, CT_MAX_PROGRAMS);
+  if (F < 1 || F > CT_MAX_TOOLS) return fail(CT_EINVAL, "n_tools %d not in [1, %d]", F, CT_MAX_TOOLS);
+  if (!tr->programs || !tr->turns || tr->n_turns < 1) return fail(CT_EINVAL, "empty trace set");
+  if (sw->n_seeds < 1 || sw->n_rates < 1 || sw->n_kv < 1 || sw->n_policies < 1)
+    return fail(CT_EINVAL, "sweep axes must be non-empty");
+  if (sw->n_seeds > tr->n_seeds) return fail(CT_EINVAL, "sweep has more seeds than the trace set");
+  if (!sw->gap_us || !sw->kv_blocks || !sw->policies) return fail(CT_EINVAL, "NULL sweep axis");
+  const int64_t R = (int64_t)sw->n_seeds * sw->n_rates * sw->n_kv * sw->n_policies;
+  if (rb < 0 || re < rb || re > R) return fail(CT_EINVAL, "replica range [%lld, %lld) outside [0, %lld)",
+                                               (long long)rb, (long long)re, (long long)R);
+  const ct_engine_params& E = *eng;
+  if (E.c0_ps < 1 || E.bs < 1 || E.max_batch < 1 || E.c_pf_ps < 0 || E.c_kv_ps < 0 ||
+      E.c_h2d_ps < 0 || E.dram_blocks < 0 || E.max_iters < 0)
+    return fail(CT_EINVAL, "invalid engine parameters (R16/R25)");
+  if (E.c0_ps >= (1ll << 48) || E.c_pf_ps >= (1ll << 40) || E.c_kv_ps >= (1ll << 30) ||
+      E.c_h2d_ps >= (1ll << 40) || E.bs >= (1 << 20) || E.dram_blocks >= (1ll << 30))
+    return fail(CT_EINVAL, "engine constants exceed the int64 fixed-point bounds");
+  bool need_est = false, need_fit = false, need_h2d = false;
+  for (int i = 0; i < sw->n_policies; ++i) {
+    const ct_policy& p = sw->policies[i];
+    if (p.priority != CT_PRIO_PROG_FCFS && p.priority != CT_PRIO_REQ_FCFS)
+      return fail(CT_EINVAL, "policy %d: priority %d", i, p.priority);
+    if (p.pause < CT_PAUSE_EVICT || p.pause > CT_PAUSE_FITTED)
+      return fail(CT_EINVAL, "policy %d: pause %d", i, p.pause);
+    if (p.flags & ~(CT_FLAG_VICTIMS_ANY | CT_FLAG_STEP_EXPIRY))
+      return fail(CT_EINVAL, "policy %d: unknown flags", i);
+    if (p.t_pin_us < 0 || p.t_pin_us >= (1ll << 50)) return fail(CT_EINVAL, "policy %d: t_pin", i);
+    need_est |= p.pause == CT_PAUSE_PAPER || (p.pause == CT_PAUSE_FIXED && p.t_thresh_us != CT_ALWAYS);
+    need_fit |= p.pause == CT_PAUSE_FITTED;
+    need_h2d |= p.dram != 0 && E.dram_blocks > 0;
+  }
+  if (need_est && !est_valid(sw->est)) return fail(CT_EINVAL, "invalid estimator parameters");
+  if (need_fit && (!sw->fitted_ttl || sw->fitted_j < 1 || sw->fitted_j > CT_MAX_J))
+    return fail(CT_EINVAL, "FITTED policy needs fitted_ttl[n_tools][fitted_j]");
+  if (need_h2d && E.c_h2d_ps < 1) return fail(CT_EINVAL, "DRAM tier needs c_h2d_ps >= 1 (R25)");
+  for (int i = 0; i < sw->n_rates; ++i)
+    if (sw->gap_us[i] < 0 || sw->gap_us[i] >= (1ll << 30)) return fail(CT_EINVAL, "gap_us[%d]", i);
+  for (int i = 0; i < sw->n_kv; ++i)
+    if (sw->kv_blocks[i] < 0 || sw->kv_blocks[i] >= (1ll << 30)) return fail(CT_EINVAL, "kv_blocks[%d]", i);
+  if (re == rb) return CT_OK;
+  if (!out) return fail(CT_EINVAL, "out is NULL");
+  cudaStream_t s = (cudaStream_t)stream;
+
+  // device copy of the sweep axes
+  const size_t n_gap = sw->n_rates, n_kv = sw->n_kv, n_pol = sw->n_policies;
+  const size_t bytes = 8 * (n_gap + n_kv) + sizeof(ct_policy) * n_pol;
+  int rc = ensure(&c->axes, &c->axes_cap, bytes);
+  if (rc) return rc;
+  std::vector<unsigned char> hb(bytes);
+  std::memcpy(hb.data(), sw->gap_us, 8 * n_gap);
+  std::memcpy(hb.data() + 8 * n_gap, sw->kv_blocks, 8 * n_kv);
+  std::memcpy(hb.data() + 8 * (n_gap + n_kv), sw->policies, sizeof(ct_policy) * n_pol);
+  CT_CUDA(cudaMemcpyAsync(c->axes, hb.data(), bytes, cudaMemcpyHostToDevice, s));
+  CT_CUDA(cudaMemsetAsync(c->counter, 0, 8, s));
+
+  ct::ReplayArgs a;
+  a.progs = tr->programs;
+  a.turns = (const int4*)tr->turns;
+  a.P = P;
+  a.F = F;
+  a.gap = (const int64_t*)c->axes;
+  a.kv = a.gap + n_gap;
+  a.pols = (const ct_policy*)(a.kv + n_kv);
+  a.n_rate = sw->n_rates;
+  a.n_kv = sw->n_kv;
+  a.n_pol = sw->n_policies;
+  a.est = sw->est;
+  a.fitted = sw->fitted_ttl;
+  a.J = sw->fitted_j > 0 ? sw->fitted_j : 1;
+  a.eng = E;
+  a.r_begin = rb;
+  a.r_end = re;
+  a.out = out;
+  a.jct = jct;
+  a.counter = c->counter;
+  const int ns = P <= 32 ? 1 : P <= 64 ? 2 : P <= 128 ? 4 : 8;
+  const int wpb = 4;
+  a.smem_per_warp = ct::replay_smem_per_warp(ns, F);
+  const int smem = a.smem_per_warp * wpb;
+  int occ = ct::replay_occupancy(ns, wpb, smem);
+  if (occ < 1) return fail(CT_ECUDA, "replay kernel cannot be resident (smem %d)", smem);
+  const int64_t need_blocks = (re - rb + wpb - 1) / wpb;
+  const int grid = (int)std::min<int64_t>((int64_t)c->sm_count * occ, need_blocks);
+  cudaError_t e = ct::launch_replay(a, ns, wpb, grid, s);
+  if (e != cudaSuccess) return cuda_fail(e, "replay launch");
+  c->last.grid = grid;
+  c->last.block = 32 * wpb;
+  c->last.warps_per_block = wpb;
+  c->last.slots_per_lane = ns;
+  c->last.smem_per_block = smem;
+  c->last.launches = 1;
+  return CT_OK;
+}
+
+int ct_simulate_batch_host(ct_ctx* c, const ct_trace_set* ht, const ct_sweep* sw,
+                           const ct_engine_params* eng, int64_t rb, int64_t re,
+                           ct_replica_summary* host_out, int64_t* host_jct, void* stream) {
+  if (!c || !ht || !sw || !eng || !host_out) return fail(CT_EINVAL, "NULL argument");
+  const int P = ht->n_programs, F = ht->n_tools;
+  if (P < 1 || P > CT_MAX_PROGRAMS || F < 1 || F > CT_MAX_TOOLS || ht->n_seeds < 1 || ht->n_turns < 1)
+    return fail(CT_EINVAL, "invalid trace-set shape");
+  // host-side trace validation (the device variant takes these as preconditions)
+  const int64_t np = (int64_t)ht->n_seeds * P;
+  for (int64_t i = 0; i < np; ++i) {
+    const ct_program& p = ht->programs[i];
+    if (p.nturns < 1 || p.turn0 < 0 || (int64_t)p.turn0 + p.nturns > ht->n_turns || p.arr_q < 0 ||
+        p.arr_q >= (1ll << 32))
+      return fail(CT_EINVAL, "program %lld invalid", (long long)i);
+    if (i % P && p.arr_q < ht->programs[i - 1].arr_q)
+      return fail(CT_EINVAL, "arrivals not sorted in seed %lld", (long long)(i / P));
+    for (int t = 0; t < p.nturns; ++t) {
+      const ct_turn& u = ht->turns[p.turn0 + t];
+      const bool last = t == p.nturns - 1;
+      if (u.decode_tokens < 1 || u.new_tokens < 0 ||
+          (!last && (u.tool < 0 || u.tool >= F || u.dur_us < 1)))
+        return fail(CT_EINVAL, "turn %d of program %lld invalid", t, (long long)i);
+    }
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t R = re - rb;
+  int rc;
+  if ((rc = ensure(&c->h_progs, &c->h_progs_cap, 16 * np))) return rc;
+  if ((rc = ensure(&c->h_turns, &c->h_turns_cap, 16 * ht->n_turns))) return rc;
+  if ((rc = ensure(&c->h_out, &c->h_out_cap, sizeof(ct_replica_summary) * std::max<int64_t>(R, 1)))) return rc;
+  if (host_jct && (rc = ensure(&c->h_jct, &c->h_jct_cap, 8 * std::max<int64_t>(R, 1) * P))) return rc;
+  CT_CUDA(cudaMemcpyAsync(c->h_progs, ht->programs, 16 * np, cudaMemcpyHostToDevice, s));
+  CT_CUDA(cudaMemcpyAsync(c->h_turns, ht->turns, 16 * ht->n_turns, cudaMemcpyHostToDevice, s));
+  ct_trace_set dt = *ht;
+  dt.programs = (const ct_program*)c->h_progs;
+  dt.turns = (const ct_turn*)c->h_turns;
+  rc = ct_simulate_batch(c, &dt, sw, eng, rb, re, (ct_replica_summary*)c->h_out,
+                         host_jct ? (int64_t*)c->h_jct : nullptr, stream);
+  if (rc) return rc;
+  CT_CUDA(cudaMemcpyAsync(host_out, c->h_out, sizeof(ct_replica_summary) * R, cudaMemcpyDeviceToHost, s));
+  if (host_jct) CT_CUDA(cudaMemcpyAsync(host_jct, c->h_jct, 8 * R * P, cudaMemcpyDeviceToHost, s));
+  CT_CUDA(cudaStreamSynchronize(s));
+  return CT_OK;
+}
+
+// ---------------------------------------------------------------------------------------------
+int ct_fit_ttl(ct_ctx* c, const ct_samples* sm, const ct_cost_params* cp,
+               const ct_estimator_params* est, ct_ttl_table* out, void* stream) {
+  if (!c || !sm || !cp || !est || !out || !out->ttl_argmax || !out->ttl_paper)
+    return fail(CT_EINVAL, "NULL argument");
+  const int F = sm->n_tools, K = cp->K, J = cp->J;
+  if (F < 1 || F > CT_MAX_TOOLS) return fail(CT_EINVAL, "n_tools %d", F);
+  if (K < 1 || K > CT_MAX_K || J < 1 || J > CT_MAX_J) return fail(CT_EINVAL, "K %d / J %d", K, J);
+  if (!sm->tool_off || sm->tool_off[0] != 0 || sm->tool_off[F] != sm->n || sm->n < 0)
+    return fail(CT_EINVAL, "tool_off must run from 0 to n");
+  if (sm->n > 0 && !sm->dur_us) return fail(CT_EINVAL, "dur_us is NULL");
+  for (int f = 0; f < F; ++f)
+    if (sm->tool_off[f + 1] < sm->tool_off[f]) return fail(CT_EINVAL, "tool_off not monotone");
+  if (!est_valid(*est)) return fail(CT_EINVAL, "invalid estimator parameters");
+  if (cp->grid_step_us < 1 || cp->bs < 1 || cp->a_den < 1 || cp->a_num < 0 || cp->c_pf_ps < 0 ||
+      cp->c_pin_ps < 0 || cp->avg_turns_num < 0 || cp->avg_turns_den < 0)
+    return fail(CT_EINVAL, "invalid cost parameters");
+  const i128 tau_max = (i128)(K - 1) * cp->grid_step_us;
+  if (tau_max >= ((i128)1 << 43)) return fail(CT_EINVAL, "grid too long: (K-1)*step >= 2^43");
+  // 128-bit headroom of n U(k) (extension C-4)
+  const i128 n = sm->n;
+  for (int j = 0; j < J; ++j) {
+    if (cp->ctx_tokens[j] < 0 || cp->ctx_tokens[j] >= (1ll << 32) || cp->turn_weight[j] < 0 ||
+        cp->turn_weight[j] >= (1ll << 32))
+      return fail(CT_EINVAL, "ctx_tokens / turn_weight[%d] out of range", j);
+    i128 V = ((i128)cp->c_pf_ps * cp->ctx_tokens[j] * ((i128)cp->a_den + (i128)cp->a_num * cp->turn_weight[j])) / cp->a_den;
+    i128 C = (i128)cp->c_pin_ps * ((cp->ctx_tokens[j] + cp->bs - 1) / cp->bs);
+    const i128 lim = (i128)1 << 125;
+    if (V > lim / (n + 1) || C > lim / ((n + 1) * (((i128)1 << 31) + tau_max + 1)))
+      return fail(CT_EINVAL, "cost products could overflow 128-bit arithmetic");
+  }
+  if (n >= ((i128)1 << 40)) return fail(CT_EINVAL, "too many samples");
+  cudaStream_t s = (cudaStream_t)stream;
+  // chunk plan: <= CH samples per CTA work item so a warp's packed bins cannot overflow
+  const int64_t tmax = std::max<int64_t>((int64_t)tau_max, 1);
+  int64_t CH = std::min<int64_t>(1ll << 17, ((1ll << 44) - 1) / tmax);
+  CH = std::min<int64_t>(CH, (1ll << 20) - 1);
+  if (CH < 256) return fail(CT_EINVAL, "grid step too large for the packed histogram");
+  std::vector<ct::FitChunk> chunks;
+  for (int f = 0; f < F; ++f)
+    for (int64_t b = sm->tool_off[f]; b < sm->tool_off[f + 1]; b += CH)
+      chunks.push_back({b, std::min(b + CH, sm->tool_off[f + 1]), f, 0});
+  const size_t hbytes = 8 * (size_t)F * (K + 1);
+  const size_t fbytes = 2 * hbytes + 8 * 6 * (size_t)F;
+  int rc = ensure(&c->fit, &c->fit_cap, fbytes);
+  if (rc) return rc;
+  CT_CUDA(cudaMemsetAsync(c->fit, 0, fbytes, s));
+  int launches = 0;
+  ct::FitArgs fa;
+  fa.dur = sm->dur_us;
+  fa.F = F;
+  fa.K = K;
+  fa.step = cp->grid_step_us;
+  fa.step_magic = (uint64_t)(((((unsigned __int128)1) << 32) + cp->grid_step_us - 1) / cp->grid_step_us);
+  fa.b_us = est->b_us;
+  fa.hcnt = (unsigned long long*)c->fit;
+  fa.hsum = fa.hcnt + (size_t)F * (K + 1);
+  fa.stat = fa.hsum + (size_t)F * (K + 1);
+  fa.n_chunks = (int64_t)chunks.size();
+  if (!chunks.empty()) {
+    if ((rc = ensure(&c->chunks, &c->chunks_cap, sizeof(ct::FitChunk) * chunks.size()))) return rc;
+    CT_CUDA(cudaMemcpyAsync(c->chunks, chunks.data(), sizeof(ct::FitChunk) * chunks.size(),
+                            cudaMemcpyHostToDevice, s));
+    fa.chunks = (const ct::FitChunk*)c->chunks;
+    const int occ = ct::fit_hist_occupancy(ct::fit_hist_smem(K));
+    if (occ < 1) return fail(CT_ECUDA, "fit_hist kernel cannot be resident");
+    const int grid = (int)std::min<int64_t>((int64_t)c->sm_count * occ, fa.n_chunks);
+    cudaError_t e = ct::launch_fit_hist(fa, grid, s);
+    if (e != cudaSuccess) return cuda_fail(e, "fit_hist launch");
+    ++launches;
+  }
+  ct::ScanArgs sa;
+  sa.hcnt = fa.hcnt;
+  sa.hsum = fa.hsum;
+  sa.stat = fa.stat;
+  sa.F = F;
+  sa.K = K;
+  sa.J = J;
+  sa.cost = *cp;
+  sa.est = *est;
+  sa.ttl_argmax = out->ttl_argmax;
+  sa.ttl_paper = out->ttl_paper;
+  sa.stats_out = out->stats;
+  cudaError_t e = ct::launch_fit_scan(sa, s);
+  if (e != cudaSuccess) return cuda_fail(e, "fit_scan launch");
+  ++launches;
+  c->last.launches = launches;
+  return CT_OK;
+}
+
+int ct_jct_stats(ct_ctx* c, const ct_replica_summary* sum, int64_t n, int32_t n_cells,
+                 ct_cell_stats* out, void* stream) {
+  if (!c || !sum || !out) return fail(CT_EINVAL, "NULL argument");
+  if (n_cells < 1 || n < 0 || n % n_cells) return fail(CT_EINVAL, "n_replicas must be a multiple of n_cells");
+  cudaError_t e = ct::launch_jct_stats(sum, n, n_cells, out, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "jct_stats launch");
+  return CT_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,110 @@
+// ct_device.cuh — device helpers shared by libcontinuum's kernels (sm_100a only).
+#pragma once
+#include <stdint.h>
+
+#include "continuum.h"
+
+#define CT_INF64 ((int64_t)0x7fffffffffffffffLL)
+#define FULL_MASK 0xffffffffu
+
+typedef unsigned __int128 u128_t;
+typedef __int128 i128_t;
+
+namespace ct {
+
+__device__ __forceinline__ int64_t warp_min64(int64_t v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    int64_t w = __shfl_xor_sync(FULL_MASK, v, o);
+    v = w < v ? w : v;
+  }
+  return v;
+}
+
+__device__ __forceinline__ int64_t warp_max64(int64_t v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    int64_t w = __shfl_xor_sync(FULL_MASK, v, o);
+    v = w > v ? w : v;
+  }
+  return v;
+}
+
+__device__ __forceinline__ uint64_t warp_sum_u64(uint64_t v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL_MASK, v, o);
+  return v;
+}
+
+__device__ __forceinline__ int64_t ceil_div_i64(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// floor(sqrt(x)) exactly: double estimate, then integer correction.
+__device__ __forceinline__ uint64_t isqrt_u64(uint64_t x) {
+  uint64_t r = (uint64_t)sqrt((double)x);
+  if (r > 0xffffffffull) r = 0xffffffffull;
+  while (r * r > x) --r;
+  while (r < 0xffffffffull && (r + 1) * (r + 1) <= x) ++r;
+  return r;
+}
+
+struct Stat {  // one estimator row: n, sum t~, sum t~^2 (128-bit as lo/hi)
+  int64_t n, s1;
+  uint64_t s2lo, s2hi;
+};
+
+// Empirical Bernstein bound B(delta), fixed point (C-1):
+// floor(s1/n) + isqrt(floor(2 v L_q / (n 2^32))) + floor(3 b L_q / (n 2^32)),
+// v = floor((n s2 - s1^2) / (n (n-1))) for n >= 2, else 0.
+__device__ __forceinline__ int64_t bernstein(const Stat& s, uint64_t lq, int64_t b_us) {
+  const int64_t n = s.n;
+  int64_t mu = s.s1 / n;
+  u128_t v = 0;
+  if (n >= 2) {
+    u128_t s2 = ((u128_t)s.s2hi << 64) | s.s2lo;
+    u128_t num = (u128_t)(uint64_t)n * s2 - (u128_t)(uint64_t)s.s1 * (uint64_t)s.s1;
+    uint64_t den = (uint64_t)n * (uint64_t)(n - 1);  // n < 2^31 (validated)
+    v = num / den;
+  }
+  uint64_t nsh = (uint64_t)n << 32;
+  u128_t a2 = ((u128_t)2 * v * lq) / nsh;
+  uint64_t t2 = isqrt_u64((uint64_t)a2);
+  u128_t t3 = ((u128_t)3 * (uint64_t)b_us * lq) / nsh;
+  return mu + (int64_t)t2 + (int64_t)t3;
+}
+
+// 𝓑(r,f) then CalcTTL offset, readings R7/R8.
+__device__ __forceinline__ int64_t calc_ttl(const Stat& g, const Stat& f,
+                                            const ct_estimator_params& e, int64_t n_done,
+                                            int64_t turns_done) {
+  int64_t B;
+  if (g.n < e.n_min) B = e.t_default_us;
+  else if (f.n >= e.n_min) B = bernstein(f, e.lq, e.b_us);
+  else B = bernstein(g, e.lq, e.b_us);
+  if (B < 1) B = 1;
+  const uint64_t T2 = (uint64_t)e.t_default_us * (uint64_t)e.t_default_us;
+  u128_t ttl;
+  if (n_done > 0) {
+    u128_t num = (u128_t)T2 * ((u128_t)(uint64_t)n_done * (uint64_t)e.a_den +
+                               (u128_t)(uint64_t)e.a_num * (uint64_t)turns_done);
+    u128_t den = (u128_t)(uint64_t)B * (uint64_t)n_done * (uint64_t)e.a_den;
+    ttl = num / den;
+  } else {
+    ttl = (u128_t)T2 / (uint64_t)B;
+  }
+  if (e.ttl_max_us > 0 && ttl > (u128_t)(uint64_t)e.ttl_max_us) ttl = (uint64_t)e.ttl_max_us;
+  return (int64_t)(uint64_t)ttl;
+}
+
+// §4.5 simplified decision, reading R9.
+__device__ __forceinline__ int64_t simplified_ttl(const Stat& g, const Stat& f,
+                                                  const ct_estimator_params& e, int64_t t_pin,
+                                                  int64_t t_thresh) {
+  if (t_thresh == CT_ALWAYS) return t_pin;
+  int64_t mu;
+  if (f.n >= e.n_min) mu = f.s1 / f.n;
+  else if (g.n >= 1) mu = g.s1 / g.n;
+  else return 0;
+  return mu < t_thresh ? t_pin : 0;
+}
+
+}  // namespace ct

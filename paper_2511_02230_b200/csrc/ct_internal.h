@@ -1,0 +1,76 @@
+// ct_internal.h — launch interfaces between libcontinuum's host runtime and its kernels.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "continuum.h"
+
+namespace ct {
+
+struct ReplayArgs {
+  const ct_program* progs;
+  const int4* turns;
+  int P, F;
+  const int64_t* gap;
+  const int64_t* kv;
+  const ct_policy* pols;
+  int n_rate, n_kv, n_pol;
+  ct_estimator_params est;
+  const int64_t* fitted;
+  int J;
+  ct_engine_params eng;
+  int64_t r_begin, r_end;
+  ct_replica_summary* out;
+  int64_t* jct;
+  unsigned long long* counter;
+  int smem_per_warp;
+};
+
+// Bytes of shared memory one replica (one warp) needs for `ns` slots per lane and F tools.
+int replay_smem_per_warp(int ns, int F);
+// Launch the persistent replay kernel; returns the cudaError of the launch.
+cudaError_t launch_replay(const ReplayArgs& a, int ns, int warps_per_block, int grid,
+                          cudaStream_t s);
+// Max resident blocks per SM for the given configuration.
+int replay_occupancy(int ns, int warps_per_block, int smem_per_block);
+
+struct FitChunk {  // one CTA work item: samples [begin, end) of tool `tool`
+  int64_t begin, end;
+  int32_t tool, pad;
+};
+
+struct FitArgs {
+  const int32_t* dur;
+  const FitChunk* chunks;
+  int64_t n_chunks;
+  int F, K;
+  int64_t step;          // grid step (µs)
+  uint64_t step_magic;   // ceil(2^40 / step) for the bucket quotient
+  int64_t b_us;
+  unsigned long long* hcnt;  // [(F) * (K+1)] bucket counts
+  unsigned long long* hsum;  // [(F) * (K+1)] bucket sums (buckets < K)
+  unsigned long long* stat;  // [F * 6]: n, s1, s2 limbs (4 x 32-bit, each in a u64 slot)
+};
+
+struct ScanArgs {
+  const unsigned long long* hcnt;
+  const unsigned long long* hsum;
+  const unsigned long long* stat;
+  int F, K, J;
+  ct_cost_params cost;
+  ct_estimator_params est;
+  int64_t* ttl_argmax;
+  int64_t* ttl_paper;
+  int64_t* stats_out;
+};
+
+cudaError_t launch_fit_hist(const FitArgs& a, int grid, cudaStream_t s);
+cudaError_t launch_fit_scan(const ScanArgs& a, cudaStream_t s);
+int fit_hist_threads();
+int fit_hist_smem(int K);
+int fit_hist_occupancy(int smem);  // resident CTAs per SM
+
+cudaError_t launch_jct_stats(const ct_replica_summary* s, int64_t n, int32_t n_cells,
+                             ct_cell_stats* out, cudaStream_t st);
+
+}  // namespace ct

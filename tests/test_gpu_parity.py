@@ -1,0 +1,221 @@
+"""GPU parity: libcontinuum (through the C ABI) vs the CPU oracle, byte for byte.
+
+Every replica's 128-B summary and every per-program JCT must be identical (integer
+arithmetic end to end).  Sizes span several warps/CTAs, every
+slots-per-lane variant (P <= 32, 64, 128, 256), ragged tails, edge cases, and — in the
+launch configuration bench.py times — sampled replicas of the full BASELINE configs.
+"""
+import random
+
+import numpy as np
+import pytest
+import torch
+
+from ctgen import configs as cf
+from ctgen import traces
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    from paper_2511_02230_b200 import build
+    build.build()
+    import paper_2511_02230_b200 as ct
+    return ct.Context(0)
+
+
+def gpu_run(ctx, tr, sw, eng, rb=0, re=None, jct=True):
+    import paper_2511_02230_b200 as ct
+    dt = ct.DeviceTrace(tr)
+    s, j = ct.ct_simulate_batch(ctx, dt, sw, eng, rb, re, jct=jct)
+    torch.cuda.synchronize()
+    return s.cpu().numpy(), (j.cpu().numpy() if j is not None else None)
+
+
+def assert_same(gs, gj, os_, oj):
+    bad = np.nonzero(np.any(gs != os_, axis=1))[0]
+    assert bad.size == 0, "summary mismatch at replicas %s:\nGPU %s\nORA %s" % (
+        bad[:5], gs[bad[:2]], os_[bad[:2]])
+    if gj is not None:
+        badj = np.nonzero(np.any(gj != oj, axis=1))[0]
+        assert badj.size == 0, "jct mismatch at %s" % badj[:5]
+
+
+UNIT = cf.Engine(c0_ps=10**6, c_pf_ps=10**6, c_kv_ps=0, c_h2d_ps=5 * 10**5, bs=1, max_batch=256,
+                 dram_blocks=1000)
+
+
+def test_goldens(ctx):
+    G1 = traces.tiny([(0, [(10, 2, 0, 5), (3, 1, -1, 0)])])
+    sw = cf.Sweep(1, [1 << 20], [100], [cf.ttl_grid(5), cf.ttl_grid(4), cf.PROG_FCFS, cf.VLLM,
+                                        cf.VLLM_LMCACHE])
+    gs, gj = gpu_run(ctx, G1, sw, UNIT)
+    assert list(gj[:, 0]) == [21, 33, 33, 33, 27]
+    os_, oj = O.simulate(G1, sw, UNIT)
+    assert_same(gs, gj, os_, oj)
+    G2 = traces.tiny([(0, [(10, 2, 0, 20), (2, 1, -1, 0)]), (1, [(10, 5, -1, 0)])])
+    sw = cf.Sweep(1, [1 << 20], [30, 20], [cf.ttl_grid(100), cf.PROG_FCFS])
+    gs, gj = gpu_run(ctx, G2, sw, UNIT)
+    assert [list(x) for x in gj] == [[45, 25], [57, 25], [47, 26], [47, 26]]
+
+
+def random_tiny_set(rng, n_seeds, P=3, n_tools=2):
+    progs = []
+    for _ in range(n_seeds):
+        arr = sorted(rng.randint(0, 20) for _ in range(P))
+        for p in range(P):
+            T = rng.randint(1, 3)
+            ts = [(rng.randint(0, 6), rng.randint(1, 4), rng.randint(0, n_tools - 1), rng.randint(1, 30))
+                  for _ in range(T)]
+            ts[-1] = (ts[-1][0], ts[-1][1], -1, 0)
+            progs.append((arr[p], ts))
+    tr = traces.tiny(progs, n_tools=n_tools)
+    tr.n_seeds, tr.n_programs = n_seeds, P
+    return tr
+
+
+def random_policies(rng, n):
+    out = []
+    for _ in range(n):
+        out.append(cf.Policy(priority=rng.choice([0, 0, 1]),
+                             pause=rng.choice([0, 1, 1, 2, 3]), dram=rng.choice([0, 1]),
+                             flags=rng.choice([0, 0, 1, 2, 3]), t_pin_us=rng.randint(0, 30),
+                             t_thresh_us=rng.choice([cf.ALWAYS, rng.randint(1, 30)])))
+    return out
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_random_tiny_instances(ctx, seed):
+    rng = random.Random(1000 + seed)
+    tr = random_tiny_set(rng, 300)
+    eng = cf.Engine(c0_ps=rng.randint(1, 3 * 10**6), c_pf_ps=rng.choice([0, 5 * 10**5, 10**6]),
+                    c_kv_ps=rng.choice([0, 10**4, 2 * 10**5]), c_h2d_ps=rng.randint(1, 2 * 10**6),
+                    bs=rng.choice([1, 2, 4]), max_batch=rng.choice([1, 2, 256]),
+                    dram_blocks=rng.randint(0, 12), max_iters=rng.choice([10**6, 40]))
+    est = cf.Estimator(b_us=rng.choice([5, 40]), t_def_us=rng.randint(1, 40), n_min=rng.randint(1, 3),
+                       a_num=rng.randint(0, 2), a_den=rng.choice([1, 3]), ttl_max_us=rng.choice([0, 25]))
+    fitted = np.array([[rng.randint(0, 30) for _ in range(3)] for _ in range(2)], np.int64)
+    sw = cf.Sweep(300, [1 << 20, 3 << 19], [6, 11, 18], random_policies(rng, 6), est, fitted)
+    gs, gj = gpu_run(ctx, tr, sw, eng)
+    os_, oj = O.simulate(tr, sw, eng, n_threads=8)
+    assert_same(gs, gj, os_, oj)
+
+
+ALL_POLICIES = [cf.VLLM, cf.VLLM_LMCACHE, cf.PROG_FCFS, cf.CONTINUUM, cf.ttl_grid(500_000),
+                cf.ttl_grid(30_000_000), cf.simplified(5_000_000, 1_000_000),
+                cf.Policy(cf.PRIO_PROG_FCFS, cf.PAUSE_PAPER, dram=1),
+                cf.Policy(cf.PRIO_PROG_FCFS, cf.PAUSE_PAPER, flags=cf.FLAG_STEP_EXPIRY),
+                cf.Policy(cf.PRIO_PROG_FCFS, cf.PAUSE_FIXED, flags=cf.FLAG_VICTIMS_ANY,
+                          t_pin_us=20_000_000),
+                cf.Policy(cf.PRIO_REQ_FCFS, cf.PAUSE_FITTED, dram=1),
+                cf.Policy(cf.PRIO_PROG_FCFS, cf.PAUSE_FITTED, flags=cf.FLAG_STEP_EXPIRY)]
+
+
+@pytest.mark.parametrize("P", [1, 7, 32, 33, 64, 100, 128, 200, 256])
+def test_workloads_all_policies(ctx, P):
+    n_seeds = 6 if P <= 64 else 2
+    tr = traces.generate(n_seeds, P, mix="mix", ctx_cap=8192, stream=P)
+    fitted = np.tile(np.array([[0, 200_000, 3_000_000, 60_000_000]], np.int64), (tr.n_tools, 1))
+    eng = cf.Engine(**{**cf.ENGINE_8B.__dict__, "dram_blocks": 40 * P})
+    sw = cf.Sweep(n_seeds, [200_000, 3_000_000], [600, 20 * P + 600], ALL_POLICIES, fitted=fitted)
+    gs, gj = gpu_run(ctx, tr, sw, eng)
+    os_, oj = O.simulate(tr, sw, eng, n_threads=8)
+    assert_same(gs, gj, os_, oj)
+    assert np.mean((gs[:, 0] & 0xFFFFFFFF) == 0) > 0.8
+
+
+def test_sharding_and_host_path(ctx):
+    import paper_2511_02230_b200 as ct
+    tr = traces.generate(8, 32, n_bfcl=16, mix="mix", ctx_cap=8192 * 16, stream=5)
+    sw = cf.Sweep(8, cf.rate_axis(4), [8192], [cf.ttl_grid(t) for t in cf.ttl_axis(8)])
+    full, fj = gpu_run(ctx, tr, sw, cf.ENGINE_8B)
+    R = sw.n_replicas
+    parts = [gpu_run(ctx, tr, sw, cf.ENGINE_8B, a, b) for a, b in [(0, 37), (37, 38), (38, R)]]
+    assert np.array_equal(full, np.concatenate([p[0] for p in parts]))
+    assert np.array_equal(fj, np.concatenate([p[1] for p in parts]))
+    hs = torch.empty((R, 16), dtype=torch.int64).pin_memory()
+    hj = torch.empty((R, 32), dtype=torch.int64).pin_memory()
+    ct.ct_simulate_batch_host(ctx, tr, sw, cf.ENGINE_8B, 0, R, hs, hj)
+    assert np.array_equal(hs.numpy(), full) and np.array_equal(hj.numpy(), fj)
+    # empty range is a no-op
+    s, _ = ct.ct_simulate_batch(ctx, ct.DeviceTrace(tr), sw, cf.ENGINE_8B, 5, 5, jct=False)
+    assert s.shape[0] == 0
+
+
+def test_edge_statuses(ctx):
+    tr = traces.tiny([(0, [(100, 1, -1, 0)]), (5, [(1, 50, -1, 0)])])
+    sw = cf.Sweep(1, [1 << 20], [50, 200], [cf.PROG_FCFS])
+    eng = cf.Engine(**{**UNIT.__dict__, "max_iters": 20})
+    gs, gj = gpu_run(ctx, tr, sw, eng)
+    os_, oj = O.simulate(tr, sw, eng)
+    assert_same(gs, gj, os_, oj)
+    assert list(gs[:, 0] & 0xFFFFFFFF) == [cf.STATUS_UNSCHEDULABLE, cf.STATUS_EVENT_BUDGET]
+
+
+def test_invalid_arguments_rejected(ctx):
+    import paper_2511_02230_b200 as ct
+    from paper_2511_02230_b200 import _lib
+    tr = traces.tiny([(0, [(1, 1, -1, 0)])])
+    sw = cf.Sweep(1, [1 << 20], [10], [cf.Policy(pause=cf.PAUSE_FITTED)])  # FITTED without table
+    with pytest.raises(_lib.CtError):
+        ct.ct_simulate_batch(ctx, ct.DeviceTrace(tr), sw, UNIT)
+    bad = cf.Engine(**{**UNIT.__dict__, "c0_ps": 0})
+    with pytest.raises(_lib.CtError):
+        ct.ct_simulate_batch(ctx, ct.DeviceTrace(tr), cf.Sweep(1, [1], [10], [cf.PROG_FCFS]), bad)
+
+
+# ---- TTL fit ----------------------------------------------------------------------------------
+def fit_both(ctx, dur, off, K, step, J, c_pf, c_pin, est, avg=(0, 0), a=(1, 10)):
+    import paper_2511_02230_b200 as ct
+    ctxj = [int(500 * 2**j) % 200_000 + 16 for j in range(J)]
+    wj = [j + 1 for j in range(J)]
+    cp = ct.cost_params(c_pf, c_pin, 16, a[0], a[1], step, K, ctxj, wj, avg)
+    d = torch.from_numpy(np.ascontiguousarray(dur, np.int32)).cuda()
+    ga, gp, gst = ct.ct_fit_ttl(ctx, d, off, cp, est)
+    torch.cuda.synchronize()
+    oa, op, ost = O.fit(dur, off, [c_pf, c_pin, 16, a[0], a[1], step, K, J], ctxj, wj,
+                        est.as_array(), avg)
+    return (ga.cpu().numpy(), gp.cpu().numpy(), gst.cpu().numpy()), (oa, op, ost)
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_fit_parity_random(ctx, seed):
+    rng = np.random.default_rng(seed)
+    F = int(rng.integers(1, 12))
+    sizes = rng.integers(0, 3000, size=F)
+    sizes[rng.integers(0, F)] = int(rng.integers(0, 5))  # a tool below N
+    off = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+    n = int(off[-1])
+    dur = np.clip(rng.lognormal(np.log(rng.uniform(5e4, 5e6)), rng.uniform(0.1, 1.5), n), 0, 2**31 - 1).astype(np.int32)
+    dur[rng.random(n) < 0.05] = 0
+    K = int(rng.choice([1, 2, 17, 64, 256, 1024]))
+    step = int(rng.choice([1, 999, 50_000, 250_000]))
+    J = int(rng.integers(1, 9))
+    est = cf.Estimator(n_min=int(rng.integers(1, 8)))
+    g, o = fit_both(ctx, dur, off, K, step, J, 13_400_000, int(rng.integers(0, 3000)), est,
+                    avg=(int(rng.integers(0, 500)), int(rng.integers(0, 50))))
+    for x, y in zip(g, o):
+        assert np.array_equal(x, y)
+
+
+def test_fit_point_mass_and_alignment(ctx):
+    # misaligned CSR segments (head/tail paths), point mass (cd-like) and duplicates
+    sizes = [1, 3, 5, 7, 4096 + 3, 70_001]
+    off = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+    dur = np.full(int(off[-1]), 100_000, np.int32)
+    dur[: off[4]] = np.arange(int(off[4])) * 7919 % 3_000_000
+    g, o = fit_both(ctx, dur, off, 256, 50_000, 4, 13_400_000, 50, cf.Estimator())
+    for x, y in zip(g, o):
+        assert np.array_equal(x, y)
+
+
+def test_jct_stats_parity(ctx):
+    import paper_2511_02230_b200 as ct
+    tr = traces.generate(16, 32, n_bfcl=16, mix="mix", ctx_cap=8192 * 16, stream=9)
+    sw = cf.Sweep(16, cf.rate_axis(3), [8192, 2000], [cf.ttl_grid(t) for t in cf.ttl_axis(4)])
+    s, _ = ct.ct_simulate_batch(ctx, ct.DeviceTrace(tr), sw, cf.ENGINE_8B, jct=False)
+    cs = ct.ct_jct_stats(ctx, s, sw.n_cells).cpu().numpy()
+    ocs = O.jct_stats(s.cpu().numpy(), sw.n_cells)
+    assert np.array_equal(cs, ocs)
