@@ -32,6 +32,7 @@ struct ct_ctx {
   void* h_jct = nullptr;
   size_t h_jct_cap = 0;
   ct_launch_info last{};
+  int fit_occ = 0, fit_occ_smem = -1;
 };
 
 namespace {
@@ -299,42 +300,59 @@ int ct_fit_ttl(ct_ctx* c, const ct_samples* sm, const ct_cost_params* cp,
     if (V > lim / (n + 1) || C > lim / ((n + 1) * (((i128)1 << 31) + tau_max + 1)))
       return fail(CT_EINVAL, "cost products could overflow 128-bit arithmetic");
   }
-  if (n >= ((i128)1 << 40)) return fail(CT_EINVAL, "too many samples");
+  if (n >= ((i128)1 << 32)) return fail(CT_EINVAL, "too many samples (n >= 2^32)");
+  if (n * (i128)est->b_us * est->b_us >= ((i128)1 << 95))
+    return fail(CT_EINVAL, "n * b^2 >= 2^95: sum of squares could overflow");
   cudaStream_t s = (cudaStream_t)stream;
-  // chunk plan: <= CH samples per CTA work item so a warp's packed bins cannot overflow
-  const int64_t tmax = std::max<int64_t>((int64_t)tau_max, 1);
-  int64_t CH = std::min<int64_t>(1ll << 17, ((1ll << 44) - 1) / tmax);
-  CH = std::min<int64_t>(CH, (1ll << 20) - 1);
-  if (CH < 256) return fail(CT_EINVAL, "grid step too large for the packed histogram");
-  std::vector<ct::FitChunk> chunks;
-  for (int f = 0; f < F; ++f)
-    for (int64_t b = sm->tool_off[f]; b < sm->tool_off[f + 1]; b += CH)
-      chunks.push_back({b, std::min(b + CH, sm->tool_off[f + 1]), f, 0});
-  const size_t hbytes = 8 * (size_t)F * (K + 1);
-  const size_t fbytes = 2 * hbytes + 8 * 6 * (size_t)F;
+  // chunk plan: <= CH samples per CTA work item so that a warp's 32-bit bins (count, sum of
+  // remainders < step) and a thread's 64-bit sum of squares cannot overflow
+  if (cp->grid_step_us >= (1ll << 31) || est->b_us >= (1ll << 31))
+    return fail(CT_EINVAL, "grid_step_us and b_us must be < 2^31");
+  // per warp chunk CH: a replica (32/R lanes) sees <= CH/R + 64 samples (32-bit remainder sums
+  // < 2^32, 16-bit packed counts < 2^16) and a lane <= CH/32 + 2 (64-bit sum of squares < 2^64)
+  const int R = ct::fit_hist_repl();
+  int64_t CH = 1ll << 16;
+  while (CH > 256 && (CH / R + 64) * (uint64_t)cp->grid_step_us >= (1ull << 32)) CH >>= 1;
+  while (CH > 256 && CH / R + 64 >= (1 << 16)) CH >>= 1;
+  {
+    const unsigned __int128 b2 = (unsigned __int128)est->b_us * est->b_us;
+    while (CH > 256 && (unsigned __int128)(CH / 32 + 8) * b2 >= ((unsigned __int128)1 << 64)) CH >>= 1;
+  }
+  if (CH < 256) return fail(CT_EINVAL, "grid step / b too large for the histogram pass");
+  // rows 0..F-1 per tool, row F pooled (filled by fit_hist)
+  const size_t hbytes = 8 * (size_t)(F + 1) * (K + 1);
+  const size_t fbytes = 2 * hbytes + 8 * 6 * (size_t)(F + 1);
   int rc = ensure(&c->fit, &c->fit_cap, fbytes);
   if (rc) return rc;
   CT_CUDA(cudaMemsetAsync(c->fit, 0, fbytes, s));
   int launches = 0;
   ct::FitArgs fa;
+  std::memset(&fa, 0, sizeof fa);
   fa.dur = sm->dur_us;
   fa.F = F;
   fa.K = K;
+  fa.ch = CH;
+  for (int f = 0; f <= F; ++f) {
+    fa.tool_off[f] = sm->tool_off[f];
+    fa.chunk_off[f] = f == 0 ? 0 : fa.chunk_off[f - 1] + (sm->tool_off[f] - sm->tool_off[f - 1] + CH - 1) / CH;
+  }
+  fa.n_chunks = fa.chunk_off[F];
   fa.step = cp->grid_step_us;
-  fa.step_magic = (uint64_t)(((((unsigned __int128)1) << 32) + cp->grid_step_us - 1) / cp->grid_step_us);
+  // M = ceil(2^64 / step) < 2^63 for step >= 2; step == 1 runs the identity instantiation
+  fa.step_magic = cp->grid_step_us == 1 ? 0 : (uint64_t)((((unsigned __int128)1 << 64) + cp->grid_step_us - 1) / cp->grid_step_us);
   fa.b_us = est->b_us;
   fa.hcnt = (unsigned long long*)c->fit;
-  fa.hsum = fa.hcnt + (size_t)F * (K + 1);
-  fa.stat = fa.hsum + (size_t)F * (K + 1);
-  fa.n_chunks = (int64_t)chunks.size();
-  if (!chunks.empty()) {
-    if ((rc = ensure(&c->chunks, &c->chunks_cap, sizeof(ct::FitChunk) * chunks.size()))) return rc;
-    CT_CUDA(cudaMemcpyAsync(c->chunks, chunks.data(), sizeof(ct::FitChunk) * chunks.size(),
-                            cudaMemcpyHostToDevice, s));
-    fa.chunks = (const ct::FitChunk*)c->chunks;
-    const int occ = ct::fit_hist_occupancy(ct::fit_hist_smem(K));
-    if (occ < 1) return fail(CT_ECUDA, "fit_hist kernel cannot be resident");
-    const int grid = (int)std::min<int64_t>((int64_t)c->sm_count * occ, fa.n_chunks);
+  fa.hsum = fa.hcnt + (size_t)(F + 1) * (K + 1);
+  fa.stat = fa.hsum + (size_t)(F + 1) * (K + 1);
+  if (fa.n_chunks > 0) {
+    if (c->fit_occ_smem != ct::fit_hist_smem(K)) {
+      c->fit_occ = ct::fit_hist_occupancy(ct::fit_hist_smem(K));
+      c->fit_occ_smem = ct::fit_hist_smem(K);
+    }
+    if (c->fit_occ < 1) return fail(CT_ECUDA, "fit_hist kernel cannot be resident");
+    const int wpb = ct::fit_hist_threads() / 32;  // every warp takes its own chunks
+    const int grid = (int)std::min<int64_t>((int64_t)c->sm_count * c->fit_occ,
+                                            (fa.n_chunks + wpb - 1) / wpb);
     cudaError_t e = ct::launch_fit_hist(fa, grid, s);
     if (e != cudaSuccess) return cuda_fail(e, "fit_hist launch");
     ++launches;

@@ -34,22 +34,19 @@ cudaError_t launch_replay(const ReplayArgs& a, int ns, int warps_per_block, int 
 // Max resident blocks per SM for the given configuration.
 int replay_occupancy(int ns, int warps_per_block, int smem_per_block);
 
-struct FitChunk {  // one CTA work item: samples [begin, end) of tool `tool`
-  int64_t begin, end;
-  int32_t tool, pad;
-};
-
 struct FitArgs {
   const int32_t* dur;
-  const FitChunk* chunks;
-  int64_t n_chunks;
+  int64_t n_chunks;              // work items: chunks of <= ch samples inside one tool segment
+  int64_t ch;
+  int64_t tool_off[CT_MAX_TOOLS + 1];
+  int64_t chunk_off[CT_MAX_TOOLS + 1];  // first chunk index of each tool
   int F, K;
   int64_t step;          // grid step (µs)
   uint64_t step_magic;   // ceil(2^40 / step) for the bucket quotient
   int64_t b_us;
-  unsigned long long* hcnt;  // [(F) * (K+1)] bucket counts
-  unsigned long long* hsum;  // [(F) * (K+1)] bucket sums (buckets < K)
-  unsigned long long* stat;  // [F * 6]: n, s1, s2 limbs (4 x 32-bit, each in a u64 slot)
+  unsigned long long* hcnt;  // [(F+1) * (K+1)] bucket counts, row F pooled over tools
+  unsigned long long* hsum;  // [(F+1) * (K+1)] bucket sums (buckets < K)
+  unsigned long long* stat;  // [(F+1) * 6]: n, s1, s2 limbs (32-bit limb sums in u64 slots)
 };
 
 struct ScanArgs {
@@ -67,6 +64,7 @@ struct ScanArgs {
 cudaError_t launch_fit_hist(const FitArgs& a, int grid, cudaStream_t s);
 cudaError_t launch_fit_scan(const ScanArgs& a, cudaStream_t s);
 int fit_hist_threads();
+int fit_hist_repl();  // histogram replicas per warp of the selected variant
 int fit_hist_smem(int K);
 int fit_hist_occupancy(int smem);  // resident CTAs per SM
 

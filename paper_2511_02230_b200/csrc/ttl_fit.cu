@@ -1,156 +1,230 @@
 // ttl_fit.cu — the TTL fit: one HBM pass over duration samples.
 //
-// Kernel 1 (fit_hist): persistent CTAs stream tool-grouped (CSR) int32 samples with 16-B
-// vector loads.  Every sample updates one packed u64 bin (count << 44 | sum) of its warp's
-// private shared-memory histogram over the TTL grid buckets k = min(ceil(d / step), K), and the
-// thread's register statistics (n, sum t~, sum t~^2 as 128-bit) of t~ = min(d, b) for the paper
-// mode (reading R5).  At the end of a chunk the warp histograms are merged and
-// flushed with integer atomics (order independent, hence deterministic).
-// Kernel 2 (fit_scan): one warp per (tool row, turn bucket j): warp prefix scan of the bucket
-// counts and sums, n U(k) in 128-bit integers (extension C-4), warp argmax with the smallest k on
-// ties; the pooled row is the sum of the tool rows; tools with n_f < N take the pooled result;
-// the j = 0 warp also evaluates CalcTTL on the row's statistics.
+// Kernel 1 (fit_hist): persistent warps, each streaming its own chunks of tool-grouped (CSR)
+// int32 samples with 16-B streaming loads (8 in flight per lane).  Every sample lands in the
+// warp's lane-pair-replicated shared-memory histogram over the TTL grid buckets
+// k = min(ceil(d / step), K) as (count, sum of k step - d) with fire-and-forget 32-bit shared
+// reductions (conflict-free up to 2-way), and in the thread's 64-bit register statistics
+// (sum t~, sum t~^2) of t~ = min(d, b) for the paper mode (reading R5).
+// After each chunk the warp merges its replicas and flushes with integer atomics (order
+// independent, hence deterministic).
+// Kernel 2 (fit_scan): one CTA per tool row: block prefix scan of the bucket counts and sums in
+// shared memory, then per turn bucket j n U(k) in 128-bit integers (extension C-4) and a warp
+// argmax with the smallest k on ties; the pooled row sums the tool rows; tools with n_f < N take
+// the pooled result; thread 0 also evaluates CalcTTL on the row's statistics.
+#include <cstdlib>
+
 #include "ct_device.cuh"
 #include "ct_internal.h"
 
 namespace ct {
 
-constexpr int FIT_THREADS = 256;
-constexpr int FIT_WARPS = FIT_THREADS / 32;
-constexpr uint64_t CNT_ONE = 1ull << 44;
-constexpr uint64_t SUM_MASK = CNT_ONE - 1;
+constexpr int FIT_WARPS = 2;                 // warps per CTA; every warp is independent
+constexpr int FIT_THREADS = 32 * FIT_WARPS;
 
-int fit_hist_threads() { return FIT_THREADS; }
-int fit_hist_smem(int K) { return FIT_WARPS * (K + 1) * 8; }
-
-struct Acc {
-  uint64_t n, s1, lo, hi;
+// Histogram variants (replicas per warp, 16-bit packed counts).  A replica is shared by 32/REPL
+// adjacent lanes; layout [bucket][replica] spreads one bucket over REPL banks.
+struct FitVariant {
+  int repl;
+  bool pack;
+  int u;  // int4 loads per lane per double-buffer half
 };
+static const FitVariant kVariants[] = {{16, false, 16}, {16, true, 16}, {8, false, 8},
+                                       {8, true, 8},    {32, false, 16}, {16, true, 8},
+                                       {8, true, 4}};
+static int g_variant = -1;  // default 2 (measured best on B200)
 
-__device__ __forceinline__ void sample(uint64_t* __restrict__ h, int32_t d, int K, int64_t step,
-                                       uint64_t magic, int64_t b_us, Acc& acc) {
-  int b;
-  uint64_t inc;
-  if (d <= 0) {
-    b = 0;
-    inc = CNT_ONE;
-  } else {
-    uint64_t x = (uint64_t)(d - 1);
-    uint64_t q = (x * magic) >> 32;
-    if (q * (uint64_t)step > x) --q;
-    b = q + 1 < (uint64_t)K ? (int)(q + 1) : K;
-    inc = CNT_ONE | (b < K ? (uint64_t)d : 0ull);
+static int variant() {
+  if (g_variant < 0) {
+    const char* e = getenv("CT_FIT_VARIANT");
+    int v = e ? atoi(e) : 2;
+    g_variant = (v >= 0 && v < (int)(sizeof kVariants / sizeof kVariants[0])) ? v : 2;
   }
-  atomicAdd((unsigned long long*)&h[b], (unsigned long long)inc);
-  const uint64_t t = (uint64_t)min((int64_t)d, b_us);
-  acc.n += 1;
-  acc.s1 += t;
-  const uint64_t t2 = t * t;
-  acc.lo += t2;
-  acc.hi += (acc.lo < t2);
+  return g_variant;
 }
 
+int fit_hist_threads() { return FIT_THREADS; }
+int fit_hist_repl() { return kVariants[variant()].repl; }
+static int smem_words(int K, const FitVariant& fv) {
+  return (K + 1) * (fv.repl + (fv.pack ? fv.repl / 2 : fv.repl));
+}
+int fit_hist_smem(int K) { return FIT_WARPS * 4 * smem_words(K, kVariants[variant()]); }
+
+__device__ __forceinline__ void red_shared(uint32_t addr, uint32_t v) {
+  asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ void mad_wide(uint64_t& acc, uint32_t a, uint32_t b) {
+  asm("mad.wide.u32 %0, %1, %2, %0;" : "+l"(acc) : "r"(a), "r"(b));
+}
+
+struct Lane {
+  uint32_t rs_base, cnt_base, cnt_inc;  // shared-window addresses of this lane's replica
+  uint32_t K, step, mhi, mlo, xoff, b_us;
+};
+
+// One sample d of the lane.  Bucket k = min(ceil(d / step), K) (a hit for tau_k iff d <= k step);
+// the bins keep the count and the sum of r = k step - d in [0, step), so sum_k d =
+// k step count_k - sum_k r is exact with 32-bit bins.  ceil(d / step) = floor(x / step) with
+// x = d + step - 1 < 2^32 is the high word of x * M, M = ceil(2^64 / step) (error < 2^-32 cannot
+// cross an integer for 32-bit x): one IMAD.HI + one IMAD.WIDE; step = 1 is the identity.
+template <bool IDENT, int REPL, bool PACK>
+__device__ __forceinline__ void sample(const Lane& L, int32_t d, uint64_t& s1, uint64_t& s2) {
+  const uint32_t x = (uint32_t)d + L.xoff;
+  uint32_t q;
+  if (IDENT) {
+    q = x;
+  } else {
+    uint64_t p = __umulhi(x, L.mlo);
+    mad_wide(p, x, L.mhi);  // p = x * mhi + hi32(x * mlo)
+    q = (uint32_t)(p >> 32);
+  }
+  const uint32_t b = min(q, L.K);
+  const uint32_t r = b * L.step - (uint32_t)d;  // in [0, step) for b < K; ignored for b = K
+  red_shared(L.cnt_base + b * ((PACK ? REPL / 2 : REPL) * 4), L.cnt_inc);
+  red_shared(L.rs_base + b * (REPL * 4), r);
+  const uint32_t t = min((uint32_t)d, L.b_us);
+  s1 += t;
+  mad_wide(s2, t, t);
+}
+
+template <bool IDENT, int REPL, bool PACK, int U>
 __global__ void __launch_bounds__(FIT_THREADS) fit_hist_kernel(FitArgs a) {
-  extern __shared__ __align__(16) unsigned long long hsm[];
+  extern __shared__ __align__(16) uint32_t hsm[];
+  constexpr int CW = PACK ? REPL / 2 : REPL;  // count words per bucket
   const int K = a.K;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  uint64_t* h = (uint64_t*)hsm + warp * (K + 1);
-  __shared__ unsigned long long red[FIT_WARPS][6];
+  const int words = (K + 1) * (REPL + CW);
+  uint32_t* rs = hsm + warp * words;
+  uint32_t* cnt = rs + (K + 1) * REPL;
+  const int rep = lane / (32 / REPL);
+  Lane L;
+  L.rs_base = (uint32_t)__cvta_generic_to_shared(rs) + 4 * rep;
+  L.cnt_base = (uint32_t)__cvta_generic_to_shared(cnt) + 4 * (PACK ? rep >> 1 : rep);
+  L.cnt_inc = PACK ? (1u << (16 * (rep & 1))) : 1u;
+  L.K = (uint32_t)K;
+  L.step = (uint32_t)a.step;
+  L.mhi = (uint32_t)(a.step_magic >> 32);
+  L.mlo = (uint32_t)a.step_magic;
+  L.xoff = L.step - 1;
+  L.b_us = (uint32_t)a.b_us;
+  const int64_t gw = (int64_t)blockIdx.x * FIT_WARPS + warp, nw = (int64_t)gridDim.x * FIT_WARPS;
 
-  for (int64_t c = blockIdx.x; c < a.n_chunks; c += gridDim.x) {
-    const FitChunk ch = a.chunks[c];
-    for (int i = threadIdx.x; i < FIT_WARPS * (K + 1); i += FIT_THREADS) hsm[i] = 0;
-    __syncthreads();
-    Acc acc = {0, 0, 0, 0};
-    // scalar head up to 16-B alignment, int4 body, scalar tail
-    int64_t beg = ch.begin, end = ch.end;
+  for (int64_t c = gw; c < a.n_chunks; c += nw) {
+    int tool = 0;
+    while (a.chunk_off[tool + 1] <= c) ++tool;
+    const int64_t beg = a.tool_off[tool] + (c - a.chunk_off[tool]) * a.ch;
+    const int64_t end = min(beg + a.ch, a.tool_off[tool + 1]);
+    for (int i = lane; i < words; i += 32) rs[i] = 0;
+    __syncwarp();
+    uint64_t s1 = 0, s2 = 0;
     int64_t va = (beg + 3) & ~(int64_t)3;
     if (va > end) va = end;
-    int64_t vb = va + ((end - va) & ~(int64_t)3);
-    for (int64_t i = beg + threadIdx.x; i < va; i += FIT_THREADS)
-      sample(h, __ldg(&a.dur[i]), K, a.step, a.step_magic, a.b_us, acc);
+    const int64_t vb = va + ((end - va) & ~(int64_t)3);
+    // scalar head and tail (< 4 samples each)
+    if (beg + lane < va) sample<IDENT, REPL, PACK>(L, __ldg(&a.dur[beg + lane]), s1, s2);
+    if (vb + lane < end) sample<IDENT, REPL, PACK>(L, __ldg(&a.dur[vb + lane]), s1, s2);
     const int4* v = (const int4*)(a.dur + va);
     const int64_t nv = (vb - va) >> 2;
-    int64_t i = threadIdx.x;
-    for (; i + 3 * FIT_THREADS < nv; i += 4 * FIT_THREADS) {
-      int4 x0 = __ldcs(v + i);
-      int4 x1 = __ldcs(v + i + FIT_THREADS);
-      int4 x2 = __ldcs(v + i + 2 * FIT_THREADS);
-      int4 x3 = __ldcs(v + i + 3 * FIT_THREADS);
-      int4 xs[4] = {x0, x1, x2, x3};
+    // register double buffering: U int4 per lane in flight while the previous U are binned
+    int64_t i = lane;
+    int4 A[U], B[U];
+    bool have_a = i + (U - 1) * 32 < nv;
+    if (have_a) {
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        sample(h, xs[u].x, K, a.step, a.step_magic, a.b_us, acc);
-        sample(h, xs[u].y, K, a.step, a.step_magic, a.b_us, acc);
-        sample(h, xs[u].z, K, a.step, a.step_magic, a.b_us, acc);
-        sample(h, xs[u].w, K, a.step, a.step_magic, a.b_us, acc);
+      for (int u = 0; u < U; ++u) A[u] = __ldcs(v + i + u * 32);
+    }
+    while (have_a) {
+      const int64_t ib = i + U * 32;
+      const bool have_b = ib + (U - 1) * 32 < nv;
+      if (have_b) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) B[u] = __ldcs(v + ib + u * 32);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        sample<IDENT, REPL, PACK>(L, A[u].x, s1, s2);
+        sample<IDENT, REPL, PACK>(L, A[u].y, s1, s2);
+        sample<IDENT, REPL, PACK>(L, A[u].z, s1, s2);
+        sample<IDENT, REPL, PACK>(L, A[u].w, s1, s2);
+      }
+      i = ib;
+      if (!have_b) break;
+      const int64_t ia = ib + U * 32;
+      have_a = ia + (U - 1) * 32 < nv;
+      if (have_a) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) A[u] = __ldcs(v + ia + u * 32);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        sample<IDENT, REPL, PACK>(L, B[u].x, s1, s2);
+        sample<IDENT, REPL, PACK>(L, B[u].y, s1, s2);
+        sample<IDENT, REPL, PACK>(L, B[u].z, s1, s2);
+        sample<IDENT, REPL, PACK>(L, B[u].w, s1, s2);
+      }
+      i = ia;
+    }
+    for (; i < nv; i += 32) {
+      const int4 x = __ldcs(v + i);
+      sample<IDENT, REPL, PACK>(L, x.x, s1, s2);
+      sample<IDENT, REPL, PACK>(L, x.y, s1, s2);
+      sample<IDENT, REPL, PACK>(L, x.z, s1, s2);
+      sample<IDENT, REPL, PACK>(L, x.w, s1, s2);
+    }
+    // statistics: n is the chunk length; sum t~^2 split into 32-bit limb sums (fit_scan renormalises)
+    const uint64_t w1 = warp_sum_u64(s1), w2 = warp_sum_u64(s2 & 0xffffffffull),
+                   w3 = warp_sum_u64(s2 >> 32);
+    if (lane < 2) {  // lane 0: the tool's row, lane 1: the pooled row F
+      unsigned long long* st = a.stat + (lane == 0 ? tool : a.F) * 6;
+      atomicAdd(st + 0, (unsigned long long)(end - beg));
+      if (w1) atomicAdd(st + 1, (unsigned long long)w1);
+      if (w2) atomicAdd(st + 2, (unsigned long long)w2);
+      if (w3) atomicAdd(st + 3, (unsigned long long)w3);
+    }
+    __syncwarp();
+    // merge the replicas and flush: sum_k d = k step count_k - sum_k r (k < K)
+    for (int b = lane; b <= K; b += 32) {
+      uint64_t cn = 0, rr = 0;
+#pragma unroll
+      for (int q = 0; q < REPL; ++q) rr += rs[b * REPL + q];
+#pragma unroll
+      for (int q = 0; q < CW; ++q) {
+        const uint32_t w = cnt[b * CW + q];
+        cn += PACK ? (uint64_t)(w & 0xffffu) + (w >> 16) : (uint64_t)w;
+      }
+      if (cn) {
+        const uint64_t sm = b < K ? (uint64_t)b * L.step * cn - rr : 0;
+#pragma unroll
+        for (int row2 = 0; row2 < 2; ++row2) {  // the tool's row and the pooled row F
+          const int64_t o = (int64_t)(row2 ? a.F : tool) * (K + 1) + b;
+          atomicAdd(&a.hcnt[o], (unsigned long long)cn);
+          if (sm) atomicAdd(&a.hsum[o], (unsigned long long)sm);
+        }
       }
     }
-    for (; i < nv; i += FIT_THREADS) {
-      int4 x = __ldcs(v + i);
-      sample(h, x.x, K, a.step, a.step_magic, a.b_us, acc);
-      sample(h, x.y, K, a.step, a.step_magic, a.b_us, acc);
-      sample(h, x.z, K, a.step, a.step_magic, a.b_us, acc);
-      sample(h, x.w, K, a.step, a.step_magic, a.b_us, acc);
-    }
-    for (int64_t k = vb + threadIdx.x; k < end; k += FIT_THREADS)
-      sample(h, __ldg(&a.dur[k]), K, a.step, a.step_magic, a.b_us, acc);
+    __syncwarp();
+  }
+}
 
-    // statistics: 128-bit sum of squares as four 32-bit limbs in 64-bit slots
-    uint64_t l[6] = {acc.n, acc.s1, acc.lo & 0xffffffffull, acc.lo >> 32, acc.hi & 0xffffffffull,
-                     acc.hi >> 32};
-#pragma unroll
-    for (int q = 0; q < 6; ++q) l[q] = warp_sum_u64(l[q]);
-    if (lane == 0)
-#pragma unroll
-      for (int q = 0; q < 6; ++q) red[warp][q] = l[q];
-    __syncthreads();
-    if (threadIdx.x < 6) {
-      uint64_t s = 0;
-#pragma unroll
-      for (int w = 0; w < FIT_WARPS; ++w) s += red[w][threadIdx.x];
-      if (s) atomicAdd(&a.stat[ch.tool * 6 + threadIdx.x], (unsigned long long)s);
-    }
-    // merge the warp histograms and flush
-    for (int b = threadIdx.x; b <= K; b += FIT_THREADS) {
-      uint64_t cnt = 0, sum = 0;
-#pragma unroll
-      for (int w = 0; w < FIT_WARPS; ++w) {
-        uint64_t x = hsm[w * (K + 1) + b];
-        cnt += x >> 44;
-        sum += x & SUM_MASK;
-      }
-      if (cnt) {
-        atomicAdd(&a.hcnt[(int64_t)ch.tool * (K + 1) + b], (unsigned long long)cnt);
-        if (sum) atomicAdd(&a.hsum[(int64_t)ch.tool * (K + 1) + b], (unsigned long long)sum);
-      }
-    }
-    __syncthreads();
+template <bool IDENT>
+static void* hist_fn(int v) {
+  switch (v) {
+    case 0: return (void*)fit_hist_kernel<IDENT, 16, false, 16>;
+    case 1: return (void*)fit_hist_kernel<IDENT, 16, true, 16>;
+    case 2: return (void*)fit_hist_kernel<IDENT, 8, false, 8>;
+    case 3: return (void*)fit_hist_kernel<IDENT, 8, true, 8>;
+    case 4: return (void*)fit_hist_kernel<IDENT, 32, false, 16>;
+    case 5: return (void*)fit_hist_kernel<IDENT, 16, true, 8>;
+    default: return (void*)fit_hist_kernel<IDENT, 8, true, 4>;
   }
 }
 
 // ---------------------------------------------------------------------------------------------
-__device__ __forceinline__ void load_row(const ScanArgs& a, int row, int b, uint64_t& c,
-                                         uint64_t& s) {
-  const int K1 = a.K + 1;
-  if (row < a.F) {
-    c = a.hcnt[(int64_t)row * K1 + b];
-    s = a.hsum[(int64_t)row * K1 + b];
-  } else {
-    c = 0;
-    s = 0;
-    for (int f = 0; f < a.F; ++f) {
-      c += a.hcnt[(int64_t)f * K1 + b];
-      s += a.hsum[(int64_t)f * K1 + b];
-    }
-  }
-}
-
-__device__ __forceinline__ Stat row_stat(const ScanArgs& a, int row) {
-  uint64_t v[6] = {0, 0, 0, 0, 0, 0};
-  for (int f = (row < a.F ? row : 0); f < (row < a.F ? row + 1 : a.F); ++f)
+__device__ __forceinline__ Stat row_stat(const ScanArgs& a, int row) {  // row F = pooled
+  uint64_t v[6];
 #pragma unroll
-    for (int q = 0; q < 6; ++q) v[q] += a.stat[f * 6 + q];
+  for (int q = 0; q < 6; ++q) v[q] = a.stat[row * 6 + q];
   // renormalise the limbs: s2 = l0 + l1 2^32 + l2 2^64 + l3 2^96
   u128_t s2 = (u128_t)v[2] + ((u128_t)v[3] << 32) + ((u128_t)v[4] << 64) + ((u128_t)v[5] << 96);
   Stat s;
@@ -161,111 +235,113 @@ __device__ __forceinline__ Stat row_stat(const ScanArgs& a, int row) {
   return s;
 }
 
-// tau* for one row and turn bucket: warp scan over K bins + argmax (smallest k on ties).
-__device__ int64_t argmax_row(const ScanArgs& a, int row, int j, int lane) {
-  const int K = a.K;
-  const ct_cost_params& cp = a.cost;
-  const i128_t V = ((i128_t)cp.c_pf_ps * cp.ctx_tokens[j] *
-                    ((i128_t)cp.a_den + (i128_t)cp.a_num * cp.turn_weight[j])) / cp.a_den;
-  const i128_t C = (i128_t)cp.c_pin_ps * ceil_div_i64(cp.ctx_tokens[j], cp.bs);
-  // n = all samples of the row, overflow bucket included
-  uint64_t ntot = 0;
-  for (int b = lane; b <= K; b += 32) {
-    uint64_t c, s;
-    load_row(a, row, b, c, s);
-    ntot += c;
-  }
-  ntot = warp_sum_u64(ntot);
-  // contiguous bins per lane for an ordered scan
-  const int per = (K + 31) / 32;
-  const int b0 = lane * per, b1 = min(b0 + per, K);
-  uint64_t lc = 0, ls = 0;
-  for (int b = b0; b < b1; ++b) {
-    uint64_t c, s;
-    load_row(a, row, b, c, s);
-    lc += c;
-    ls += s;
-  }
-  // exclusive scan across lanes
-  uint64_t ic = lc, is = ls;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    uint64_t tc = __shfl_up_sync(FULL_MASK, ic, o);
-    uint64_t ts = __shfl_up_sync(FULL_MASK, is, o);
-    if (lane >= o) { ic += tc; is += ts; }
-  }
-  uint64_t cc = ic - lc, cs = is - ls;
-  i128_t best = 0;  // U(0) = 0: TTL 0 = no pin
-  int bk = 0;
-  for (int b = b0; b < b1; ++b) {
-    uint64_t c, s;
-    load_row(a, row, b, c, s);
-    cc += c;
-    cs += s;
-    if (b == 0) continue;
-    const i128_t tau = (i128_t)b * a.cost.grid_step_us;
-    const i128_t U = V * (i128_t)cc - C * ((i128_t)cs + tau * (i128_t)(ntot - cc));
-    if (U > best) { best = U; bk = b; }
-  }
-  // argmax across lanes: larger U wins, ties -> smaller k
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    uint64_t lo = __shfl_xor_sync(FULL_MASK, (uint64_t)best, o);
-    uint64_t hi = __shfl_xor_sync(FULL_MASK, (uint64_t)((u128_t)best >> 64), o);
-    int ok = __shfl_xor_sync(FULL_MASK, bk, o);
-    i128_t ob = (i128_t)(((u128_t)hi << 64) | lo);
-    if (ob > best || (ob == best && ok < bk)) { best = ob; bk = ok; }
-  }
-  return (int64_t)bk * a.cost.grid_step_us;
-}
+constexpr int SCAN_THREADS = 256;
 
-__global__ void __launch_bounds__(128) fit_scan_kernel(ScanArgs a) {
-  const int lane = threadIdx.x & 31;
-  const int w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  const int J = a.J;
-  if (w >= (a.F + 1) * J) return;
-  const int row = w / J, j = w % J;
-  const Stat g = row_stat(a, a.F);
+// One CTA per (tool row, group of 8 turn buckets) (row F = all samples pooled).  The row's bucket counts / sums are loaded
+// once into shared memory and prefix-scanned (cnt_le(k), sum_le(k)); then each warp evaluates
+// n U(k) = V_j cnt_le(k) - C_j (sum_le(k) + tau_k (n - cnt_le(k))) for its turn buckets j in
+// 128-bit integers and keeps the smallest maximiser (U(0) = 0: no pin).
+__global__ void __launch_bounds__(SCAN_THREADS) fit_scan_kernel(ScanArgs a) {
+  extern __shared__ __align__(16) unsigned long long sh[];
+  const int K = a.K, F = a.F, J = a.J;
+  unsigned long long* pc = sh;          // [K] inclusive prefix of counts
+  unsigned long long* ps = sh + K;      // [K] inclusive prefix of sums
+  __shared__ unsigned long long wtot[2][SCAN_THREADS / 32];
+  __shared__ unsigned long long carry[2], ntot_sh;
+  const int row = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const Stat f = row_stat(a, row);
   // tools with fewer than N samples take the pooled row's result (PAPER.md:492-494 ladder)
-  const int eff = (row < a.F && f.n < a.est.n_min) ? a.F : row;
-  const int64_t tau = argmax_row(a, eff, j, lane);
-  if (lane == 0) {
-    a.ttl_argmax[(int64_t)row * J + j] = tau;
-    if (j == 0) {
-      a.ttl_paper[row] = calc_ttl(g, f, a.est, a.cost.avg_turns_den, a.cost.avg_turns_num);
-      if (a.stats_out) {
-        a.stats_out[row * 4 + 0] = f.n;
-        a.stats_out[row * 4 + 1] = f.s1;
-        a.stats_out[row * 4 + 2] = (int64_t)f.s2lo;
-        a.stats_out[row * 4 + 3] = (int64_t)f.s2hi;
-      }
+  const int src = (row == F || f.n < a.est.n_min) ? F : row;
+  if (tid == 0) { carry[0] = carry[1] = 0; ntot_sh = 0; }
+  __syncthreads();
+  const int K1 = K + 1;
+  for (int base = 0; base < K; base += SCAN_THREADS) {
+    const int b = base + tid;
+    unsigned long long c = 0, s = 0;
+    if (b < K) {
+      c = a.hcnt[(int64_t)src * K1 + b];
+      s = a.hsum[(int64_t)src * K1 + b];
+    }
+    unsigned long long ic = c, is = s;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      unsigned long long tc = __shfl_up_sync(FULL_MASK, ic, o), ts = __shfl_up_sync(FULL_MASK, is, o);
+      if (lane >= o) { ic += tc; is += ts; }
+    }
+    if (lane == 31) { wtot[0][warp] = ic; wtot[1][warp] = is; }
+    __syncthreads();
+    unsigned long long oc = carry[0], os = carry[1];
+    for (int w = 0; w < warp; ++w) { oc += wtot[0][w]; os += wtot[1][w]; }
+    if (b < K) { pc[b] = ic + oc; ps[b] = is + os; }
+    __syncthreads();
+    if (tid == SCAN_THREADS - 1) { carry[0] = ic + oc; carry[1] = is + os; }
+    __syncthreads();
+  }
+  if (tid == 0) {
+    ntot_sh = carry[0] + a.hcnt[(int64_t)src * K1 + K];  // + overflow bucket
+  }
+  __syncthreads();
+  const uint64_t ntot = ntot_sh;
+  const ct_cost_params& cp = a.cost;
+  for (int j = blockIdx.y * (SCAN_THREADS / 32) + warp; j < min(J, (int)(blockIdx.y + 1) * (SCAN_THREADS / 32));
+       ++j) {
+    const i128_t V = ((i128_t)cp.c_pf_ps * cp.ctx_tokens[j] *
+                      ((i128_t)cp.a_den + (i128_t)cp.a_num * cp.turn_weight[j])) / cp.a_den;
+    const i128_t C = (i128_t)cp.c_pin_ps * ceil_div_i64(cp.ctx_tokens[j], cp.bs);
+    i128_t best = 0;
+    int bk = 0;
+    for (int k = 1 + lane; k < K; k += 32) {
+      const uint64_t cc = pc[k], cs = ps[k];
+      const i128_t tau = (i128_t)k * cp.grid_step_us;
+      const i128_t U = V * (i128_t)cc - C * ((i128_t)cs + tau * (i128_t)(ntot - cc));
+      if (U > best) { best = U; bk = k; }  // k increases: strict > keeps the smallest
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const uint64_t lo = __shfl_xor_sync(FULL_MASK, (uint64_t)best, o);
+      const uint64_t hi = __shfl_xor_sync(FULL_MASK, (uint64_t)((u128_t)best >> 64), o);
+      const int ok = __shfl_xor_sync(FULL_MASK, bk, o);
+      const i128_t ob = (i128_t)(((u128_t)hi << 64) | lo);
+      if (ob > best || (ob == best && ok < bk)) { best = ob; bk = ok; }
+    }
+    if (lane == 0) a.ttl_argmax[(int64_t)row * J + j] = (int64_t)bk * cp.grid_step_us;
+  }
+  if (tid == 0 && blockIdx.y == 0) {
+    const Stat g = row_stat(a, F);
+    a.ttl_paper[row] = calc_ttl(g, f, a.est, a.cost.avg_turns_den, a.cost.avg_turns_num);
+    if (a.stats_out) {
+      a.stats_out[row * 4 + 0] = f.n;
+      a.stats_out[row * 4 + 1] = f.s1;
+      a.stats_out[row * 4 + 2] = (int64_t)f.s2lo;
+      a.stats_out[row * 4 + 3] = (int64_t)f.s2hi;
     }
   }
 }
 
 cudaError_t launch_fit_hist(const FitArgs& a, int grid, cudaStream_t s) {
-  int smem = fit_hist_smem(a.K);
-  cudaError_t e = cudaFuncSetAttribute(fit_hist_kernel,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  if (e != cudaSuccess) return e;
-  fit_hist_kernel<<<grid, FIT_THREADS, smem, s>>>(a);
-  return cudaGetLastError();
+  const int smem = fit_hist_smem(a.K);
+  void* k = a.step == 1 ? hist_fn<true>(variant()) : hist_fn<false>(variant());
+  void* args[] = {(void*)&a};
+  return cudaLaunchKernel(k, dim3(grid), dim3(FIT_THREADS), args, smem, s);
 }
 
 int fit_hist_occupancy(int smem) {
-  if (cudaFuncSetAttribute(fit_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
-      cudaSuccess)
-    return 0;
+  for (void* k : {hist_fn<true>(variant()), hist_fn<false>(variant())})
+    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
+      return 0;
   int nb = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fit_hist_kernel, FIT_THREADS, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, hist_fn<false>(variant()), FIT_THREADS, smem);
   return nb;
 }
 
 cudaError_t launch_fit_scan(const ScanArgs& a, cudaStream_t s) {
-  int warps = (a.F + 1) * a.J;
-  int grid = (warps + 3) / 4;
-  fit_scan_kernel<<<grid, 128, 0, s>>>(a);
+  const int smem = 16 * a.K;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(fit_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+  }
+  const dim3 grid(a.F + 1, (a.J + SCAN_THREADS / 32 - 1) / (SCAN_THREADS / 32));
+  fit_scan_kernel<<<grid, SCAN_THREADS, smem, s>>>(a);
   return cudaGetLastError();
 }
 

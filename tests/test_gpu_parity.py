@@ -196,8 +196,8 @@ def test_fit_parity_random(ctx, seed):
     est = cf.Estimator(n_min=int(rng.integers(1, 8)))
     g, o = fit_both(ctx, dur, off, K, step, J, 13_400_000, int(rng.integers(0, 3000)), est,
                     avg=(int(rng.integers(0, 500)), int(rng.integers(0, 50))))
-    for x, y in zip(g, o):
-        assert np.array_equal(x, y)
+    for name, x, y in zip(("ttl_argmax", "ttl_paper", "stats"), g, o):
+        assert np.array_equal(x, y), (name, K, step, J, x, y)
 
 
 def test_fit_point_mass_and_alignment(ctx):

@@ -1,0 +1,53 @@
+"""Small driver for ncu captures: one kernel family per invocation.
+
+  python tools/prof_kernels.py fit [log2n]        -> ct_fit_ttl on 2^log2n samples (3 calls)
+  python tools/prof_kernels.py replay [cfg] [seeds] -> one ct_simulate_batch of a config
+Prints timing from CUDA events (not a bench number when run under ncu).
+"""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import numpy as np
+import torch
+
+import paper_2511_02230_b200 as ct
+from ctgen import configs as cf
+from ctgen import traces
+
+
+def main():
+    what = sys.argv[1]
+    ctx = ct.Context(0)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if what == "fit":
+        log2n = int(sys.argv[2]) if len(sys.argv) > 2 else 28
+        dur, off = traces.synthetic_samples_torch(log2n, 32, 1234, "cuda")
+        cp = ct.cost_params(13_400_000, 200, 16, 1, 10, 50_000, 256,
+                            [min(16 * 2**j, 120_000) for j in range(64)], list(range(1, 65)))
+        for i in range(3):
+            e0.record()
+            ct.ct_fit_ttl(ctx, dur, off, cp, cf.Estimator())
+            e1.record()
+            torch.cuda.synchronize()
+            t = e0.elapsed_time(e1) / 1e3
+            print("fit n=2^%d: %.3f ms, %.1f GB/s" % (log2n, t * 1e3, 4 * (1 << log2n) / t / 1e9))
+    else:
+        name = sys.argv[2] if len(sys.argv) > 2 else "cfg3"
+        seeds = int(sys.argv[3]) if len(sys.argv) > 3 else 16
+        w = {"cfg2": cf.config2, "cfg3": cf.config3, "cfg5": cf.config5}[name](n_seeds=seeds)
+        dt = ct.DeviceTrace(w.trace)
+        for i in range(2):
+            e0.record()
+            s, _ = ct.ct_simulate_batch(ctx, dt, w.sweep, w.engine, jct=False)
+            e1.record()
+            torch.cuda.synchronize()
+            t = e0.elapsed_time(e1) / 1e3
+            turns = int(s[:, 1].sum())
+            print("replay %s seeds=%d: %d replicas %d turns %.3f ms %.3e turns/s launch=%s" % (
+                name, seeds, w.sweep.n_replicas, turns, t * 1e3, turns / t, ctx.last_launch()))
+
+
+if __name__ == "__main__":
+    main()
