@@ -38,6 +38,33 @@ __device__ __forceinline__ uint64_t warp_sum_u64(uint64_t v) {
 
 __device__ __forceinline__ int64_t ceil_div_i64(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
+// Warp minimum of non-negative 64-bit values with two REDUX.MIN (hi word, then lo word of the
+// lanes holding the minimal hi word).
+__device__ __forceinline__ int64_t warp_min64_redux(int64_t v) {
+  const uint32_t hi = (uint32_t)((uint64_t)v >> 32), lo = (uint32_t)v;
+  const uint32_t mh = __reduce_min_sync(FULL_MASK, hi);
+  const uint32_t ml = __reduce_min_sync(FULL_MASK, hi == mh ? lo : 0xffffffffu);
+  return (int64_t)(((uint64_t)mh << 32) | ml);
+}
+
+// ceil(x / 1e6) for picosecond sums below 2^63 (constant divisor: multiply-high sequence).
+__device__ __forceinline__ int64_t ceil_ps_to_us(uint64_t ps) {
+  return (int64_t)((ps + 999999ull) / 1000000ull);
+}
+
+// ceil(x / d) for x < 2^31 and a runtime divisor d < 2^20 given by its magic M = ceil(2^64 / d):
+// floor(y / d), y = x + d - 1 < 2^32, is the high word of y * M (exact for 32-bit y); d = 1 uses
+// ident = 1, M = 0.
+struct DivMagic {
+  uint32_t mhi, mlo, dm1, ident;
+};
+__device__ __forceinline__ uint32_t ceil_div_magic(uint32_t x, const DivMagic& m) {
+  const uint32_t y = x + m.dm1;
+  uint64_t p = __umulhi(y, m.mlo);
+  asm("mad.wide.u32 %0, %1, %2, %0;" : "+l"(p) : "r"(y), "r"(m.mhi));
+  return (uint32_t)(p >> 32) + y * m.ident;
+}
+
 // floor(sqrt(x)) exactly: double estimate, then integer correction.
 __device__ __forceinline__ uint64_t isqrt_u64(uint64_t x) {
   uint64_t r = (uint64_t)sqrt((double)x);

@@ -24,6 +24,7 @@ struct ReplayArgs {
   int64_t* jct;
   unsigned long long* counter;
   int smem_per_warp;
+  uint64_t bs_magic;  // ceil(2^64 / bs) (0 when bs == 1)
 };
 
 // Bytes of shared memory one replica (one warp) needs for `ns` slots per lane and F tools.

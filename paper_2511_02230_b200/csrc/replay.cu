@@ -53,6 +53,11 @@ __device__ __forceinline__ void replay_one(const ReplayArgs& a, int64_t r, unsig
   const ct_engine_params& E = a.eng;
   const ct_estimator_params& est = a.est;
   const int64_t bs = E.bs;
+  DivMagic bsm;
+  bsm.mhi = (uint32_t)(a.bs_magic >> 32);
+  bsm.mlo = (uint32_t)a.bs_magic;
+  bsm.dm1 = (uint32_t)(bs - 1);
+  bsm.ident = bs == 1 ? 1u : 0u;
   const bool eager = (pol.flags & CT_FLAG_STEP_EXPIRY) == 0;
   const bool vany = (pol.flags & CT_FLAG_VICTIMS_ANY) != 0;
   const bool dram_on = pol.dram != 0 && E.dram_blocks > 0;
@@ -103,7 +108,7 @@ __device__ __forceinline__ void replay_one(const ReplayArgs& a, int64_t r, unsig
     int64_t g = gblk[v];
     free_blk += g;
     if (dram_on) {
-      int64_t nb = ceil_div_i64(ctx[v], bs);
+      int64_t nb = ceil_div_magic((uint32_t)ctx[v], bsm);
       dfree += dblk[v];
       int64_t keep = 0;
       if (nb > 0 && nb <= dfree) { keep = nb; dfree -= nb; }
@@ -126,7 +131,7 @@ __device__ __forceinline__ void replay_one(const ReplayArgs& a, int64_t r, unsig
       if (eager) x = min(x, t_exp[p]);
       lt = min(lt, x);
     }
-    const int64_t t_prog = warp_min64(lt);
+    const int64_t t_prog = warp_min64_redux(lt);
     int64_t t = min(t_prog, t_arr);
     if (in_flight) t = min(t, iter_end);
     if (t == CT_INF64) break;
@@ -341,7 +346,7 @@ __device__ __forceinline__ void replay_one(const ReplayArgs& a, int64_t r, unsig
       }
       const int4 tr = turn_rec(h, turn[h]);
       const int64_t hctx = ctx[h];
-      const int64_t need = ceil_div_i64(hctx + tr.x + tr.y, bs) - gblk[h];
+      const int64_t need = (int64_t)ceil_div_magic((uint32_t)(hctx + tr.x + tr.y), bsm) - gblk[h];
       if (need > free_blk && (admitted == 0 || vany)) {
         while (need > free_blk) {  // victims: latest program arrival first, never the head
           int v = -1;
@@ -379,10 +384,10 @@ __device__ __forceinline__ void replay_one(const ReplayArgs& a, int64_t r, unsig
       if (hp) {
         cached = hctx;
         ++c_hits;
-      } else if (dram_on && hd > 0 && hd == ceil_div_i64(hctx, bs)) {
+      } else if (dram_on && hd > 0 && hd == (int64_t)ceil_div_magic((uint32_t)hctx, bsm)) {
         cached = hctx;
         loading = true;
-        ld = max(now, chan) + ceil_div_i64(hd * E.c_h2d_ps, 1000000);
+        ld = max(now, chan) + ceil_ps_to_us((uint64_t)(hd * E.c_h2d_ps));
         chan = ld;
         ++c_reload;
       } else {
@@ -427,10 +432,10 @@ __device__ __forceinline__ void replay_one(const ReplayArgs& a, int64_t r, unsig
       const int64_t base = E.c0_ps + E.c_kv_ps * bs * kv_sum;
       int64_t k = 1, dur;
       if (pf > 0) {
-        dur = ceil_div_i64(base + E.c_pf_ps * pf, 1000000);
+        dur = ceil_ps_to_us((uint64_t)(base + E.c_pf_ps * pf));
         pf = 0;
       } else {
-        const int64_t d = ceil_div_i64(base, 1000000);
+        const int64_t d = ceil_ps_to_us((uint64_t)base);
         if (stable) {
           // macro-step: identical iterations until the first finish or the first boundary at or
           // after the next external event (arrival, tool return, load done, pin expiry)
@@ -441,14 +446,20 @@ __device__ __forceinline__ void replay_one(const ReplayArgs& a, int64_t r, unsig
             if ((rb >> s) & 1u) lf = min(lf, fin[pl]);
             le = min(le, min(t_ev[pl], t_exp[pl]));
           }
-          const int64_t mfin = warp_min64(lf);
-          const int64_t te = min(warp_min64(le), t_arr);
+          const int64_t mfin = warp_min64_redux(lf);
+          const int64_t te = min(warp_min64_redux(le), t_arr);
           const int64_t m = mfin - n_it;
           int64_t j = m;
+          // first boundary at or after te: ceil((te - now) / d), needed only when < m
           if (te != CT_INF64) {
-            int64_t jb = ceil_div_i64(te - now, d);
-            if (jb < 1) jb = 1;
-            if (jb < j) j = jb;
+            const int64_t gap = te - now;  // >= 1
+            const double est = (double)gap / (double)d;
+            if (est < (double)m + 2.0) {  // exact correction of the estimate (no overflow here)
+              int64_t jb = (int64_t)est;
+              while (jb * d < gap) ++jb;
+              while (jb > 1 && (jb - 1) * d >= gap) --jb;
+              if (jb < j) j = jb;
+            }
           }
           k = j;
         }
@@ -494,8 +505,8 @@ __device__ __forceinline__ void replay_one(const ReplayArgs& a, int64_t r, unsig
         if (lt < r99 && r99 <= le) c99 = v;
       }
     }
-    p50 = warp_min64(c50);
-    p99 = warp_min64(c99);
+    p50 = warp_min64_redux(c50);
+    p99 = warp_min64_redux(c99);
   }
   if (lane == 0) {
     ct_replica_summary o;
