@@ -222,18 +222,26 @@ def fit_bandwidth(ctx, ct, cf, log2n, dev, peaks, consts):
     s = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     reps = 10
+    ctx.set_timing(True)
+    kms = []
     e0.record(s)
     for _ in range(reps):
         ct.ct_fit_ttl(ctx, dur, off, cp, est)
+        kms.append(ctx.last_launch()["fit_hist_ms"])  # waits for this launch's end event
     e1.record(s)
     torch.cuda.synchronize()
-    t = e0.elapsed_time(e1) / 1e3 / reps
+    ctx.set_timing(False)
+    t_call = e0.elapsed_time(e1) / 1e3 / reps
+    t = float(np.mean(kms)) / 1e3
     gbs = 4.0 * n / t / 1e9
     peak = float(peaks["hbm_gbs"])
+    tr = consts.get("fit_dram_bytes_per_sample")
     return {"bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s", "frac": gbs / peak,
-            "traffic": consts.get("fit_dram_bytes_per_launch"),
-            "kernel": "ct_fit_ttl (fit_hist + fit_scan)", "samples": n, "bytes_per_sample": 4,
-            "ms_per_launch": t * 1e3}
+            "traffic": tr * n if tr else None,
+            "kernel": "fit_hist_kernel (CUDA events around the launch, inside the library)",
+            "samples": n, "bytes_per_sample": 4, "ms_per_launch": t * 1e3,
+            "call_ms": t_call * 1e3, "call_gbs": 4.0 * n / t_call / 1e9,
+            "note": "call = fit_hist + fit_scan + scratch memset, host-synchronised per call"}
 
 
 def main():
@@ -374,7 +382,8 @@ def main():
     roofline = {"bound": "alu", "kernel": "replay_kernel", "unit": "Twarp-inst/s",
                 "achieved": achieved, "peak": alu_peak,
                 "frac": (achieved / alu_peak) if achieved else None,
-                "traffic": consts.get("replay_dram_bytes_per_turn", {}).get(w.name) if consts else None,
+                "traffic": (consts.get("replay_dram_bytes_per_turn", {}).get(w.name, 0) * turns_shard)
+                if consts.get("replay_dram_bytes_per_turn", {}).get(w.name) is not None else None,
                 "peak_basis": "148 SMs x 4 schedulers x 1 warp-inst/clk x %.0f MHz (max clock)" % clk_mhz,
                 "achieved_basis": "ncu warp-inst per replica-turn (profiles/ncu_constants.json) x "
                                   "replica-turns per launch / CUDA-event launch time",

@@ -231,13 +231,20 @@ int ct_simulate_batch_host(ct_ctx* ctx, const ct_trace_set* host_traces, const c
 int ct_jct_stats(ct_ctx* ctx, const ct_replica_summary* summaries, int64_t n_replicas,
                  int32_t n_cells, ct_cell_stats* out, void* stream);
 
-/* Launch statistics of the last ct_simulate_batch on this context (for bench accounting). */
+/* Launch statistics of the last ct_simulate_batch / ct_fit_ttl on this context (bench
+ * accounting).  With timing enabled (ct_ctx_set_timing), the library records CUDA events on the
+ * caller's stream around the dominant kernel of each call (replay_kernel, fit_hist_kernel);
+ * ct_last_launch then waits for them and reports the kernel-only durations in milliseconds
+ * (-1 when not timed). */
 typedef struct {
   int32_t grid, block, warps_per_block, slots_per_lane;
   int64_t smem_per_block;
-  int64_t launches;         /* kernels launched by the last call */
+  int64_t launches;         /* kernels launched by the last ct_simulate_batch */
+  float replay_ms;          /* last replay_kernel duration */
+  float fit_hist_ms;        /* last fit_hist_kernel duration */
 } ct_launch_info;
 int ct_last_launch(ct_ctx* ctx, ct_launch_info* info);
+int ct_ctx_set_timing(ct_ctx* ctx, int enable);
 
 #ifdef __cplusplus
 }

@@ -18,7 +18,8 @@ MAX_J = 64
 
 # every symbol include/continuum.h declares (checked by tests/test_abi.py)
 EXPORTS = ["ct_version", "ct_last_error", "ct_ctx_create", "ct_ctx_destroy", "ct_fit_ttl",
-           "ct_simulate_batch", "ct_simulate_batch_host", "ct_jct_stats", "ct_last_launch"]
+           "ct_simulate_batch", "ct_simulate_batch_host", "ct_jct_stats", "ct_last_launch",
+           "ct_ctx_set_timing"]
 
 
 class TraceSet(C.Structure):
@@ -63,7 +64,8 @@ class TtlTable(C.Structure):
 
 class LaunchInfo(C.Structure):
     _fields_ = [("grid", i32), ("block", i32), ("warps_per_block", i32), ("slots_per_lane", i32),
-                ("smem_per_block", i64), ("launches", i64)]
+                ("smem_per_block", i64), ("launches", i64), ("replay_ms", C.c_float),
+                ("fit_hist_ms", C.c_float)]
 
 
 assert C.sizeof(Policy) == 48 and C.sizeof(EngineParams) == 64 and C.sizeof(EstimatorParams) == 64
@@ -90,8 +92,9 @@ def lib() -> C.CDLL:
                                              C.POINTER(EngineParams), i64, i64, vp, vp, vp]
         L.ct_jct_stats.argtypes = [vp, vp, i64, i32, vp, vp]
         L.ct_last_launch.argtypes = [vp, C.POINTER(LaunchInfo)]
+        L.ct_ctx_set_timing.argtypes = [vp, C.c_int]
         for f in ("ct_ctx_create", "ct_ctx_destroy", "ct_fit_ttl", "ct_simulate_batch",
-                  "ct_simulate_batch_host", "ct_jct_stats", "ct_last_launch"):
+                  "ct_simulate_batch_host", "ct_jct_stats", "ct_last_launch", "ct_ctx_set_timing"):
             getattr(L, f).restype = C.c_int
         _lib = L
     return _lib

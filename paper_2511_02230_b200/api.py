@@ -49,6 +49,10 @@ class Context:
     def handle(self):
         return self._h
 
+    def set_timing(self, enable: bool = True) -> None:
+        """Record CUDA events around the dominant kernel of each call (kernel-only times)."""
+        L.check(L.lib().ct_ctx_set_timing(self._h, 1 if enable else 0), "ct_ctx_set_timing")
+
     def last_launch(self) -> dict:
         info = L.LaunchInfo()
         L.check(L.lib().ct_last_launch(self._h, C.byref(info)), "ct_last_launch")

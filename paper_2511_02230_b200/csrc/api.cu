@@ -33,6 +33,9 @@ struct ct_ctx {
   size_t h_jct_cap = 0;
   ct_launch_info last{};
   int fit_occ = 0, fit_occ_smem = -1;
+  bool timing = false;
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};  // replay start/end, fit start/end
+  bool replay_timed = false, fit_timed = false;
 };
 
 namespace {
@@ -114,12 +117,32 @@ int ct_ctx_destroy(ct_ctx* c) {
   void* ps[] = {c->counter, c->axes, c->fit, c->chunks, c->h_progs, c->h_turns, c->h_out, c->h_jct};
   for (void* p : ps)
     if (p) cudaFree(p);
+  for (auto e : c->ev)
+    if (e) cudaEventDestroy(e);
   delete c;
+  return CT_OK;
+}
+
+int ct_ctx_set_timing(ct_ctx* c, int enable) {
+  if (!c) return fail(CT_EINVAL, "NULL argument");
+  if (enable && !c->ev[0])
+    for (auto& e : c->ev) CT_CUDA(cudaEventCreate(&e));
+  c->timing = enable != 0;
   return CT_OK;
 }
 
 int ct_last_launch(ct_ctx* c, ct_launch_info* info) {
   if (!c || !info) return fail(CT_EINVAL, "NULL argument");
+  c->last.replay_ms = -1.f;
+  c->last.fit_hist_ms = -1.f;
+  if (c->replay_timed) {
+    CT_CUDA(cudaEventSynchronize(c->ev[1]));
+    CT_CUDA(cudaEventElapsedTime(&c->last.replay_ms, c->ev[0], c->ev[1]));
+  }
+  if (c->fit_timed) {
+    CT_CUDA(cudaEventSynchronize(c->ev[3]));
+    CT_CUDA(cudaEventElapsedTime(&c->last.fit_hist_ms, c->ev[2], c->ev[3]));
+  }
   *info = c->last;
   return CT_OK;
 }
@@ -216,8 +239,11 @@ int ct_simulate_batch(ct_ctx* c, const ct_trace_set* tr, const ct_sweep* sw,
   if (occ < 1) return fail(CT_ECUDA, "replay kernel cannot be resident (smem %d)", smem);
   const int64_t need_blocks = (re - rb + wpb - 1) / wpb;
   const int grid = (int)std::min<int64_t>((int64_t)c->sm_count * occ, need_blocks);
+  if (c->timing) CT_CUDA(cudaEventRecord(c->ev[0], s));
   cudaError_t e = ct::launch_replay(a, ns, wpb, grid, s);
   if (e != cudaSuccess) return cuda_fail(e, "replay launch");
+  if (c->timing) CT_CUDA(cudaEventRecord(c->ev[1], s));
+  c->replay_timed = c->timing;
   c->last.grid = grid;
   c->last.block = 32 * wpb;
   c->last.warps_per_block = wpb;
@@ -356,8 +382,11 @@ int ct_fit_ttl(ct_ctx* c, const ct_samples* sm, const ct_cost_params* cp,
     const int wpb = ct::fit_hist_threads() / 32;  // every warp takes its own chunks
     const int grid = (int)std::min<int64_t>((int64_t)c->sm_count * c->fit_occ,
                                             (fa.n_chunks + wpb - 1) / wpb);
+    if (c->timing) CT_CUDA(cudaEventRecord(c->ev[2], s));
     cudaError_t e = ct::launch_fit_hist(fa, grid, s);
     if (e != cudaSuccess) return cuda_fail(e, "fit_hist launch");
+    if (c->timing) CT_CUDA(cudaEventRecord(c->ev[3], s));
+    c->fit_timed = c->timing;
     ++launches;
   }
   ct::ScanArgs sa;

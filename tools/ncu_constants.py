@@ -1,0 +1,48 @@
+"""Write profiles/ncu_constants.json entries from an ncu report (bench.py roofline inputs).
+
+usage: python tools/ncu_constants.py replay <report> <workload_name> <replica_turns>
+       python tools/ncu_constants.py fit <report> <samples>
+"""
+import csv, io, json, os, subprocess, sys
+
+OUT = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles", "ncu_constants.json")
+
+
+def raw(rep):
+    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    return [dict(zip(rows[0], r)) for r in rows[2:]], dict(zip(rows[0], rows[1]))
+
+
+def num(d, k):
+    return float(d[k].replace(",", ""))
+
+
+def scale(unit):
+    return {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1)
+
+
+def main():
+    c = json.load(open(OUT)) if os.path.exists(OUT) else {}
+    kind, rep = sys.argv[1], sys.argv[2]
+    rows, units = raw(rep)
+    d = rows[0]
+    dram = num(d, "dram__bytes_read.sum") * scale(units["dram__bytes_read.sum"]) + \
+        num(d, "dram__bytes_write.sum") * scale(units["dram__bytes_write.sum"])
+    if kind == "replay":
+        name, turns = sys.argv[3], float(sys.argv[4])
+        inst = num(d, "smsp__inst_executed.sum")
+        c.setdefault("replay_warp_inst_per_turn", {})[name] = inst / turns
+        c.setdefault("replay_dram_bytes_per_turn", {})[name] = dram / turns
+        c.setdefault("source", {})["replay_" + name] = os.path.basename(rep)
+    else:
+        n = float(sys.argv[3])
+        c["fit_dram_bytes_per_sample"] = dram / n
+        c["fit_dram_bytes_per_launch_2^28"] = dram / n * 2**28
+        c.setdefault("source", {})["fit"] = os.path.basename(rep)
+    json.dump(c, open(OUT, "w"), indent=1, sort_keys=True)
+    print(json.dumps(c, indent=1))
+
+
+if __name__ == "__main__":
+    main()
