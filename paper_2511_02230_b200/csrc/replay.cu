@@ -10,6 +10,8 @@
 // iterations are macro-stepped: the warp jumps straight to the first iteration boundary that
 // is a finish or lies at/after the next external event, which parity tests prove equal to the
 // oracle's one-iteration-at-a-time stepping.
+#include <cstdlib>
+
 #include "ct_device.cuh"
 #include "ct_internal.h"
 
@@ -18,6 +20,7 @@ namespace ct {
 enum : int { S_OUT = 0, S_QUEUED = 1, S_RUN = 2, S_LOAD = 3, S_READY = 4, S_TOOL = 5, S_DONE = 6 };
 
 int replay_smem_per_warp(int ns, int F) {
+  if (ns == 1) return (32 * (F + 1) + 48 + 15) & ~15;  // registers hold the programs; SMEM: estimator + Acc
   int pm = 32 * ns;
   int b = 53 * pm;
   b = (b + 15) & ~15;
@@ -547,8 +550,452 @@ __device__ __forceinline__ void replay_one(const ReplayArgs& a, int64_t r, unsig
   __syncwarp();
 }
 
-template <int NS>
-__global__ void __launch_bounds__(256) replay_kernel(ReplayArgs a) {
+// -----------------------------------------------------------------------------------------------
+// P <= 32: one program per lane, all per-program state in registers.  Every event source is a
+// per-lane time (program arrival, tool return, load done, pin expiry), so the next event is one
+// 64-bit REDUX minimum; events of one kind at one instant are applied by their owner lanes in
+// parallel, and only order-dependent work (finishes, DRAM write-through, estimator updates,
+// admission) is serialised in program-index order with the operands broadcast by shuffles.
+// Same semantics as replay_one<NS> (C-5/C-6), checked byte for byte by the tests.
+struct Acc {  // per-replica summary counters (P <= 32 path)
+  int64_t bubble, prefill, recomp, busy;
+  int32_t hits, exp, vict, reload;
+};
+
+__device__ __forceinline__ int64_t shfl64(int64_t v, int src) {
+  return (int64_t)__shfl_sync(FULL_MASK, (unsigned long long)v, src);
+}
+
+__device__ __forceinline__ void replay_one_w32(const ReplayArgs& a, int64_t r, Stat* stats,
+                                               int lane) {
+  const int P = a.P, F = a.F;
+  const int64_t npol = a.n_pol, nkv = a.n_kv, nrate = a.n_rate;
+  const int pol_i = (int)(r % npol);
+  const int kv_i = (int)((r / npol) % nkv);
+  const int rate_i = (int)((r / (npol * nkv)) % nrate);
+  const int64_t seed = r / (npol * nkv * nrate);
+  const ct_policy* polp = a.pols + pol_i;  // t_pin / t_thresh re-read from L1 when needed
+  const int prio = polp->priority, pause = polp->pause, pflags = polp->flags;
+  const int64_t gap = a.gap[rate_i];
+  const ct_engine_params& E = a.eng;
+  const ct_estimator_params& est = a.est;
+  const int64_t bs = E.bs;
+  DivMagic bsm;
+  bsm.mhi = (uint32_t)(a.bs_magic >> 32);
+  bsm.mlo = (uint32_t)a.bs_magic;
+  bsm.dm1 = (uint32_t)(bs - 1);
+  bsm.ident = bs == 1 ? 1u : 0u;
+  const bool eager = (pflags & CT_FLAG_STEP_EXPIRY) == 0;
+  const bool vany = (pflags & CT_FLAG_VICTIMS_ANY) != 0;
+  const bool dram_on = polp->dram != 0 && E.dram_blocks > 0;
+  const bool need_stats = pause == CT_PAUSE_PAPER ||
+                          (pause == CT_PAUSE_FIXED && polp->t_thresh_us != CT_ALWAYS);
+  if (need_stats) {
+    for (int i = lane; i < 4 * (F + 1); i += 32) ((int64_t*)stats)[i] = 0;
+    __syncwarp();
+  }
+
+  // ---- this lane's program -----------------------------------------------------------------
+  const bool live = lane < P;
+  int32_t turn0 = 0, nturns = 1;
+  int64_t arr = CT_INF64;
+  if (live) {
+    const ct_program pr = a.progs[seed * P + lane];
+    turn0 = pr.turn0;
+    nturns = pr.nturns;
+    arr = (pr.arr_q * gap) >> 20;
+  }
+  const int64_t arr0 = shfl64(arr, 0);  // programs arrive in index order: min arrival
+  int st = S_OUT;
+  int64_t tev = arr;          // arrival (OUT), tool return (TOOL), load done (LOAD); INF otherwise
+  int64_t texp = CT_INF64;    // expiry + 1 while pinned in a tool call
+  int64_t req = 0;            // request arrival; JCT once done
+  int64_t fin = 0;            // iteration index at whose end the running request finishes
+  int32_t ctx = 0, gblk = 0, dblk = 0, unc = 0, turn = 0;
+  bool pin = false;
+  int4 rec = make_int4(0, 0, -1, 0);  // current turn record (new, decode, tool, dur)
+
+  int64_t now = 0, iter_end = 0, n_it = 0;
+  bool in_flight = false;
+  int64_t free_blk = a.kv[kv_i];
+  int64_t dfree = dram_on ? E.dram_blocks : 0, chan = 0;
+  int32_t D = 0, turns_done = 0;  // completed programs and their turns (P <= 32)
+  int n_run = 0, n_load = 0;  // n_load counts LOADING and READY
+  int64_t kv_sum = 0, pf = 0;
+  int status = CT_R_OK;
+  // summary counters live in shared memory (lane 0 updates them) to keep registers for occupancy
+  Acc* acc = (Acc*)(stats + F + 1);
+  if (lane == 0) *acc = Acc{0, 0, 0, 0, 0, 0, 0, 0};
+  int64_t busy = 0;
+  // duration of a no-prefill iteration for the current batch (depends on kv_sum only) and its
+  // reciprocal for the macro-step division, recomputed only when kv_sum changes
+  int64_t kv_at = -1, d_cur = 0;
+  double rd_cur = 0.0;
+  // next program-event time computed by the last macro-step plan; valid until an event fires
+  int64_t t_plan = -1;
+
+  // evict(v): free its GPU blocks; DRAM write-through when the tier is on (R18).  Uniform.
+  auto evict = [&](int v) {
+    const int64_t g = __shfl_sync(FULL_MASK, gblk, v);
+    free_blk += g;
+    int32_t keep = 0;
+    if (dram_on) {
+      const uint32_t vctx = __shfl_sync(FULL_MASK, (uint32_t)ctx, v);
+      const int64_t nb = ceil_div_magic(vctx, bsm);
+      dfree += __shfl_sync(FULL_MASK, dblk, v);
+      if (nb > 0 && nb <= dfree) { keep = (int32_t)nb; dfree -= nb; }
+    }
+    if (lane == v) { gblk = 0; dblk = keep; pin = false; texp = CT_INF64; }
+  };
+
+#ifdef CT_DEBUG_LOOPS
+  int64_t dbg_loops = 0, dbg_sched = 0, dbg_macro = 0;
+#endif
+  for (;;) {
+#ifdef CT_DEBUG_LOOPS
+    ++dbg_loops;
+#endif
+    // ---- next event (R1, R3) --------------------------------------------------------------
+    const int64_t t_prog = t_plan >= 0 ? t_plan : warp_min64_redux(eager ? min(tev, texp) : tev);
+    t_plan = -1;
+    int64_t t = t_prog;
+    if (in_flight) t = min(t, iter_end);
+    if (t == CT_INF64) break;
+    now = t;
+
+    if (t_prog == now) {
+      // PinExpiry (EAGER, R4/R15): first µs with now > expiry while not in Q
+      if (eager) {
+        uint32_t m = __ballot_sync(FULL_MASK, texp == now);
+        if (m) {
+          if (lane == 0) acc->exp += __popc(m);
+          if (dram_on) {  // write-through order matters: index order
+            while (m) {
+              const int p = __ffs(m) - 1;
+              m &= m - 1;
+              evict(p);
+            }
+          } else {
+            const bool mine = texp == now;
+            free_blk += (int64_t)__reduce_add_sync(FULL_MASK, mine ? (uint32_t)gblk : 0u);
+            if (mine) { gblk = 0; pin = false; texp = CT_INF64; }
+          }
+        }
+      }
+      const bool due = tev == now;
+      // ToolReturn == OnRequestArrive of a seen program
+      const bool ret = due && st == S_TOOL;
+      if (need_stats) {
+        uint32_t m = __ballot_sync(FULL_MASK, ret);
+        while (m) {  // estimator rows: Δ_obs = dur of the finished turn's tool, clamped (R5)
+          const int p = __ffs(m) - 1;
+          m &= m - 1;
+          const int f = __shfl_sync(FULL_MASK, rec.z, p);
+          const int64_t x = min((int64_t)__shfl_sync(FULL_MASK, rec.w, p), est.b_us);
+          const uint64_t x2 = (uint64_t)x * (uint64_t)x;
+          if (lane == 0) {
+            Stat* rows[2] = {&stats[F], &stats[f]};
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+              Stat* q = rows[k];
+              q->n += 1;
+              q->s1 += x;
+              const uint64_t lo = q->s2lo + x2;
+              q->s2hi += (lo < x2);
+              q->s2lo = lo;
+            }
+          }
+          __syncwarp();
+        }
+      }
+      if (ret) {
+        ++turn;
+        rec = __ldg((const int4*)a.turns + turn0 + turn);
+        st = S_QUEUED;
+        req = now;
+        tev = CT_INF64;
+        texp = CT_INF64;  // a retained pin has no expiry event while waiting
+      }
+      // LoadDone
+      if (due && st == S_LOAD) { st = S_READY; tev = CT_INF64; }
+      // ProgramArrival
+      if (due && st == S_OUT) {
+        st = S_QUEUED;
+        req = now;
+        tev = CT_INF64;
+        rec = __ldg((const int4*)a.turns + turn0);
+      }
+    }
+
+    // IterationEnd: members whose last token was emitted finish, in index order (C-6)
+    if (in_flight && iter_end == now) {
+      in_flight = false;
+      uint32_t m = __ballot_sync(FULL_MASK, st == S_RUN && fin == n_it);
+      while (m) {
+        const int p = __ffs(m) - 1;
+        m &= m - 1;
+        // OnRequestFinish
+        const int pt = __shfl_sync(FULL_MASK, turn, p);
+        const int pn = __shfl_sync(FULL_MASK, nturns, p);
+        const int pg = __shfl_sync(FULL_MASK, gblk, p);
+        const int ptool = __shfl_sync(FULL_MASK, rec.z, p);
+        --n_run;
+        kv_sum -= pg;
+        if (lane == p) ctx += rec.x + rec.y;
+        if (pt == pn - 1) {  // last request: free its KV, the program completes
+          free_blk += pg;
+          dfree += __shfl_sync(FULL_MASK, dblk, p);
+          if (lane == p) { gblk = 0; dblk = 0; st = S_DONE; req = now - arr; }
+          ++D;
+          turns_done += pn;
+        } else {
+          int64_t ttl = 0;
+          switch (pause) {
+            case CT_PAUSE_FIXED:
+            case CT_PAUSE_PAPER: {
+              const Stat sg = stats[F], sf = stats[ptool];
+              ttl = pause == CT_PAUSE_PAPER
+                        ? calc_ttl(sg, sf, est, D, turns_done)
+                        : simplified_ttl(sg, sf, est, polp->t_pin_us, polp->t_thresh_us);
+              break;
+            }
+            case CT_PAUSE_FITTED:
+              ttl = __ldg(&a.fitted[(int64_t)ptool * a.J + min(pt, a.J - 1)]);
+              break;
+            default:
+              ttl = 0;
+          }
+          if (ttl > 0) {  // pin_request only if TTL != 0
+            if (lane == p) { pin = true; texp = now + ttl + 1; }
+          } else {
+            evict(p);
+          }
+          if (lane == p) { tev = now + rec.w; st = S_TOOL; }
+        }
+      }
+    }
+    if (in_flight) continue;  // mid-iteration: events only mutate Q / stats / pins (R2)
+
+    // ---- scheduling point (R3) --------------------------------------------------------------
+#ifdef CT_DEBUG_LOOPS
+    ++dbg_sched;
+#endif
+    // (a) STEP reading: release expired pins of programs not waiting
+    if (!eager) {
+      uint32_t m = __ballot_sync(FULL_MASK, pin && st == S_TOOL && texp <= now);
+      if (lane == 0) acc->exp += __popc(m);
+      while (m) {
+        const int p = __ffs(m) - 1;
+        m &= m - 1;
+        evict(p);
+      }
+    }
+    // fast path: nothing waiting and nothing loaded -> (b)-(d) are no-ops
+    const bool work = __any_sync(FULL_MASK, st == S_QUEUED || st == S_READY);
+    int admitted = 0;
+    bool stable = true;
+    if (work) {
+    // (b) loaded requests join the batch
+    {
+      const bool join = st == S_READY;
+      const uint32_t m = __ballot_sync(FULL_MASK, join);
+      if (m) {
+        kv_sum += (int64_t)__reduce_add_sync(FULL_MASK, join ? (uint32_t)gblk : 0u);
+        pf += (int64_t)__reduce_add_sync(FULL_MASK, join ? (uint32_t)unc : 0u);
+        n_run += __popc(m);
+        n_load -= __popc(m);
+        if (join) { st = S_RUN; fin = n_it + rec.y; }
+      }
+    }
+    // (c) admit loop (victims PAPER.md:645-655)
+    for (;;) {
+      const uint32_t mq = __ballot_sync(FULL_MASK, st == S_QUEUED);
+      if (!mq) break;
+      if (n_run + n_load >= E.max_batch) break;
+      int h;
+      if (prio == CT_PRIO_PROG_FCFS) {
+        const uint32_t mp = __ballot_sync(FULL_MASK, st == S_QUEUED && pin);
+        h = __ffs(mp ? mp : mq) - 1;
+      } else {
+        const bool q = st == S_QUEUED;
+        const int64_t mr = warp_min64_redux(q ? req : CT_INF64);
+        h = __ffs(__ballot_sync(FULL_MASK, q && req == mr)) - 1;
+      }
+      const int32_t hctx = __shfl_sync(FULL_MASK, ctx, h);
+      const int32_t hg = __shfl_sync(FULL_MASK, gblk, h);
+      const int32_t hnew = __shfl_sync(FULL_MASK, rec.x, h);
+      const int32_t hdec = __shfl_sync(FULL_MASK, rec.y, h);
+      const int64_t need = (int64_t)ceil_div_magic((uint32_t)(hctx + hnew + hdec), bsm) - hg;
+      if (need > free_blk && (admitted == 0 || vany)) {
+        while (need > free_blk) {  // victims: latest program arrival first, never the head
+          const uint32_t mv = __ballot_sync(FULL_MASK, pin && lane != h);
+          if (!mv) break;
+          evict(31 - __clz(mv));
+          if (lane == 0) acc->vict += 1;
+        }
+      }
+      if (need > free_blk) {  // HOL break
+        if (admitted > 0 && !vany && __ballot_sync(FULL_MASK, pin && lane != h)) stable = false;
+        break;
+      }
+      // issue h
+      free_blk -= need;
+      const int32_t ng = hg + (int32_t)need;
+      const int64_t hreq = shfl64(req, h);
+      if (lane == 0) acc->bubble += now - hreq;
+      const bool hp = __shfl_sync(FULL_MASK, pin ? 1 : 0, h) != 0;
+      const int32_t hd = __shfl_sync(FULL_MASK, dblk, h);
+      int64_t cached;
+      bool loading = false;
+      int64_t ld = 0;
+      if (hp) {
+        cached = hctx;
+        if (lane == 0) acc->hits += 1;
+      } else if (dram_on && hd > 0 && hd == (int32_t)ceil_div_magic((uint32_t)hctx, bsm)) {
+        cached = hctx;
+        loading = true;
+        ld = max(now, chan) + ceil_ps_to_us((uint64_t)((int64_t)hd * E.c_h2d_ps));
+        chan = ld;
+        if (lane == 0) acc->reload += 1;
+      } else {
+        cached = 0;
+        if (lane == 0) acc->recomp += hctx;
+      }
+      const int64_t u = hctx + hnew - cached;
+      if (lane == 0) acc->prefill += u;
+      if (lane == h) {
+        pin = false;
+        texp = CT_INF64;
+        gblk = ng;
+        unc = (int32_t)u;
+        if (loading) {
+          st = S_LOAD;
+          tev = ld;
+        } else {
+          st = S_RUN;
+          fin = n_it + rec.y;
+        }
+      }
+      if (loading) {
+        ++n_load;
+      } else {
+        ++n_run;
+        kv_sum += ng;
+        pf += u;
+      }
+      ++admitted;
+    }
+    // (d) unschedulable: the head missed with nothing running or loading; the victim loop has
+    // already released every other pin, so no future event can free memory for it (C-5 5c)
+    if (admitted == 0 && n_run == 0 && n_load == 0 && __any_sync(FULL_MASK, st == S_QUEUED)) {
+      status = CT_R_UNSCHEDULABLE;
+      break;
+    }
+    }  // work
+    // (e) start the next iteration(s) (linear cost model, R16)
+    if (n_run > 0) {
+      if (kv_sum != kv_at) {
+        kv_at = kv_sum;
+        d_cur = ceil_ps_to_us((uint64_t)(E.c0_ps + E.c_kv_ps * bs * kv_sum));
+        rd_cur = 1.0 / (double)d_cur;
+      }
+      const int64_t d = d_cur;
+      int64_t k = 1, dur;
+      if (pf > 0) {
+        dur = ceil_ps_to_us((uint64_t)(E.c0_ps + E.c_kv_ps * bs * kv_sum + E.c_pf_ps * pf));
+        pf = 0;
+      } else {
+        if (stable) {
+          // macro-step: identical iterations up to the first finish or the first boundary at
+          // or after the next external event (arrival, tool return, load done, pin expiry)
+          const int64_t mfin = warp_min64_redux(st == S_RUN ? fin : CT_INF64);
+          const int64_t te = warp_min64_redux(min(tev, texp));
+          if (eager) t_plan = te;  // = the next loop's program-event minimum (nothing changes)
+          const int64_t m = mfin - n_it;
+          int64_t j = m;
+          if (te != CT_INF64) {
+            const int64_t gap2 = te - now;  // >= 1
+            const double estq = (double)gap2 * rd_cur;
+            if (estq < (double)m + 2.0) {
+              int64_t jb = (int64_t)estq;
+              while (jb * d < gap2) ++jb;
+              while (jb > 1 && (jb - 1) * d >= gap2) --jb;
+              if (jb < j) j = jb;
+            }
+          }
+          k = j;
+#ifdef CT_DEBUG_LOOPS
+          ++dbg_macro;
+#endif
+        }
+        dur = k * d;
+      }
+      if (n_it + k > E.max_iters) { status = CT_R_EVENT_BUDGET; break; }
+      n_it += k;
+      iter_end = now + dur;
+      busy += dur;
+      in_flight = true;
+    }
+  }
+  if (status == CT_R_OK && D != P) status = CT_R_UNSCHEDULABLE;
+
+  // ---- per-replica summary (A-8) --------------------------------------------------------------
+  const int64_t ri = r - a.r_begin;
+  int64_t jsum = 0, jmax = 0, p50 = 0, p99 = 0;
+  if (status == CT_R_OK) {
+    const int64_t jv = live ? req : 0;
+    jsum = (int64_t)warp_sum_u64((uint64_t)jv);
+    jmax = warp_max64(jv);
+    const int r50 = (50 * P + 99) / 100, r99 = (99 * P + 99) / 100;
+    int lt = 0, le = 0;
+    for (int q = 0; q < P; ++q) {
+      const int64_t x = shfl64(req, q);
+      lt += x < req;
+      le += x <= req;
+    }
+    const bool c5 = live && lt < r50 && r50 <= le, c9 = live && lt < r99 && r99 <= le;
+    p50 = shfl64(req, __ffs(__ballot_sync(FULL_MASK, c5)) - 1);
+    p99 = shfl64(req, __ffs(__ballot_sync(FULL_MASK, c9)) - 1);
+  }
+  if (lane == 0) {
+    ct_replica_summary o;
+    if (status == CT_R_OK) {
+      o.status = status;
+      o.n_done = D;
+      o.turns_done = turns_done;
+      o.sum_jct_us = jsum;
+      o.max_jct_us = jmax;
+      o.p50_jct_us = p50;
+      o.p99_jct_us = p99;
+      o.sum_bubble_us = acc->bubble;
+      o.makespan_us = now - arr0;  // the last event processed is the last completion
+      o.iterations = n_it;
+      o.busy_us = busy;
+      o.prefill_tokens = acc->prefill;
+      o.recompute_tokens = acc->recomp;
+      o.pin_hits = acc->hits;
+      o.pin_expiries = acc->exp;
+      o.victims = acc->vict;
+      o.reloads = acc->reload;
+#ifdef CT_DEBUG_LOOPS
+      o.reloads = dbg_loops;
+      o.victims = dbg_sched;
+      o.pin_hits = dbg_macro;
+#endif
+    } else {
+      int64_t* w = (int64_t*)&o;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) w[i] = 0;
+      o.status = status;
+    }
+    a.out[ri] = o;
+  }
+  if (a.jct && live) a.jct[ri * P + lane] = status == CT_R_OK ? req : -1;
+  __syncwarp();
+}
+
+template <int NS, int MINB>
+__global__ void __launch_bounds__(128, MINB) replay_kernel(ReplayArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x & 31;
   unsigned char* wm = smem + (threadIdx.x >> 5) * a.smem_per_warp;
@@ -558,19 +1005,36 @@ __global__ void __launch_bounds__(256) replay_kernel(ReplayArgs a) {
     idx = __shfl_sync(FULL_MASK, idx, 0);
     const int64_t r = a.r_begin + (int64_t)idx;
     if (r >= a.r_end) break;
-    replay_one<NS>(a, r, wm, lane);
+    if (NS == 1)
+      replay_one_w32(a, r, (Stat*)wm, lane);
+    else
+      replay_one<NS>(a, r, wm, lane);
   }
 }
 
-template <int NS>
-static void* kernel_ptr() { return (void*)replay_kernel<NS>; }
+// P <= 32 variants differ only in the register budget (min resident CTAs of 4 warps per SM);
+// CT_REPLAY_MINB selects one for experiments, the default is the measured best.
+static int g_minb = -1;
+static int minb() {
+  if (g_minb < 0) {
+    const char* e = getenv("CT_REPLAY_MINB");
+    g_minb = e ? atoi(e) : 8;
+  }
+  return g_minb;
+}
 
 static void* pick(int ns) {
   switch (ns) {
-    case 1: return kernel_ptr<1>();
-    case 2: return kernel_ptr<2>();
-    case 4: return kernel_ptr<4>();
-    case 8: return kernel_ptr<8>();
+    case 1:
+      switch (minb()) {
+        case 6: return (void*)replay_kernel<1, 6>;
+        case 10: return (void*)replay_kernel<1, 10>;
+        case 12: return (void*)replay_kernel<1, 12>;
+        default: return (void*)replay_kernel<1, 8>;
+      }
+    case 2: return (void*)replay_kernel<2, 1>;
+    case 4: return (void*)replay_kernel<4, 1>;
+    case 8: return (void*)replay_kernel<8, 1>;
   }
   return nullptr;
 }
