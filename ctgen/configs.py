@@ -14,8 +14,8 @@ import numpy as np
 from . import traces
 
 # ---- enums shared by the binary contract (values fixed in include/continuum.h) ----
-PRIO_PROG_FCFS, PRIO_REQ_FCFS = 0, 1
-PAUSE_EVICT, PAUSE_FIXED, PAUSE_PAPER, PAUSE_FITTED = 0, 1, 2, 3
+PRIO_PROG_FCFS, PRIO_REQ_FCFS, PRIO_PLAS = 0, 1, 2
+PAUSE_EVICT, PAUSE_FIXED, PAUSE_PAPER, PAUSE_FITTED, PAUSE_INFERCEPT = 0, 1, 2, 3, 4
 FLAG_VICTIMS_ANY = 1      # reading R13 alternative: victims whenever the head does not fit
 FLAG_STEP_EXPIRY = 2      # reading R4 alternative: release pins only at scheduling points
 ALWAYS = (1 << 63) - 1    # T_thresh sentinel: pin unconditionally (TTL grid policy)
@@ -91,6 +91,10 @@ VLLM_LMCACHE = Policy(PRIO_REQ_FCFS, PAUSE_EVICT, dram=1)
 PROG_FCFS = Policy(PRIO_PROG_FCFS, PAUSE_EVICT)
 CONTINUUM = Policy(PRIO_PROG_FCFS, PAUSE_PAPER)
 CONTINUUM_FITTED = Policy(PRIO_PROG_FCFS, PAUSE_FITTED)
+# comparison systems of the paper's evaluation (NEXT-1): Autellix PLAS and
+# InferCept preserve/swap/evict on vLLM's request FCFS
+AUTELLIX = Policy(PRIO_PLAS, PAUSE_EVICT)
+INFERCEPT = Policy(PRIO_REQ_FCFS, PAUSE_INFERCEPT, dram=1)
 
 
 def ttl_grid(tau_us: int) -> Policy:

@@ -47,12 +47,19 @@ extern "C" {
 /* priority (PAPER.md:535-551 for PROG_FCFS; vanilla vLLM request FCFS PAPER.md:272) */
 #define CT_PRIO_PROG_FCFS 0   /* key (not pinned, program index): pinned first, then FCFS */
 #define CT_PRIO_REQ_FCFS 1    /* key (request arrival time, program index) */
+#define CT_PRIO_PLAS 2        /* Autellix PLAS: key (attained engine time of
+                                 the program, program index); every running request accrues
+                                 each iteration's duration */
 
 /* pause action on a non-final finish */
 #define CT_PAUSE_EVICT 0      /* free KV at once (vanilla vLLM) */
 #define CT_PAUSE_FIXED 1      /* §4.5 simplified: pin T_pin iff mean < T_thresh */
 #define CT_PAUSE_PAPER 2      /* Alg. 1 CalcTTL with the online empirical-Bernstein bound */
 #define CT_PAUSE_FITTED 3     /* table lookup ttl[tool][turn bucket] from ct_fit_ttl */
+#define CT_PAUSE_INFERCEPT 4  /* InferCept: preserve without TTL iff the
+                                 predicted tool time (tool mean if |S_f| >= N, else global mean,
+                                 else T_default) < swap round trip 2 ceil(ceil(ctx/bs) c_h2d / 1e6);
+                                 else evict (DRAM write-through = swap when policy.dram = 1) */
 
 #define CT_FLAG_VICTIMS_ANY 1 /* DESIGN.md R13 alternative: victims whenever the head misses */
 #define CT_FLAG_STEP_EXPIRY 2 /* DESIGN.md R4 alternative: release only at scheduling points */

@@ -108,6 +108,20 @@ int64_t or_simplified(const int64_t* g, const int64_t* f, const int64_t* est, in
   return mu < t_thresh ? t_pin : 0;
 }
 
+// InferCept: predicted tool time = mean of the tool
+// when |S_f| >= N, else the global mean when |S| >= 1, else T_default.
+int64_t or_infercept_predict(const int64_t* g, const int64_t* f, const int64_t* est) {
+  if (f[0] >= est[3]) return f[1] / f[0];
+  if (g[0] >= 1) return g[1] / g[0];
+  return est[2];
+}
+
+// Swap round trip of a context: out + in, each ceil(blocks * c_h2d / 1e6) µs, blocks = ceil(ctx/bs).
+int64_t or_infercept_swap_us(int64_t ctx, int64_t bs, int64_t c_h2d_ps) {
+  int64_t blocks = ceil_div(ctx, bs);
+  return 2 * ceil_div((i128)blocks * c_h2d_ps, 1000000);
+}
+
 // ---------------------------------------------------------------------------
 // TTL fit (extension C-4): plain definition over raw samples.
 // ---------------------------------------------------------------------------
@@ -177,8 +191,8 @@ int or_fit(const int32_t* dur, const int64_t* tool_off, int F, const int64_t* co
 namespace {
 
 enum { NOT_ARRIVED = 0, QUEUED = 1, RUNNING = 2, LOADING = 3, READY = 4, TOOL = 5, DONE = 6 };
-enum { PRIO_PROG_FCFS = 0, PRIO_REQ_FCFS = 1 };
-enum { PAUSE_EVICT = 0, PAUSE_FIXED = 1, PAUSE_PAPER = 2, PAUSE_FITTED = 3 };
+enum { PRIO_PROG_FCFS = 0, PRIO_REQ_FCFS = 1, PRIO_PLAS = 2 };
+enum { PAUSE_EVICT = 0, PAUSE_FIXED = 1, PAUSE_PAPER = 2, PAUSE_FITTED = 3, PAUSE_INFERCEPT = 4 };
 enum { FLAG_VICTIMS_ANY = 1, FLAG_STEP_EXPIRY = 2 };
 enum { ST_OK = 0, ST_UNSCHED = 1, ST_BUDGET = 2, ST_INVARIANT = -1 };
 
@@ -189,6 +203,7 @@ struct Prog {
   bool pinned = false;
   int64_t expiry = 0, req_arr = 0, t_ret = 0, load_done = 0, emitted = 0;
   int64_t arrival = 0, completion = -1;
+  int64_t service = 0;  // attained engine time (Autellix PLAS)
   bool first = false;
 };
 
@@ -261,6 +276,11 @@ struct Sim {
         int j = p[i].turn < J - 1 ? p[i].turn : J - 1;
         return fitted[(int64_t)f * J + j];
       }
+      case PAUSE_INFERCEPT: {  // preserve (no TTL) iff predicted tool time < swap round trip
+        int64_t pred = or_infercept_predict(g, fr, est);
+        int64_t swap = or_infercept_swap_us(p[i].ctx, eng[4], eng[3]);
+        return pred < swap ? INF : 0;
+      }
     }
     return 0;
   }
@@ -277,7 +297,7 @@ struct Sim {
     }
     int64_t ttl = ttl_for(i);
     if (ttl > 0) {  // pin_request(request, TTL) only if TTL != 0
-      p[i].pinned = true; p[i].expiry = now + ttl; pins_created++;
+      p[i].pinned = true; p[i].expiry = ttl == INF ? INF : now + ttl; pins_created++;
     } else {
       evict(i);
     }
@@ -290,9 +310,12 @@ struct Sim {
     if (pol[0] == PRIO_PROG_FCFS) {
       for (int i = 0; i < P; ++i) if (p[i].st == QUEUED && p[i].pinned) return i;
       for (int i = 0; i < P; ++i) if (p[i].st == QUEUED) return i;
-    } else {
+    } else if (pol[0] == PRIO_REQ_FCFS) {
       for (int i = 0; i < P; ++i)
         if (p[i].st == QUEUED && (best < 0 || p[i].req_arr < p[best].req_arr)) best = i;
+    } else {  // PLAS: least attained service first, ties by program arrival
+      for (int i = 0; i < P; ++i)
+        if (p[i].st == QUEUED && (best < 0 || p[i].service < p[best].service)) best = i;
     }
     return best;
   }
@@ -383,6 +406,8 @@ struct Sim {
       in_flight = true;
       iterations++;
       busy += dur;
+      for (int i = 0; i < P; ++i)
+        if (p[i].st == RUNNING) p[i].service += dur;  // PLAS attained service
     }
     return true;
   }
@@ -416,7 +441,7 @@ struct Sim {
       for (int i = 0; i < P; ++i) {
         if (p[i].st == TOOL) {
           t = std::min(t, p[i].t_ret);
-          if (p[i].pinned && eager()) t = std::min(t, p[i].expiry + 1);
+          if (p[i].pinned && eager() && p[i].expiry != INF) t = std::min(t, p[i].expiry + 1);
         }
         if (p[i].st == LOADING) t = std::min(t, p[i].load_done);
       }
@@ -429,7 +454,7 @@ struct Sim {
       // PinExpiry: first instant with now > expiry, program not in Q
       if (eager())
         for (int i = 0; i < P; ++i)
-          if (p[i].st == TOOL && p[i].pinned && p[i].expiry + 1 == now) {
+          if (p[i].st == TOOL && p[i].pinned && p[i].expiry != INF && p[i].expiry + 1 == now) {
             evict(i); p[i].pinned = false; expiries++;
           }
       // ToolReturn = OnRequestArrive of a seen program

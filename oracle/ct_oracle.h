@@ -38,6 +38,10 @@ int64_t or_calc_ttl(const int64_t* g, const int64_t* f, const int64_t* est,
 int64_t or_simplified(const int64_t* g, const int64_t* f, const int64_t* est,
                       int64_t t_pin, int64_t t_thresh);
 
+/* InferCept baseline (NEXT-1): predicted tool time and swap round trip (µs). */
+int64_t or_infercept_predict(const int64_t* g, const int64_t* f, const int64_t* est);
+int64_t or_infercept_swap_us(int64_t ctx, int64_t bs, int64_t c_h2d_ps);
+
 /* TTL fit (extension C-4 + paper-mode C-2 per tool).
  * dur[n] grouped by tool, tool_off[F+1]; cost = {c_pf, c_pin, bs, a_num, a_den,
  * delta_us, K, J}; ctx_j[J], w_j[J]; est = estimator vector; avg = {turns_done, n_done}.

@@ -46,6 +46,10 @@ def lib():
         _lib.or_calc_ttl.argtypes = [p, p, p, i64, i64]
         _lib.or_simplified.restype = i64
         _lib.or_simplified.argtypes = [p, p, p, i64, i64]
+        _lib.or_infercept_predict.restype = i64
+        _lib.or_infercept_predict.argtypes = [p, p, p]
+        _lib.or_infercept_swap_us.restype = i64
+        _lib.or_infercept_swap_us.argtypes = [i64, i64, i64]
         _lib.or_fit.restype = C.c_int
         _lib.or_fit.argtypes = [p, p, C.c_int, p, p, p, p, p, p, p, p]
         _lib.or_simulate.restype = C.c_int
@@ -98,6 +102,15 @@ def calc_ttl(g, f, est, n_done: int, turns_done: int) -> int:
 def simplified(g, f, est, t_pin: int, t_thresh: int) -> int:
     g, f, est = _i64(g), _i64(f), _i64(est)
     return int(lib().or_simplified(_ptr(g), _ptr(f), _ptr(est), t_pin, t_thresh))
+
+
+def infercept_predict(g, f, est) -> int:
+    g, f, est = _i64(g), _i64(f), _i64(est)
+    return int(lib().or_infercept_predict(_ptr(g), _ptr(f), _ptr(est)))
+
+
+def infercept_swap_us(ctx: int, bs: int, c_h2d_ps: int) -> int:
+    return int(lib().or_infercept_swap_us(ctx, bs, c_h2d_ps))
 
 
 def fit(dur: np.ndarray, tool_off: np.ndarray, cost, ctx_j, w_j, est, avg=(0, 0)):

@@ -173,14 +173,15 @@ int ct_simulate_batch(ct_ctx* c, const ct_trace_set* tr, const ct_sweep* sw,
   bool need_est = false, need_fit = false, need_h2d = false;
   for (int i = 0; i < sw->n_policies; ++i) {
     const ct_policy& p = sw->policies[i];
-    if (p.priority != CT_PRIO_PROG_FCFS && p.priority != CT_PRIO_REQ_FCFS)
+    if (p.priority < CT_PRIO_PROG_FCFS || p.priority > CT_PRIO_PLAS)
       return fail(CT_EINVAL, "policy %d: priority %d", i, p.priority);
-    if (p.pause < CT_PAUSE_EVICT || p.pause > CT_PAUSE_FITTED)
+    if (p.pause < CT_PAUSE_EVICT || p.pause > CT_PAUSE_INFERCEPT)
       return fail(CT_EINVAL, "policy %d: pause %d", i, p.pause);
     if (p.flags & ~(CT_FLAG_VICTIMS_ANY | CT_FLAG_STEP_EXPIRY))
       return fail(CT_EINVAL, "policy %d: unknown flags", i);
     if (p.t_pin_us < 0 || p.t_pin_us >= (1ll << 50)) return fail(CT_EINVAL, "policy %d: t_pin", i);
-    need_est |= p.pause == CT_PAUSE_PAPER || (p.pause == CT_PAUSE_FIXED && p.t_thresh_us != CT_ALWAYS);
+    need_est |= p.pause == CT_PAUSE_PAPER || p.pause == CT_PAUSE_INFERCEPT ||
+                (p.pause == CT_PAUSE_FIXED && p.t_thresh_us != CT_ALWAYS);
     need_fit |= p.pause == CT_PAUSE_FITTED;
     need_h2d |= p.dram != 0 && E.dram_blocks > 0;
   }

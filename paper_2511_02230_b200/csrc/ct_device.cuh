@@ -134,4 +134,13 @@ __device__ __forceinline__ int64_t simplified_ttl(const Stat& g, const Stat& f,
   return mu < t_thresh ? t_pin : 0;
 }
 
+// InferCept: predicted tool time = mean of the tool when |S_f| >= N,
+// else the global mean when |S| >= 1, else T_default.
+__device__ __forceinline__ int64_t infercept_predict(const Stat& g, const Stat& f,
+                                                     const ct_estimator_params& e) {
+  if (f.n >= e.n_min) return f.s1 / f.n;
+  if (g.n >= 1) return g.s1 / g.n;
+  return e.t_default_us;
+}
+
 }  // namespace ct

@@ -22,7 +22,7 @@ enum : int { S_OUT = 0, S_QUEUED = 1, S_RUN = 2, S_LOAD = 3, S_READY = 4, S_TOOL
 int replay_smem_per_warp(int ns, int F) {
   if (ns == 1) return (32 * (F + 1) + 48 + 15) & ~15;  // registers hold the programs; SMEM: estimator + Acc
   int pm = 32 * ns;
-  int b = 53 * pm;
+  int b = 61 * pm;
   b = (b + 15) & ~15;
   b += 32 * (F + 1);
   return (b + 15) & ~15;
@@ -41,8 +41,9 @@ __device__ __forceinline__ void replay_one(const ReplayArgs& a, int64_t r, unsig
   int32_t* dblk = gblk + PM;              // DRAM copy blocks
   int32_t* unc = dblk + PM;               // uncached tokens of the current request
   int32_t* turn = unc + PM;               // current turn
-  uint8_t* st = (uint8_t*)(turn + PM);    // lifecycle state
-  Stat* stats = (Stat*)(wm + ((53 * PM + 15) & ~15));  // [F] per tool, [F] = global
+  int64_t* svc = (int64_t*)(turn + PM);   // attained engine time (PLAS)
+  uint8_t* st = (uint8_t*)(svc + PM);     // lifecycle state
+  Stat* stats = (Stat*)(wm + ((61 * PM + 15) & ~15));  // [F] per tool, [F] = global
 
   const int P = a.P, F = a.F;
   const int64_t npol = a.n_pol, nkv = a.n_kv, nrate = a.n_rate;
@@ -64,8 +65,9 @@ __device__ __forceinline__ void replay_one(const ReplayArgs& a, int64_t r, unsig
   const bool eager = (pol.flags & CT_FLAG_STEP_EXPIRY) == 0;
   const bool vany = (pol.flags & CT_FLAG_VICTIMS_ANY) != 0;
   const bool dram_on = pol.dram != 0 && E.dram_blocks > 0;
-  const bool need_stats = pol.pause == CT_PAUSE_PAPER ||
+  const bool need_stats = pol.pause == CT_PAUSE_PAPER || pol.pause == CT_PAUSE_INFERCEPT ||
                           (pol.pause == CT_PAUSE_FIXED && pol.t_thresh_us != CT_ALWAYS);
+  const bool plas = pol.priority == CT_PRIO_PLAS;
 
 #pragma unroll
   for (int s = 0; s < NS; ++s) {
@@ -79,6 +81,7 @@ __device__ __forceinline__ void replay_one(const ReplayArgs& a, int64_t r, unsig
     dblk[p] = 0;
     unc[p] = 0;
     turn[p] = 0;
+    svc[p] = 0;
     st[p] = S_OUT;
   }
   if (need_stats)
@@ -259,11 +262,18 @@ __device__ __forceinline__ void replay_one(const ReplayArgs& a, int64_t r, unsig
               case CT_PAUSE_FITTED:
                 ttl = __ldg(&a.fitted[(int64_t)f * a.J + min(tp, a.J - 1)]);
                 break;
+              case CT_PAUSE_INFERCEPT: {  // preserve (no TTL) iff prediction < swap round trip
+                const int64_t pred = infercept_predict(stats[F], stats[f], est);
+                const int64_t blocks = ceil_div_magic((uint32_t)nctx, bsm);
+                const int64_t swap = 2 * ceil_ps_to_us((uint64_t)(blocks * E.c_h2d_ps));
+                ttl = pred < swap ? CT_INF64 : 0;
+                break;
+              }
               default:
                 ttl = 0;
             }
             if (ttl > 0) {  // pin_request only if TTL != 0
-              if (own(p)) { pb |= bit(p); t_exp[p] = now + ttl + 1; }
+              if (own(p)) { pb |= bit(p); t_exp[p] = ttl == CT_INF64 ? CT_INF64 : now + ttl + 1; }
             } else {
               evict(p);
             }
@@ -335,7 +345,7 @@ __device__ __forceinline__ void replay_one(const ReplayArgs& a, int64_t r, unsig
         for (int s = 0; s < NS; ++s) {
           int pl = lane + 32 * s;
           if ((qb >> s) & 1u) {
-            int64_t k = req[pl];
+            int64_t k = plas ? svc[pl] : req[pl];  // PLAS: least attained service
             if (k < bk || (k == bk && pl < bp)) { bk = k; bp = pl; }
           }
         }
@@ -472,6 +482,11 @@ __device__ __forceinline__ void replay_one(const ReplayArgs& a, int64_t r, unsig
       n_it += k;
       iter_end = now + dur;
       c_busy += dur;
+      if (plas) {
+#pragma unroll
+        for (int s = 0; s < NS; ++s)
+          if ((rb >> s) & 1u) svc[lane + 32 * s] += dur;  // owners accrue their own programs
+      }
       in_flight = true;
     }
   }
@@ -588,8 +603,9 @@ __device__ __forceinline__ void replay_one_w32(const ReplayArgs& a, int64_t r, S
   const bool eager = (pflags & CT_FLAG_STEP_EXPIRY) == 0;
   const bool vany = (pflags & CT_FLAG_VICTIMS_ANY) != 0;
   const bool dram_on = polp->dram != 0 && E.dram_blocks > 0;
-  const bool need_stats = pause == CT_PAUSE_PAPER ||
+  const bool need_stats = pause == CT_PAUSE_PAPER || pause == CT_PAUSE_INFERCEPT ||
                           (pause == CT_PAUSE_FIXED && polp->t_thresh_us != CT_ALWAYS);
+  const bool plas = prio == CT_PRIO_PLAS;
   if (need_stats) {
     for (int i = lane; i < 4 * (F + 1); i += 32) ((int64_t*)stats)[i] = 0;
     __syncwarp();
@@ -613,6 +629,7 @@ __device__ __forceinline__ void replay_one_w32(const ReplayArgs& a, int64_t r, S
   int64_t fin = 0;            // iteration index at whose end the running request finishes
   int32_t ctx = 0, gblk = 0, dblk = 0, unc = 0, turn = 0;
   bool pin = false;
+  int64_t svc = 0;  // attained engine time of the program (PLAS)
   int4 rec = make_int4(0, 0, -1, 0);  // current turn record (new, decode, tool, dur)
 
   int64_t now = 0, iter_end = 0, n_it = 0;
@@ -762,11 +779,19 @@ __device__ __forceinline__ void replay_one_w32(const ReplayArgs& a, int64_t r, S
             case CT_PAUSE_FITTED:
               ttl = __ldg(&a.fitted[(int64_t)ptool * a.J + min(pt, a.J - 1)]);
               break;
+            case CT_PAUSE_INFERCEPT: {  // preserve (no TTL) iff prediction < swap round trip
+              const int64_t pred = infercept_predict(stats[F], stats[ptool], est);
+              const uint32_t pctx = __shfl_sync(FULL_MASK, (uint32_t)ctx, p);
+              const int64_t blocks = ceil_div_magic(pctx, bsm);
+              const int64_t swap = 2 * ceil_ps_to_us((uint64_t)(blocks * E.c_h2d_ps));
+              ttl = pred < swap ? CT_INF64 : 0;
+              break;
+            }
             default:
               ttl = 0;
           }
           if (ttl > 0) {  // pin_request only if TTL != 0
-            if (lane == p) { pin = true; texp = now + ttl + 1; }
+            if (lane == p) { pin = true; texp = ttl == CT_INF64 ? CT_INF64 : now + ttl + 1; }
           } else {
             evict(p);
           }
@@ -816,10 +841,11 @@ __device__ __forceinline__ void replay_one_w32(const ReplayArgs& a, int64_t r, S
       if (prio == CT_PRIO_PROG_FCFS) {
         const uint32_t mp = __ballot_sync(FULL_MASK, st == S_QUEUED && pin);
         h = __ffs(mp ? mp : mq) - 1;
-      } else {
+      } else {  // REQ_FCFS: earliest request; PLAS: least attained service; ties: index
         const bool q = st == S_QUEUED;
-        const int64_t mr = warp_min64_redux(q ? req : CT_INF64);
-        h = __ffs(__ballot_sync(FULL_MASK, q && req == mr)) - 1;
+        const int64_t key = plas ? svc : req;
+        const int64_t mr = warp_min64_redux(q ? key : CT_INF64);
+        h = __ffs(__ballot_sync(FULL_MASK, q && key == mr)) - 1;
       }
       const int32_t hctx = __shfl_sync(FULL_MASK, ctx, h);
       const int32_t hg = __shfl_sync(FULL_MASK, gblk, h);
@@ -934,6 +960,7 @@ __device__ __forceinline__ void replay_one_w32(const ReplayArgs& a, int64_t r, S
       n_it += k;
       iter_end = now + dur;
       busy += dur;
+      if (plas && st == S_RUN) svc += dur;  // every running request accrues the iterations
       in_flight = true;
     }
   }

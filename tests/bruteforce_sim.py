@@ -20,6 +20,9 @@ import math
 from oracle import oracle as O  # the TTL formula itself is pinned separately
 
 
+NEVER = 1 << 80  # a preserved pin has no expiry
+
+
 def simulate(trace, gap_us, kv, pol, est, eng, fitted=None, horizon=200000):
     P = trace.n_programs
     progs = trace.programs
@@ -39,7 +42,8 @@ def simulate(trace, gap_us, kv, pol, est, eng, fitted=None, horizon=200000):
 
     # per-program state as plain dicts
     S = [dict(where="out", turn=0, ctx=0, blk=0, dblk=0, pin=None, waited_since=None,
-              tool_back=None, load_at=None, left=0, fresh=0, done_at=None) for _ in range(P)]
+              tool_back=None, load_at=None, left=0, fresh=0, done_at=None, served=0)
+         for _ in range(P)]
     free = kv
     dfree = dram_cap if dram_on else 0
     chan = 0
@@ -78,6 +82,10 @@ def simulate(trace, gap_us, kv, pol, est, eng, fitted=None, horizon=200000):
             return O.simplified(as_row(row("g")), as_row(row(f)), est, t_pin, t_thresh)
         if pause == 2:
             return O.calc_ttl(as_row(row("g")), as_row(row(f)), est, n_done, turns_done)
+        if pause == 4:  # InferCept: preserve without TTL iff predicted tool time < swap round trip
+            pred = O.infercept_predict(as_row(row("g")), as_row(row(f)), est)
+            swap = O.infercept_swap_us(S[i]["ctx"], bs, ch2d)
+            return NEVER if pred < swap else 0
         return int(fitted[f][min(k, fitted.shape[1] - 1)])
 
     now = 0
@@ -139,7 +147,7 @@ def simulate(trace, gap_us, kv, pol, est, eng, fitted=None, horizon=200000):
                     else:
                         ttl = pause_ttl(i)
                         if ttl > 0:
-                            s["pin"] = now + ttl
+                            s["pin"] = NEVER if ttl == NEVER else now + ttl
                         else:
                             drop(i)
                         s["tool_back"] = now + d
@@ -159,8 +167,10 @@ def simulate(trace, gap_us, kv, pol, est, eng, fitted=None, horizon=200000):
                 if prio == 0:
                     pinned_w = [i for i in waiting if S[i]["pin"] is not None]
                     h = min(pinned_w) if pinned_w else min(waiting)
-                else:
+                elif prio == 1:
                     h = min(waiting, key=lambda i: (S[i]["waited_since"], i))
+                else:  # Autellix PLAS: least attained engine time first
+                    h = min(waiting, key=lambda i: (S[i]["served"], i))
                 s = S[h]
                 new, dec, _, _ = rec(h, s["turn"])
                 total = -(-(s["ctx"] + new + dec) // bs)
@@ -213,6 +223,8 @@ def simulate(trace, gap_us, kv, pol, est, eng, fitted=None, horizon=200000):
                     S[i]["fresh"] = 0
                 dur = -(-ps // 10**6)
                 engine_until = now + dur
+                for i in batch:
+                    S[i]["served"] += dur
                 cnt["iters"] += 1
                 cnt["busy"] += dur
         if n_done == P:

@@ -79,8 +79,8 @@ def random_tiny_set(rng, n_seeds, P=3, n_tools=2):
 def random_policies(rng, n):
     out = []
     for _ in range(n):
-        out.append(cf.Policy(priority=rng.choice([0, 0, 1]),
-                             pause=rng.choice([0, 1, 1, 2, 3]), dram=rng.choice([0, 1]),
+        out.append(cf.Policy(priority=rng.choice([0, 0, 1, 2]),
+                             pause=rng.choice([0, 1, 1, 2, 3, 4]), dram=rng.choice([0, 1]),
                              flags=rng.choice([0, 0, 1, 2, 3]), t_pin_us=rng.randint(0, 30),
                              t_thresh_us=rng.choice([cf.ALWAYS, rng.randint(1, 30)])))
     return out
@@ -110,7 +110,10 @@ ALL_POLICIES = [cf.VLLM, cf.VLLM_LMCACHE, cf.PROG_FCFS, cf.CONTINUUM, cf.ttl_gri
                 cf.Policy(cf.PRIO_PROG_FCFS, cf.PAUSE_FIXED, flags=cf.FLAG_VICTIMS_ANY,
                           t_pin_us=20_000_000),
                 cf.Policy(cf.PRIO_REQ_FCFS, cf.PAUSE_FITTED, dram=1),
-                cf.Policy(cf.PRIO_PROG_FCFS, cf.PAUSE_FITTED, flags=cf.FLAG_STEP_EXPIRY)]
+                cf.Policy(cf.PRIO_PROG_FCFS, cf.PAUSE_FITTED, flags=cf.FLAG_STEP_EXPIRY),
+                cf.AUTELLIX, cf.INFERCEPT,
+                cf.Policy(cf.PRIO_PLAS, cf.PAUSE_PAPER, dram=1),
+                cf.Policy(cf.PRIO_PROG_FCFS, cf.PAUSE_INFERCEPT, flags=cf.FLAG_STEP_EXPIRY)]
 
 
 @pytest.mark.parametrize("P", [1, 7, 32, 33, 64, 100, 128, 200, 256])

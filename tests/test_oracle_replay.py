@@ -175,13 +175,13 @@ def random_tiny(rng):
 
 def random_policy(rng):
     pause = rng.choice([cf.PAUSE_EVICT, cf.PAUSE_FIXED, cf.PAUSE_FIXED, cf.PAUSE_PAPER,
-                        cf.PAUSE_FITTED])
-    return cf.Policy(priority=rng.choice([0, 0, 1]), pause=pause, dram=rng.choice([0, 1]),
+                        cf.PAUSE_FITTED, cf.PAUSE_INFERCEPT])
+    return cf.Policy(priority=rng.choice([0, 0, 1, 2]), pause=pause, dram=rng.choice([0, 1]),
                      flags=rng.choice([0, 0, cf.FLAG_VICTIMS_ANY]), t_pin_us=rng.randint(0, 30),
                      t_thresh_us=rng.choice([cf.ALWAYS, cf.ALWAYS, rng.randint(1, 30)]))
 
 
-@pytest.mark.parametrize("seed", range(4))
+@pytest.mark.parametrize("seed", range(6))
 def test_bruteforce_tiny(seed):
     rng = random.Random(100 + seed)
     agree = 0
@@ -291,3 +291,79 @@ def test_event_budget_status():
     eng = cf.Engine(**{**UNIT.__dict__, "max_iters": 10})
     s, j = run(tr, cf.PROG_FCFS, 100, eng=eng)
     assert O.status(s) == cf.STATUS_EVENT_BUDGET
+
+
+# ---------------------------------------------------------------------------------------------
+# NEXT-1 comparison systems: InferCept and Autellix PLAS
+# ---------------------------------------------------------------------------------------------
+def test_infercept_spec_decisions():
+    """predicted 0.2 s vs round trip 1.0 s -> preserve; 30 s -> swap / evict."""
+    e = cf.Estimator(n_min=1).as_array()
+    g_short = O.stats_row([200_000] * 4)
+    g_long = O.stats_row([30_000_000] * 4)
+    assert O.infercept_predict(g_short, g_short, e) == 200_000
+    assert O.infercept_predict(g_long, g_long, e) == 30_000_000
+    # round trip 1.0 s: 25 blocks (400 tokens, bs 16) at 20 ms per block each way
+    assert O.infercept_swap_us(400, 16, 20_000_000_000) == 1_000_000
+    assert O.infercept_predict(g_short, g_short, e) < 1_000_000 < O.infercept_predict(g_long, g_long, e)
+    # empty statistics fall back to T_default (SPEC.md:480)
+    g0 = O.stats_row([])
+    assert O.infercept_predict(g0, g0, e) == cf.Estimator().t_def_us
+
+
+def test_infercept_replay_preserve_swap_evict():
+    # one program, 2 turns; context 12 tokens, bs 1; c_h2d 5e5 ps/block -> round trip 12 µs
+    eng = cf.Engine(**{**UNIT.__dict__, "dram_blocks": 1000})
+    est = cf.Estimator(t_def_us=5, n_min=1)  # cold start predicts T_default = 5 µs < 12 µs
+    tr = traces.tiny([(0, [(10, 2, 0, 30), (3, 1, -1, 0)])])
+    s, j = run(tr, cf.INFERCEPT, 100, eng=eng, est=est)
+    # preserved despite a 30 µs tool (no TTL): hit at 42, 42->46
+    assert list(j) == [46] and s[12] == 1 and s[13] == 0
+    # prediction 20 µs >= 12 µs -> swap out (write-through), reload 42->48, iteration 48->52
+    s, j = run(tr, cf.INFERCEPT, 100, eng=eng, est=cf.Estimator(t_def_us=20, n_min=1))
+    assert list(j) == [52] and s[15] == 1 and s[12] == 0
+    # same but DRAM too small for the 12-block context -> evict, recompute 15 tokens: 42->58
+    eng_small = cf.Engine(**{**UNIT.__dict__, "dram_blocks": 5})
+    s, j = run(tr, cf.INFERCEPT, 100, eng=eng_small, est=cf.Estimator(t_def_us=20, n_min=1))
+    assert list(j) == [58] and s[11] == 12
+
+
+def test_plas_prefers_least_attained_service():
+    """A (long first turn, more attained service) is served after B.
+
+    Pool 25, bs 1, unit costs.  A@0 (20+1, tool 10), B@1 (2+1, tool 10), C@2 (24+1, last).
+    0->21 A; 21->24 B (C does not fit beside it); 24->49 C; A and B return at 31 and 34; at 49
+    only one of A (needs 23) and B (needs 5) fits.  FCFS: A 49->72, B 72->77 (JCT 72, 76).
+    PLAS (service A 21 > B 3): B 49->54, A 54->77 (JCT 77, 53)."""
+    tr = traces.tiny([(0, [(20, 1, 0, 10), (1, 1, -1, 0)]), (1, [(2, 1, 0, 10), (1, 1, -1, 0)]),
+                      (2, [(24, 1, -1, 0)])])
+    s_f, j_f = run(tr, cf.PROG_FCFS, 25)
+    s_p, j_p = run(tr, cf.AUTELLIX, 25)
+    assert list(j_f[:2]) == [72, 76] and list(j_p[:2]) == [77, 53]
+    # fresh programs tie at 0 service -> program arrival order (SPEC.md:498)
+    tr2 = traces.tiny([(0, [(5, 1, -1, 0)]), (0, [(5, 1, -1, 0)])])
+    s2, j2 = run(tr2, cf.AUTELLIX, 6)
+    assert j2[0] < j2[1]
+
+
+def test_time_scale_invariance():
+    """Doubling every time quantity (integer-µs costs, tool durations, arrival gaps, TTLs)
+    doubles every JCT exactly: the schedule depends on time only through order (SPEC.md:504,
+    PLAS ordering invariant under uniform scaling of service)."""
+    tr = small_workload(7, P=10, n_seeds=2)
+    t2 = traces.TraceSet(tr.programs.copy(), tr.turns.copy(), tr.n_seeds, tr.n_programs,
+                         tr.n_tools, tr.pclass)
+    t2.turns[:, 3] *= 2
+    e1 = cf.Engine(c0_ps=3 * 10**6, c_pf_ps=10**6, c_kv_ps=0, c_h2d_ps=2 * 10**6, bs=16,
+                   dram_blocks=300)
+    e2 = cf.Engine(c0_ps=6 * 10**6, c_pf_ps=2 * 10**6, c_kv_ps=0, c_h2d_ps=4 * 10**6, bs=16,
+                   dram_blocks=300)
+    pols1 = [cf.AUTELLIX, cf.PROG_FCFS, cf.VLLM, cf.ttl_grid(20_000), cf.INFERCEPT]
+    pols2 = [cf.AUTELLIX, cf.PROG_FCFS, cf.VLLM, cf.ttl_grid(40_000), cf.INFERCEPT]
+    est1 = cf.Estimator(t_def_us=30_000, n_min=2)
+    est2 = cf.Estimator(t_def_us=60_000, n_min=2, b_us=2 * cf.Estimator().b_us)
+    s1, j1 = O.simulate(tr, cf.Sweep(2, [1 << 20], [700], pols1, est1), e1)
+    s2, j2 = O.simulate(t2, cf.Sweep(2, [1 << 21], [700], pols2, est2), e2)
+    assert np.all((s1[:, 0] & 0xFFFFFFFF) == 0)
+    assert np.array_equal(j2, 2 * j1)
+    assert np.array_equal(s2[:, 6], 2 * s1[:, 6]) and np.array_equal(s2[:, 12:16], s1[:, 12:16])
