@@ -340,13 +340,18 @@ int ct_fit_ttl(ct_ctx* c, const ct_samples* sm, const ct_cost_params* cp,
     return fail(CT_EINVAL, "grid_step_us and b_us must be < 2^31");
   // per warp chunk CH: a replica (32/R lanes) sees <= CH/R + 64 samples (32-bit remainder sums
   // < 2^32, 16-bit packed counts < 2^16) and a lane <= CH/32 + 2 (64-bit sum of squares < 2^64)
-  const int R = ct::fit_hist_repl();
-  int64_t CH = 1ll << 16;
-  while (CH > 256 && (CH / R + 64) * (uint64_t)cp->grid_step_us >= (1ull << 32)) CH >>= 1;
-  while (CH > 256 && CH / R + 64 >= (1 << 16)) CH >>= 1;
+  // CTA-shared variant: CTA chunks of CH samples over 256 threads, a lane-index replica sees
+  // <= CH/32 + 64 samples and a thread <= CH/256 + 8.
+  const bool cta = ct::fit_hist_cta_chunks();
+  const int R = cta ? 1 : ct::fit_hist_repl();
+  const int per_thread_div = cta ? 256 : 32;
+  int64_t CH = cta ? (1ll << 17) : (1ll << 16);
+  const int64_t rdiv = cta ? 32 : R;
+  while (CH > 256 && (CH / rdiv + 64) * (uint64_t)cp->grid_step_us >= (1ull << 32)) CH >>= 1;
+  while (CH > 256 && !cta && CH / R + 64 >= (1 << 16)) CH >>= 1;
   {
     const unsigned __int128 b2 = (unsigned __int128)est->b_us * est->b_us;
-    while (CH > 256 && (unsigned __int128)(CH / 32 + 8) * b2 >= ((unsigned __int128)1 << 64)) CH >>= 1;
+    while (CH > 256 && (unsigned __int128)(CH / per_thread_div + 8) * b2 >= ((unsigned __int128)1 << 64)) CH >>= 1;
   }
   if (CH < 256) return fail(CT_EINVAL, "grid step / b too large for the histogram pass");
   // rows 0..F-1 per tool, row F pooled (filled by fit_hist)
@@ -380,7 +385,8 @@ int ct_fit_ttl(ct_ctx* c, const ct_samples* sm, const ct_cost_params* cp,
       c->fit_occ_smem = ct::fit_hist_smem(K);
     }
     if (c->fit_occ < 1) return fail(CT_ECUDA, "fit_hist kernel cannot be resident");
-    const int wpb = ct::fit_hist_threads() / 32;  // every warp takes its own chunks
+    // warp variants: every warp takes its own chunks; CTA variant: one chunk per CTA
+    const int wpb = ct::fit_hist_cta_chunks() ? 1 : ct::fit_hist_threads() / 32;
     const int grid = (int)std::min<int64_t>((int64_t)c->sm_count * c->fit_occ,
                                             (fa.n_chunks + wpb - 1) / wpb);
     if (c->timing) CT_CUDA(cudaEventRecord(c->ev[2], s));

@@ -66,6 +66,7 @@ cudaError_t launch_fit_hist(const FitArgs& a, int grid, cudaStream_t s);
 cudaError_t launch_fit_scan(const ScanArgs& a, cudaStream_t s);
 int fit_hist_threads();
 int fit_hist_repl();  // histogram replicas per warp of the selected variant
+bool fit_hist_cta_chunks();  // work items are CTA-level chunks (CTA-shared histogram)
 int fit_hist_smem(int K);
 int fit_hist_occupancy(int smem);  // resident CTAs per SM
 

@@ -31,8 +31,9 @@ struct FitVariant {
 };
 static const FitVariant kVariants[] = {{16, false, 16}, {16, true, 16}, {8, false, 8},
                                        {8, true, 8},    {32, false, 16}, {16, true, 8},
-                                       {8, true, 4}};
-static int g_variant = -1;  // default 2 (measured best on B200)
+                                       {8, true, 4},    {4, false, 8},   {4, false, 4},
+                                       {8, false, 4}};
+static int g_variant = -1;  // default 2: measured best on B200 (DESIGN.md §8 variant table)
 
 static int variant() {
   if (g_variant < 0) {
@@ -43,12 +44,16 @@ static int variant() {
   return g_variant;
 }
 
-int fit_hist_threads() { return FIT_THREADS; }
+static bool cta_variant() { return variant() >= 10; }
+int fit_hist_threads() { return cta_variant() ? 256 : FIT_THREADS; }
 int fit_hist_repl() { return kVariants[variant()].repl; }
+bool fit_hist_cta_chunks() { return cta_variant(); }
 static int smem_words(int K, const FitVariant& fv) {
   return (K + 1) * (fv.repl + (fv.pack ? fv.repl / 2 : fv.repl));
 }
-int fit_hist_smem(int K) { return FIT_WARPS * 4 * smem_words(K, kVariants[variant()]); }
+int fit_hist_smem(int K) {
+  return cta_variant() ? (K + 1) * 64 * 4 : FIT_WARPS * 4 * smem_words(K, kVariants[variant()]);
+}
 
 __device__ __forceinline__ void red_shared(uint32_t addr, uint32_t v) {
   asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
@@ -207,6 +212,130 @@ __global__ void __launch_bounds__(FIT_THREADS) fit_hist_kernel(FitArgs a) {
   }
 }
 
+// CTA-shared variant: the CTA's FW warps share one histogram with one replica per lane index,
+// laid out [bucket][count x 32 | remainder x 32]: within a warp instruction the 32 lanes always
+// hit 32 distinct banks (no conflicts, no same-address serialisation, even for a point mass),
+// while the footprint per warp is 1/FW of a lane-private histogram.  Chunks are CTA-level.
+constexpr int FW = 8;
+
+template <bool IDENT, int U>
+__global__ void __launch_bounds__(32 * FW) fit_hist_cta_kernel(FitArgs a) {
+  extern __shared__ __align__(16) uint32_t hsm[];
+  const int K = a.K;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int words = (K + 1) * 64;
+  Lane L;
+  L.rs_base = (uint32_t)__cvta_generic_to_shared(hsm) + 4 * lane + 128;  // remainders
+  L.cnt_base = L.rs_base - 128;                                           // counts
+  L.cnt_inc = 1u;
+  L.K = (uint32_t)K;
+  L.step = (uint32_t)a.step;
+  L.mhi = (uint32_t)(a.step_magic >> 32);
+  L.mlo = (uint32_t)a.step_magic;
+  L.xoff = L.step - 1;
+  L.b_us = (uint32_t)a.b_us;
+  __shared__ unsigned long long red[FW][3];
+
+  for (int64_t c = blockIdx.x; c < a.n_chunks; c += gridDim.x) {
+    int tool = 0;
+    while (a.chunk_off[tool + 1] <= c) ++tool;
+    const int64_t beg = a.tool_off[tool] + (c - a.chunk_off[tool]) * a.ch;
+    const int64_t end = min(beg + a.ch, a.tool_off[tool + 1]);
+    for (int i = tid; i < words; i += 32 * FW) hsm[i] = 0;
+    __syncthreads();
+    uint64_t s1 = 0, s2 = 0;
+    int64_t va = (beg + 3) & ~(int64_t)3;
+    if (va > end) va = end;
+    const int64_t vb = va + ((end - va) & ~(int64_t)3);
+    if (tid < 32) {
+      if (beg + lane < va) sample<IDENT, 64, false>(L, __ldg(&a.dur[beg + lane]), s1, s2);
+      if (vb + lane < end) sample<IDENT, 64, false>(L, __ldg(&a.dur[vb + lane]), s1, s2);
+    }
+    const int4* v = (const int4*)(a.dur + va);
+    const int64_t nv = (vb - va) >> 2;
+    constexpr int T = 32 * FW;
+    int64_t i = tid;
+    int4 A[U], B[U];
+    bool have_a = i + (U - 1) * T < nv;
+    if (have_a) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) A[u] = __ldcs(v + i + u * T);
+    }
+    while (have_a) {
+      const int64_t ib = i + U * T;
+      const bool have_b = ib + (U - 1) * T < nv;
+      if (have_b) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) B[u] = __ldcs(v + ib + u * T);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        sample<IDENT, 64, false>(L, A[u].x, s1, s2);
+        sample<IDENT, 64, false>(L, A[u].y, s1, s2);
+        sample<IDENT, 64, false>(L, A[u].z, s1, s2);
+        sample<IDENT, 64, false>(L, A[u].w, s1, s2);
+      }
+      i = ib;
+      if (!have_b) break;
+      const int64_t ia = ib + U * T;
+      have_a = ia + (U - 1) * T < nv;
+      if (have_a) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) A[u] = __ldcs(v + ia + u * T);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        sample<IDENT, 64, false>(L, B[u].x, s1, s2);
+        sample<IDENT, 64, false>(L, B[u].y, s1, s2);
+        sample<IDENT, 64, false>(L, B[u].z, s1, s2);
+        sample<IDENT, 64, false>(L, B[u].w, s1, s2);
+      }
+      i = ia;
+    }
+    for (; i < nv; i += T) {
+      const int4 x = __ldcs(v + i);
+      sample<IDENT, 64, false>(L, x.x, s1, s2);
+      sample<IDENT, 64, false>(L, x.y, s1, s2);
+      sample<IDENT, 64, false>(L, x.z, s1, s2);
+      sample<IDENT, 64, false>(L, x.w, s1, s2);
+    }
+    const uint64_t w1 = warp_sum_u64(s1), w2 = warp_sum_u64(s2 & 0xffffffffull),
+                   w3 = warp_sum_u64(s2 >> 32);
+    if (lane == 0) { red[tid >> 5][0] = w1; red[tid >> 5][1] = w2; red[tid >> 5][2] = w3; }
+    __syncthreads();
+    if (tid < 6) {  // tid 0-2: the tool's row, 3-5: the pooled row F
+      const int q = tid % 3;
+      uint64_t sum = 0;
+#pragma unroll
+      for (int w = 0; w < FW; ++w) sum += red[w][q];
+      unsigned long long* st = a.stat + (tid < 3 ? tool : a.F) * 6;
+      if (q == 0) atomicAdd(st, (unsigned long long)(end - beg));
+      if (sum) atomicAdd(st + 1 + q, (unsigned long long)sum);
+    }
+    // merge the 32 lane replicas of every bucket and flush (tool row + pooled row)
+    for (int b = tid; b <= K; b += T) {
+      const uint4* pc = (const uint4*)(hsm + b * 64);
+      uint64_t cn = 0, rr = 0;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const uint4 x = pc[q], y = pc[8 + q];
+        cn += (uint64_t)x.x + x.y + x.z + x.w;
+        rr += (uint64_t)y.x + y.y + y.z + y.w;
+      }
+      if (cn) {
+        const uint64_t sm = b < K ? (uint64_t)b * L.step * cn - rr : 0;
+#pragma unroll
+        for (int row2 = 0; row2 < 2; ++row2) {
+          const int64_t o = (int64_t)(row2 ? a.F : tool) * (K + 1) + b;
+          atomicAdd(&a.hcnt[o], (unsigned long long)cn);
+          if (sm) atomicAdd(&a.hsum[o], (unsigned long long)sm);
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
 template <bool IDENT>
 static void* hist_fn(int v) {
   switch (v) {
@@ -216,7 +345,12 @@ static void* hist_fn(int v) {
     case 3: return (void*)fit_hist_kernel<IDENT, 8, true, 8>;
     case 4: return (void*)fit_hist_kernel<IDENT, 32, false, 16>;
     case 5: return (void*)fit_hist_kernel<IDENT, 16, true, 8>;
-    default: return (void*)fit_hist_kernel<IDENT, 8, true, 4>;
+    case 6: return (void*)fit_hist_kernel<IDENT, 8, true, 4>;
+    case 7: return (void*)fit_hist_kernel<IDENT, 4, false, 8>;
+    case 8: return (void*)fit_hist_kernel<IDENT, 4, false, 4>;
+    case 9: return (void*)fit_hist_kernel<IDENT, 8, false, 4>;
+    case 10: return (void*)fit_hist_cta_kernel<IDENT, 4>;
+    default: return (void*)fit_hist_cta_kernel<IDENT, 8>;
   }
 }
 
@@ -322,7 +456,7 @@ cudaError_t launch_fit_hist(const FitArgs& a, int grid, cudaStream_t s) {
   const int smem = fit_hist_smem(a.K);
   void* k = a.step == 1 ? hist_fn<true>(variant()) : hist_fn<false>(variant());
   void* args[] = {(void*)&a};
-  return cudaLaunchKernel(k, dim3(grid), dim3(FIT_THREADS), args, smem, s);
+  return cudaLaunchKernel(k, dim3(grid), dim3(fit_hist_threads()), args, smem, s);
 }
 
 int fit_hist_occupancy(int smem) {
@@ -330,7 +464,7 @@ int fit_hist_occupancy(int smem) {
     if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
       return 0;
   int nb = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, hist_fn<false>(variant()), FIT_THREADS, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, hist_fn<false>(variant()), fit_hist_threads(), smem);
   return nb;
 }
 
