@@ -232,7 +232,7 @@ int ct_simulate_batch(ct_ctx* c, const ct_trace_set* tr, const ct_sweep* sw,
   a.bs_magic = E.bs == 1 ? 0
                          : (uint64_t)(((((unsigned __int128)1) << 64) + (uint64_t)E.bs - 1) /
                                       (unsigned __int128)(uint64_t)E.bs);
-  const int ns = P <= 32 ? 1 : P <= 64 ? 2 : P <= 128 ? 4 : 8;
+  const int ns = (P + 31) / 32;  // slots per lane
   const int wpb = 4;
   a.smem_per_warp = ct::replay_smem_per_warp(ns, F);
   const int smem = a.smem_per_warp * wpb;

@@ -22,547 +22,10 @@ enum : int { S_OUT = 0, S_QUEUED = 1, S_RUN = 2, S_LOAD = 3, S_READY = 4, S_TOOL
 int replay_smem_per_warp(int ns, int F) {
   if (ns == 1) return (32 * (F + 1) + 48 + 15) & ~15;  // registers hold the programs; SMEM: estimator + Acc
   int pm = 32 * ns;
-  int b = 61 * pm;
+  int b = 60 * pm;
   b = (b + 15) & ~15;
-  b += 32 * (F + 1);
+  b += 32 * (F + 1) + 48;  // estimator rows + Acc
   return (b + 15) & ~15;
-}
-
-template <int NS>
-__device__ __forceinline__ void replay_one(const ReplayArgs& a, int64_t r, unsigned char* wm,
-                                           int lane) {
-  constexpr int PM = 32 * NS;
-  int64_t* t_ev = (int64_t*)wm;           // tool return / load done time, INF otherwise
-  int64_t* t_exp = t_ev + PM;             // expiry + 1 while pinned and in a tool call
-  int64_t* req = t_exp + PM;              // request arrival (Q entry time); JCT once done
-  int64_t* fin = req + PM;                // iteration index at whose end the request finishes
-  int32_t* ctx = (int32_t*)(fin + PM);    // context tokens
-  int32_t* gblk = ctx + PM;               // GPU blocks held
-  int32_t* dblk = gblk + PM;              // DRAM copy blocks
-  int32_t* unc = dblk + PM;               // uncached tokens of the current request
-  int32_t* turn = unc + PM;               // current turn
-  int64_t* svc = (int64_t*)(turn + PM);   // attained engine time (PLAS)
-  uint8_t* st = (uint8_t*)(svc + PM);     // lifecycle state
-  Stat* stats = (Stat*)(wm + ((61 * PM + 15) & ~15));  // [F] per tool, [F] = global
-
-  const int P = a.P, F = a.F;
-  const int64_t npol = a.n_pol, nkv = a.n_kv, nrate = a.n_rate;
-  const int pol_i = (int)(r % npol);
-  const int kv_i = (int)((r / npol) % nkv);
-  const int rate_i = (int)((r / (npol * nkv)) % nrate);
-  const int64_t seed = r / (npol * nkv * nrate);
-  const ct_policy pol = a.pols[pol_i];
-  const int64_t gap = a.gap[rate_i];
-  const ct_program* prog = a.progs + seed * P;
-  const ct_engine_params& E = a.eng;
-  const ct_estimator_params& est = a.est;
-  const int64_t bs = E.bs;
-  DivMagic bsm;
-  bsm.mhi = (uint32_t)(a.bs_magic >> 32);
-  bsm.mlo = (uint32_t)a.bs_magic;
-  bsm.dm1 = (uint32_t)(bs - 1);
-  bsm.ident = bs == 1 ? 1u : 0u;
-  const bool eager = (pol.flags & CT_FLAG_STEP_EXPIRY) == 0;
-  const bool vany = (pol.flags & CT_FLAG_VICTIMS_ANY) != 0;
-  const bool dram_on = pol.dram != 0 && E.dram_blocks > 0;
-  const bool need_stats = pol.pause == CT_PAUSE_PAPER || pol.pause == CT_PAUSE_INFERCEPT ||
-                          (pol.pause == CT_PAUSE_FIXED && pol.t_thresh_us != CT_ALWAYS);
-  const bool plas = pol.priority == CT_PRIO_PLAS;
-
-#pragma unroll
-  for (int s = 0; s < NS; ++s) {
-    int p = lane + 32 * s;
-    t_ev[p] = CT_INF64;
-    t_exp[p] = CT_INF64;
-    req[p] = 0;
-    fin[p] = 0;
-    ctx[p] = 0;
-    gblk[p] = 0;
-    dblk[p] = 0;
-    unc[p] = 0;
-    turn[p] = 0;
-    svc[p] = 0;
-    st[p] = S_OUT;
-  }
-  if (need_stats)
-    for (int i = lane; i < 4 * (F + 1); i += 32) ((int64_t*)stats)[i] = 0;
-  __syncwarp();
-
-  uint32_t qb = 0, pb = 0, rb = 0;  // bit s: program lane + 32 s is queued / pinned / running
-
-  auto arrival = [&](int i) -> int64_t { return (prog[i].arr_q * gap) >> 20; };
-  auto own = [&](int p) { return lane == (p & 31); };
-  auto bit = [&](int p) { return 1u << (p >> 5); };
-  auto is_pinned = [&](int p) -> bool { return (__shfl_sync(FULL_MASK, pb, p & 31) >> (p >> 5)) & 1u; };
-  auto turn_rec = [&](int p, int t) -> int4 { return __ldg(&a.turns[prog[p].turn0 + t]); };
-
-  int64_t now = 0, iter_end = 0, n_it = 0;
-  bool in_flight = false;
-  int64_t free_blk = a.kv[kv_i];
-  int64_t dfree = dram_on ? E.dram_blocks : 0, chan = 0;
-  int next_arr = 0;
-  int64_t t_arr = P > 0 ? arrival(0) : CT_INF64;
-  int64_t D = 0, turns_done = 0;
-  int n_run = 0, n_load = 0;  // n_load counts LOADING and READY
-  int64_t kv_sum = 0, pf = 0;
-  int status = CT_R_OK;
-  int64_t c_bubble = 0, c_prefill = 0, c_recomp = 0, c_hits = 0, c_exp = 0, c_vict = 0,
-          c_reload = 0, c_busy = 0, max_comp = 0;
-
-  // evict(v): free its GPU blocks, DRAM write-through when the tier is on (R18).
-  auto evict = [&](int v) {
-    int64_t g = gblk[v];
-    free_blk += g;
-    if (dram_on) {
-      int64_t nb = ceil_div_magic((uint32_t)ctx[v], bsm);
-      dfree += dblk[v];
-      int64_t keep = 0;
-      if (nb > 0 && nb <= dfree) { keep = nb; dfree -= nb; }
-      if (own(v)) dblk[v] = (int32_t)keep;
-    }
-    if (own(v)) gblk[v] = 0;
-    __syncwarp();
-  };
-  auto unpin = [&](int v) {
-    if (own(v)) { pb &= ~bit(v); t_exp[v] = CT_INF64; }
-  };
-
-  for (;;) {
-    // ---- next event (R1, R3) --------------------------------------------------------
-    int64_t lt = CT_INF64;
-#pragma unroll
-    for (int s = 0; s < NS; ++s) {
-      int p = lane + 32 * s;
-      int64_t x = t_ev[p];
-      if (eager) x = min(x, t_exp[p]);
-      lt = min(lt, x);
-    }
-    const int64_t t_prog = warp_min64_redux(lt);
-    int64_t t = min(t_prog, t_arr);
-    if (in_flight) t = min(t, iter_end);
-    if (t == CT_INF64) break;
-    now = t;
-
-    if (t_prog == now) {
-      // PinExpiry: first µs with now > expiry while not in Q — EAGER (R4)
-      if (eager) {
-#pragma unroll
-        for (int s = 0; s < NS; ++s) {
-          uint32_t m = __ballot_sync(FULL_MASK, t_exp[lane + 32 * s] == now);
-          while (m) {
-            int p = 32 * s + __ffs(m) - 1;
-            m &= m - 1;
-            evict(p);
-            unpin(p);
-            ++c_exp;
-          }
-        }
-      }
-      // ToolReturn == OnRequestArrive of a seen program
-#pragma unroll
-      for (int s = 0; s < NS; ++s) {
-        int pl = lane + 32 * s;
-        uint32_t m = __ballot_sync(FULL_MASK, t_ev[pl] == now && st[pl] == S_TOOL);
-        while (m) {
-          int p = 32 * s + __ffs(m) - 1;
-          m &= m - 1;
-          int tp = turn[p];
-          if (need_stats) {
-            int4 tr = turn_rec(p, tp);
-            int64_t x = min((int64_t)tr.w, est.b_us);  // Δ_obs clamped at b (R5)
-            uint64_t x2 = (uint64_t)x * (uint64_t)x;
-            if (lane == 0) {
-              Stat* rows[2] = {&stats[F], &stats[tr.z]};
-#pragma unroll
-              for (int k = 0; k < 2; ++k) {
-                Stat* q = rows[k];
-                q->n += 1;
-                q->s1 += x;
-                uint64_t lo = q->s2lo + x2;
-                q->s2hi += (lo < x2);
-                q->s2lo = lo;
-              }
-            }
-          }
-          if (own(p)) {
-            turn[p] = tp + 1;
-            st[p] = S_QUEUED;
-            req[p] = now;
-            t_ev[p] = CT_INF64;
-            t_exp[p] = CT_INF64;  // a retained pin has no expiry event while waiting
-            qb |= bit(p);
-          }
-          __syncwarp();
-        }
-      }
-      // LoadDone
-#pragma unroll
-      for (int s = 0; s < NS; ++s) {
-        int pl = lane + 32 * s;
-        bool hit = t_ev[pl] == now && st[pl] == S_LOAD;
-        if (hit) { st[pl] = S_READY; t_ev[pl] = CT_INF64; }
-      }
-      __syncwarp();
-    }
-    // ProgramArrival
-    while (t_arr == now) {
-      int p = next_arr;
-      if (own(p)) {
-        st[p] = S_QUEUED;
-        turn[p] = 0;
-        ctx[p] = 0;
-        req[p] = now;
-        qb |= bit(p);
-      }
-      ++next_arr;
-      t_arr = next_arr < P ? arrival(next_arr) : CT_INF64;
-    }
-    __syncwarp();
-
-    // IterationEnd: members whose last token was emitted finish, in index order (C-6)
-    if (in_flight && iter_end == now) {
-      in_flight = false;
-#pragma unroll
-      for (int s = 0; s < NS; ++s) {
-        int pl = lane + 32 * s;
-        uint32_t m = __ballot_sync(FULL_MASK, ((rb >> s) & 1u) && fin[pl] == n_it);
-        while (m) {
-          int p = 32 * s + __ffs(m) - 1;
-          m &= m - 1;
-          // OnRequestFinish (PAPER.md:378-386)
-          const int tp = turn[p];
-          const int4 tr = turn_rec(p, tp);
-          const int nctx = ctx[p] + tr.x + tr.y;
-          const int64_t g = gblk[p];
-          --n_run;
-          kv_sum -= g;
-          if (own(p)) { rb &= ~bit(p); ctx[p] = nctx; }
-          __syncwarp();
-          if (tp == prog[p].nturns - 1) {  // last request: free its KV, program completes
-            free_blk += g;
-            dfree += dblk[p];
-            const int64_t j = now - arrival(p);
-            if (own(p)) { gblk[p] = 0; dblk[p] = 0; st[p] = S_DONE; req[p] = j; }
-            ++D;
-            turns_done += prog[p].nturns;
-            max_comp = now;
-            __syncwarp();
-          } else {
-            const int f = tr.z;
-            int64_t ttl = 0;
-            switch (pol.pause) {
-              case CT_PAUSE_FIXED:
-              case CT_PAUSE_PAPER: {
-                Stat sg = stats[F], sf = stats[f];
-                ttl = pol.pause == CT_PAUSE_PAPER
-                          ? calc_ttl(sg, sf, est, D, turns_done)
-                          : simplified_ttl(sg, sf, est, pol.t_pin_us, pol.t_thresh_us);
-                break;
-              }
-              case CT_PAUSE_FITTED:
-                ttl = __ldg(&a.fitted[(int64_t)f * a.J + min(tp, a.J - 1)]);
-                break;
-              case CT_PAUSE_INFERCEPT: {  // preserve (no TTL) iff prediction < swap round trip
-                const int64_t pred = infercept_predict(stats[F], stats[f], est);
-                const int64_t blocks = ceil_div_magic((uint32_t)nctx, bsm);
-                const int64_t swap = 2 * ceil_ps_to_us((uint64_t)(blocks * E.c_h2d_ps));
-                ttl = pred < swap ? CT_INF64 : 0;
-                break;
-              }
-              default:
-                ttl = 0;
-            }
-            if (ttl > 0) {  // pin_request only if TTL != 0 (PAPER.md:633)
-              if (own(p)) { pb |= bit(p); t_exp[p] = ttl == CT_INF64 ? CT_INF64 : now + ttl + 1; }
-            } else {
-              evict(p);
-            }
-            if (own(p)) { t_ev[p] = now + tr.w; st[p] = S_TOOL; }
-            __syncwarp();
-          }
-        }
-      }
-    }
-    if (in_flight) continue;  // mid-iteration: events only mutate Q / stats / pins (R2)
-
-    // ---- scheduling point (R3) ----------------------------------------------------------
-    // (a) STEP reading: release expired pins of programs not waiting (PAPER.md:390-397, 638)
-    if (!eager) {
-#pragma unroll
-      for (int s = 0; s < NS; ++s) {
-        int pl = lane + 32 * s;
-        uint32_t m = __ballot_sync(FULL_MASK, ((pb >> s) & 1u) && st[pl] == S_TOOL && t_exp[pl] <= now);
-        while (m) {
-          int p = 32 * s + __ffs(m) - 1;
-          m &= m - 1;
-          evict(p);
-          unpin(p);
-          ++c_exp;
-        }
-      }
-    }
-    // (b) loaded requests join the batch
-#pragma unroll
-    for (int s = 0; s < NS; ++s) {
-      int pl = lane + 32 * s;
-      uint32_t m = __ballot_sync(FULL_MASK, st[pl] == S_READY);
-      while (m) {
-        int p = 32 * s + __ffs(m) - 1;
-        m &= m - 1;
-        const int4 tr = turn_rec(p, turn[p]);
-        if (own(p)) { st[p] = S_RUN; rb |= bit(p); fin[p] = n_it + tr.y; }
-        kv_sum += gblk[p];
-        pf += unc[p];
-        ++n_run;
-        --n_load;
-        __syncwarp();
-      }
-    }
-    // (c) admit loop (victims PAPER.md:645-655)
-    int admitted = 0;
-    bool stable = true;
-    for (;;) {
-      if (!__any_sync(FULL_MASK, qb != 0)) break;
-      if (n_run + n_load >= E.max_batch) break;
-      int h = -1;
-      if (pol.priority == CT_PRIO_PROG_FCFS) {
-#pragma unroll
-        for (int s = 0; s < NS; ++s) {
-          uint32_t m = __ballot_sync(FULL_MASK, ((qb & pb) >> s) & 1u);
-          if (h < 0 && m) h = 32 * s + __ffs(m) - 1;
-        }
-        if (h < 0) {
-#pragma unroll
-          for (int s = 0; s < NS; ++s) {
-            uint32_t m = __ballot_sync(FULL_MASK, (qb >> s) & 1u);
-            if (h < 0 && m) h = 32 * s + __ffs(m) - 1;
-          }
-        }
-      } else {
-        int64_t bk = CT_INF64;
-        int bp = 0x7fffffff;
-#pragma unroll
-        for (int s = 0; s < NS; ++s) {
-          int pl = lane + 32 * s;
-          if ((qb >> s) & 1u) {
-            int64_t k = plas ? svc[pl] : req[pl];  // PLAS: least attained service
-            if (k < bk || (k == bk && pl < bp)) { bk = k; bp = pl; }
-          }
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          int64_t ok = __shfl_xor_sync(FULL_MASK, bk, o);
-          int op = __shfl_xor_sync(FULL_MASK, bp, o);
-          if (ok < bk || (ok == bk && op < bp)) { bk = ok; bp = op; }
-        }
-        h = bp;
-      }
-      const int4 tr = turn_rec(h, turn[h]);
-      const int64_t hctx = ctx[h];
-      const int64_t need = (int64_t)ceil_div_magic((uint32_t)(hctx + tr.x + tr.y), bsm) - gblk[h];
-      if (need > free_blk && (admitted == 0 || vany)) {
-        while (need > free_blk) {  // victims: latest program arrival first, never the head
-          int v = -1;
-#pragma unroll
-          for (int s = NS - 1; s >= 0; --s) {
-            uint32_t m = __ballot_sync(FULL_MASK, (pb >> s) & 1u);
-            if (s == (h >> 5)) m &= ~(1u << (h & 31));
-            if (v < 0 && m) v = 32 * s + 31 - __clz(m);
-          }
-          if (v < 0) break;
-          evict(v);
-          unpin(v);
-          ++c_vict;
-        }
-      }
-      if (need > free_blk) {  // HOL break
-        if (admitted > 0 && !vany) {
-          // the next boundary would run the victim rule: it is not a no-op if pins remain
-          uint32_t any = 0;
-#pragma unroll
-          for (int s = 0; s < NS; ++s) any |= __ballot_sync(FULL_MASK, (pb >> s) & 1u) & ~(s == (h >> 5) ? (1u << (h & 31)) : 0u);
-          if (any) stable = false;
-        }
-        break;
-      }
-      // issue h
-      free_blk -= need;
-      const int64_t ng = gblk[h] + need;
-      c_bubble += now - req[h];
-      const bool hp = is_pinned(h);
-      int64_t cached;
-      bool loading = false;
-      int64_t ld = 0;
-      const int64_t hd = dblk[h];
-      if (hp) {
-        cached = hctx;
-        ++c_hits;
-      } else if (dram_on && hd > 0 && hd == (int64_t)ceil_div_magic((uint32_t)hctx, bsm)) {
-        cached = hctx;
-        loading = true;
-        ld = max(now, chan) + ceil_ps_to_us((uint64_t)(hd * E.c_h2d_ps));
-        chan = ld;
-        ++c_reload;
-      } else {
-        cached = 0;
-        c_recomp += hctx;
-      }
-      const int64_t u = hctx + tr.x - cached;
-      c_prefill += u;
-      if (own(h)) {
-        qb &= ~bit(h);
-        pb &= ~bit(h);
-        t_exp[h] = CT_INF64;
-        gblk[h] = (int32_t)ng;
-        unc[h] = (int32_t)u;
-        if (loading) {
-          st[h] = S_LOAD;
-          t_ev[h] = ld;
-        } else {
-          st[h] = S_RUN;
-          rb |= bit(h);
-          fin[h] = n_it + tr.y;
-        }
-      }
-      if (loading) {
-        ++n_load;
-      } else {
-        ++n_run;
-        kv_sum += ng;
-        pf += u;
-      }
-      ++admitted;
-      __syncwarp();
-    }
-    // (d) unschedulable: the head missed with nothing running or loading; the victim loop has
-    // already released every other pin, so no future event can free memory for it (C-5 5c)
-    if (admitted == 0 && n_run == 0 && n_load == 0 && __any_sync(FULL_MASK, qb != 0)) {
-      status = CT_R_UNSCHEDULABLE;
-      break;
-    }
-    // (e) start the next iteration(s) (linear cost model, R16)
-    if (n_run > 0) {
-      const int64_t base = E.c0_ps + E.c_kv_ps * bs * kv_sum;
-      int64_t k = 1, dur;
-      if (pf > 0) {
-        dur = ceil_ps_to_us((uint64_t)(base + E.c_pf_ps * pf));
-        pf = 0;
-      } else {
-        const int64_t d = ceil_ps_to_us((uint64_t)base);
-        if (stable) {
-          // macro-step: identical iterations until the first finish or the first boundary at or
-          // after the next external event (arrival, tool return, load done, pin expiry)
-          int64_t lf = CT_INF64, le = CT_INF64;
-#pragma unroll
-          for (int s = 0; s < NS; ++s) {
-            int pl = lane + 32 * s;
-            if ((rb >> s) & 1u) lf = min(lf, fin[pl]);
-            le = min(le, min(t_ev[pl], t_exp[pl]));
-          }
-          const int64_t mfin = warp_min64_redux(lf);
-          const int64_t te = min(warp_min64_redux(le), t_arr);
-          const int64_t m = mfin - n_it;
-          int64_t j = m;
-          // first boundary at or after te: ceil((te - now) / d), needed only when < m
-          if (te != CT_INF64) {
-            const int64_t gap = te - now;  // >= 1
-            const double est = (double)gap / (double)d;
-            if (est < (double)m + 2.0) {  // exact correction of the estimate (no overflow here)
-              int64_t jb = (int64_t)est;
-              while (jb * d < gap) ++jb;
-              while (jb > 1 && (jb - 1) * d >= gap) --jb;
-              if (jb < j) j = jb;
-            }
-          }
-          k = j;
-        }
-        dur = k * d;
-      }
-      if (n_it + k > E.max_iters) { status = CT_R_EVENT_BUDGET; break; }
-      n_it += k;
-      iter_end = now + dur;
-      c_busy += dur;
-      if (plas) {
-#pragma unroll
-        for (int s = 0; s < NS; ++s)
-          if ((rb >> s) & 1u) svc[lane + 32 * s] += dur;  // owners accrue their own programs
-      }
-      in_flight = true;
-    }
-  }
-  if (status == CT_R_OK && D != P) status = CT_R_UNSCHEDULABLE;
-
-  // ---- per-replica summary (A-8) ------------------------------------------------------------
-  __syncwarp();
-  const int64_t ri = r - a.r_begin;
-  int64_t jsum = 0, jmax = 0, p50 = 0, p99 = 0;
-  if (status == CT_R_OK) {
-    int64_t ls = 0, lm = 0;
-#pragma unroll
-    for (int s = 0; s < NS; ++s) {
-      int p = lane + 32 * s;
-      if (p < P) { ls += req[p]; lm = max(lm, req[p]); }
-    }
-    jsum = (int64_t)warp_sum_u64((uint64_t)ls);
-    jmax = warp_max64(lm);
-    // nearest rank (R20): value v with #(x < v) < rank <= #(x <= v)
-    const int r50 = (50 * P + 99) / 100, r99 = (99 * P + 99) / 100;
-    int64_t c50 = CT_INF64, c99 = CT_INF64;
-#pragma unroll
-    for (int s = 0; s < NS; ++s) {
-      int p = lane + 32 * s;
-      if (p < P) {
-        int64_t v = req[p];
-        int lt = 0, le = 0;
-        for (int q = 0; q < P; ++q) {
-          int64_t x = req[q];
-          lt += x < v;
-          le += x <= v;
-        }
-        if (lt < r50 && r50 <= le) c50 = v;
-        if (lt < r99 && r99 <= le) c99 = v;
-      }
-    }
-    p50 = warp_min64_redux(c50);
-    p99 = warp_min64_redux(c99);
-  }
-  if (lane == 0) {
-    ct_replica_summary o;
-    if (status == CT_R_OK) {
-      o.status = status;
-      o.n_done = (int32_t)D;
-      o.turns_done = turns_done;
-      o.sum_jct_us = jsum;
-      o.max_jct_us = jmax;
-      o.p50_jct_us = p50;
-      o.p99_jct_us = p99;
-      o.sum_bubble_us = c_bubble;
-      o.makespan_us = max_comp - arrival(0);
-      o.iterations = n_it;
-      o.busy_us = c_busy;
-      o.prefill_tokens = c_prefill;
-      o.recompute_tokens = c_recomp;
-      o.pin_hits = c_hits;
-      o.pin_expiries = c_exp;
-      o.victims = c_vict;
-      o.reloads = c_reload;
-    } else {
-      int64_t* w = (int64_t*)&o;
-#pragma unroll
-      for (int i = 0; i < 16; ++i) w[i] = 0;
-      o.status = status;
-    }
-    a.out[ri] = o;
-  }
-  if (a.jct) {
-    int64_t* jo = a.jct + ri * P;
-#pragma unroll
-    for (int s = 0; s < NS; ++s) {
-      int p = lane + 32 * s;
-      if (p < P) jo[p] = status == CT_R_OK ? req[p] : -1;
-    }
-  }
-  __syncwarp();
 }
 
 // -----------------------------------------------------------------------------------------------
@@ -1021,6 +484,558 @@ __device__ __forceinline__ void replay_one_w32(const ReplayArgs& a, int64_t r, S
   __syncwarp();
 }
 
+// -----------------------------------------------------------------------------------------------
+// 32 < P <= 256: program p lives on lane p % 32, slot p / 32.  Per-program scalars are SoA in
+// shared memory (written only by the owner lane); lifecycle sets are per-lane bit registers
+// (bit s = slot s); every lane caches the minimum of its own programs' event times (tool return /
+// load done, pin expiry) and of their finishing iterations, refreshed only when one of its
+// programs changes.  The next event, the macro-step bound and the first finish are therefore one
+// REDUX minimum each, and only lanes that own a due program scan their slots.  Same semantics as
+// replay_one_w32 (C-5/C-6), checked byte for byte by the tests.
+template <int NS>
+__device__ __forceinline__ void replay_one_ns(const ReplayArgs& a, int64_t r, unsigned char* wm,
+                                              int lane) {
+  constexpr int PM = 32 * NS;
+  int64_t* tev = (int64_t*)wm;         // tool return / load done, INF otherwise
+  int64_t* texp = tev + PM;            // expiry + 1 while pinned in a tool call, INF otherwise
+  int64_t* req = texp + PM;            // request arrival; JCT once done
+  int64_t* fin = req + PM;             // finishing iteration while running, INF otherwise
+  int64_t* svc = fin + PM;             // attained engine time (PLAS)
+  int32_t* ctx = (int32_t*)(svc + PM); // context tokens
+  int32_t* gblk = ctx + PM;            // GPU blocks held
+  int32_t* dblk = gblk + PM;           // DRAM copy blocks
+  int32_t* unc = dblk + PM;            // uncached tokens of the current request
+  int32_t* turn = unc + PM;            // current turn
+  Stat* stats = (Stat*)(wm + ((60 * PM + 15) & ~15));
+  Acc* acc = (Acc*)(stats + a.F + 1);
+
+  const int P = a.P, F = a.F;
+  const int64_t npol = a.n_pol, nkv = a.n_kv, nrate = a.n_rate;
+  const int pol_i = (int)(r % npol);
+  const int kv_i = (int)((r / npol) % nkv);
+  const int rate_i = (int)((r / (npol * nkv)) % nrate);
+  const int64_t seed = r / (npol * nkv * nrate);
+  const ct_policy* polp = a.pols + pol_i;
+  const int prio = polp->priority, pause = polp->pause, pflags = polp->flags;
+  const int64_t gap = a.gap[rate_i];
+  const ct_program* prog = a.progs + seed * P;
+  const ct_engine_params& E = a.eng;
+  const ct_estimator_params& est = a.est;
+  const int64_t bs = E.bs;
+  DivMagic bsm;
+  bsm.mhi = (uint32_t)(a.bs_magic >> 32);
+  bsm.mlo = (uint32_t)a.bs_magic;
+  bsm.dm1 = (uint32_t)(bs - 1);
+  bsm.ident = bs == 1 ? 1u : 0u;
+  const bool eager = (pflags & CT_FLAG_STEP_EXPIRY) == 0;
+  const bool vany = (pflags & CT_FLAG_VICTIMS_ANY) != 0;
+  const bool dram_on = polp->dram != 0 && E.dram_blocks > 0;
+  const bool need_stats = pause == CT_PAUSE_PAPER || pause == CT_PAUSE_INFERCEPT ||
+                          (pause == CT_PAUSE_FIXED && polp->t_thresh_us != CT_ALWAYS);
+  const bool plas = prio == CT_PRIO_PLAS;
+
+#pragma unroll
+  for (int s = 0; s < NS; ++s) {
+    const int p = lane + 32 * s;
+    tev[p] = CT_INF64;
+    texp[p] = CT_INF64;
+    req[p] = 0;
+    fin[p] = CT_INF64;
+    svc[p] = 0;
+    ctx[p] = 0;
+    gblk[p] = 0;
+    dblk[p] = 0;
+    unc[p] = 0;
+    turn[p] = 0;
+  }
+  if (need_stats)
+    for (int i = lane; i < 4 * (F + 1); i += 32) ((int64_t*)stats)[i] = 0;
+  if (lane == 0) *acc = Acc{0, 0, 0, 0, 0, 0, 0, 0};
+  __syncwarp();
+
+  // per-lane sets over this lane's slots and cached minima
+  uint32_t qb = 0, pb = 0, rb = 0, lb = 0, yb = 0, tb = 0;
+  int64_t lev = CT_INF64, lexp = CT_INF64, fmin = CT_INF64;
+  auto own = [&](int p) { return lane == (p & 31); };
+  auto bit = [&](int p) { return 1u << (p >> 5); };
+  auto turn_rec = [&](int p, int t) -> int4 { return __ldg(&a.turns[prog[p].turn0 + t]); };
+  auto arrival = [&](int i) -> int64_t { return (prog[i].arr_q * gap) >> 20; };
+  // Visit the programs whose bit is set in the per-lane slot mask `m` in program-index order
+  // (slot-major, lane-minor), skipping empty slots with one REDUX.OR.
+  auto for_each_set = [&](uint32_t m, auto&& fn) {
+    uint32_t slots = __reduce_or_sync(FULL_MASK, m);
+    while (slots) {
+      const int s = __ffs(slots) - 1;
+      slots &= slots - 1;
+      uint32_t b = __ballot_sync(FULL_MASK, (m >> s) & 1u);
+      while (b) {
+        const int p = 32 * s + __ffs(b) - 1;
+        b &= b - 1;
+        fn(p);
+      }
+    }
+  };
+  auto rescan_lev = [&]() {
+    int64_t m = CT_INF64;
+#pragma unroll
+    for (int s = 0; s < NS; ++s) m = min(m, tev[lane + 32 * s]);
+    lev = m;
+  };
+  auto rescan_lexp = [&]() {
+    int64_t m = CT_INF64;
+#pragma unroll
+    for (int s = 0; s < NS; ++s) m = min(m, texp[lane + 32 * s]);
+    lexp = m;
+  };
+  auto rescan_fmin = [&]() {
+    int64_t m = CT_INF64;
+#pragma unroll
+    for (int s = 0; s < NS; ++s) m = min(m, fin[lane + 32 * s]);
+    fmin = m;
+  };
+
+  int64_t now = 0, iter_end = 0, n_it = 0, busy = 0;
+  bool in_flight = false;
+  int64_t free_blk = a.kv[kv_i];
+  int64_t dfree = dram_on ? E.dram_blocks : 0, chan = 0;
+  int next_arr = 0;
+  const int64_t arr0 = arrival(0);
+  int64_t t_arr = arr0;
+  int32_t D = 0, turns_done = 0;
+  int n_run = 0, n_load = 0;  // n_load counts LOADING and READY
+  int64_t kv_sum = 0, pf = 0;
+  int status = CT_R_OK;
+  int64_t kv_at = -1, d_cur = 0;
+  double rd_cur = 0.0;
+
+  // evict(v): free its GPU blocks, DRAM write-through when the tier is on (R18); unpin.  Uniform.
+  auto evict_unpin = [&](int v) {
+    const int64_t g = gblk[v];
+    free_blk += g;
+    int32_t keep = 0;
+    if (dram_on) {
+      const int64_t nb = ceil_div_magic((uint32_t)ctx[v], bsm);
+      dfree += dblk[v];
+      if (nb > 0 && nb <= dfree) { keep = (int32_t)nb; dfree -= nb; }
+    }
+    if (own(v)) {
+      gblk[v] = 0;
+      if (dram_on) dblk[v] = keep;
+      if (pb & bit(v)) {
+        pb &= ~bit(v);
+        if (texp[v] != CT_INF64) { texp[v] = CT_INF64; rescan_lexp(); }
+      }
+    }
+    __syncwarp();
+  };
+
+  for (;;) {
+    // ---- next event (R1, R3) --------------------------------------------------------------
+    const int64_t t_prog = warp_min64_redux(eager ? min(lev, lexp) : lev);
+    int64_t t = min(t_prog, t_arr);
+    if (in_flight) t = min(t, iter_end);
+    if (t == CT_INF64) break;
+    now = t;
+
+    if (t_prog == now) {
+      // PinExpiry (EAGER): first µs with now > expiry while not in Q (R4/R15)
+      if (eager && __any_sync(FULL_MASK, lexp == now)) {
+        uint32_t me = 0;
+        if (lexp == now) {
+#pragma unroll
+          for (int s = 0; s < NS; ++s) me |= (texp[lane + 32 * s] == now ? 1u : 0u) << s;
+        }
+        const uint32_t cnt = __reduce_add_sync(FULL_MASK, (uint32_t)__popc(me));
+        if (lane == 0) acc->exp += cnt;
+        for_each_set(me, [&](int p) { evict_unpin(p); });
+      }
+      // ToolReturn (OnRequestArrive of a seen program) and LoadDone
+      if (__any_sync(FULL_MASK, lev == now)) {
+        uint32_t md = 0;
+        if (lev == now) {
+#pragma unroll
+          for (int s = 0; s < NS; ++s) md |= (tev[lane + 32 * s] == now ? 1u : 0u) << s;
+        }
+        const uint32_t mret = md & tb, mld = md & lb;
+        if (need_stats) {
+          for_each_set(mret, [&](int p) {  // estimator rows: Δ_obs = dur of the finished turn (R5)
+              const int4 tr = turn_rec(p, turn[p]);
+              const int64_t x = min((int64_t)tr.w, est.b_us);
+              const uint64_t x2 = (uint64_t)x * (uint64_t)x;
+              if (lane == 0) {
+                Stat* rows[2] = {&stats[F], &stats[tr.z]};
+#pragma unroll
+                for (int k = 0; k < 2; ++k) {
+                  Stat* q = rows[k];
+                  q->n += 1;
+                  q->s1 += x;
+                  const uint64_t lo = q->s2lo + x2;
+                  q->s2hi += (lo < x2);
+                  q->s2lo = lo;
+                }
+              }
+              __syncwarp();
+          });
+        }
+        if (md) {
+          bool rescan_e = false;
+#pragma unroll
+          for (int s = 0; s < NS; ++s) {
+            const int p = lane + 32 * s;
+            if ((mret >> s) & 1u) {
+              turn[p] += 1;
+              req[p] = now;
+              tev[p] = CT_INF64;
+              if (texp[p] != CT_INF64) { texp[p] = CT_INF64; rescan_e = true; }  // retained pin
+            }
+            if ((mld >> s) & 1u) tev[p] = CT_INF64;
+          }
+          qb |= mret;
+          tb &= ~mret;
+          yb |= mld;
+          lb &= ~mld;
+          rescan_lev();
+          if (rescan_e) rescan_lexp();
+        }
+        __syncwarp();
+      }
+    }
+    // ProgramArrival (programs arrive in index order)
+    while (t_arr == now) {
+      const int p = next_arr;
+      if (own(p)) { qb |= bit(p); req[p] = now; }
+      ++next_arr;
+      t_arr = next_arr < P ? arrival(next_arr) : CT_INF64;
+    }
+    __syncwarp();
+
+    // IterationEnd: requests whose last token was emitted finish, in index order (C-6)
+    if (in_flight && iter_end == now) {
+      in_flight = false;
+      uint32_t mf = 0;
+      if (fmin == n_it) {
+#pragma unroll
+        for (int s = 0; s < NS; ++s) mf |= (fin[lane + 32 * s] == n_it ? 1u : 0u) << s;
+      }
+      for_each_set(mf, [&](int p) {
+          // OnRequestFinish (PAPER.md:378-386)
+          const int tp = turn[p];
+          const int4 tr = turn_rec(p, tp);
+          const int nctx = ctx[p] + tr.x + tr.y;
+          const int64_t g = gblk[p];
+          --n_run;
+          kv_sum -= g;
+          if (own(p)) { rb &= ~bit(p); fin[p] = CT_INF64; ctx[p] = nctx; }
+          __syncwarp();
+          const int nt = prog[p].nturns;
+          if (tp == nt - 1) {  // last request: free its KV, the program completes
+            free_blk += g;
+            dfree += dblk[p];
+            if (own(p)) { gblk[p] = 0; dblk[p] = 0; req[p] = now - arrival(p); }
+            ++D;
+            turns_done += nt;
+            __syncwarp();
+          } else {
+            const int f = tr.z;
+            int64_t ttl = 0;
+            switch (pause) {
+              case CT_PAUSE_FIXED:
+              case CT_PAUSE_PAPER: {
+                const Stat sg = stats[F], sf = stats[f];
+                ttl = pause == CT_PAUSE_PAPER
+                          ? calc_ttl(sg, sf, est, D, turns_done)
+                          : simplified_ttl(sg, sf, est, polp->t_pin_us, polp->t_thresh_us);
+                break;
+              }
+              case CT_PAUSE_FITTED:
+                ttl = __ldg(&a.fitted[(int64_t)f * a.J + min(tp, a.J - 1)]);
+                break;
+              case CT_PAUSE_INFERCEPT: {  // preserve (no TTL) iff prediction < swap round trip
+                const int64_t pred = infercept_predict(stats[F], stats[f], est);
+                const int64_t blocks = ceil_div_magic((uint32_t)nctx, bsm);
+                const int64_t swap = 2 * ceil_ps_to_us((uint64_t)(blocks * E.c_h2d_ps));
+                ttl = pred < swap ? CT_INF64 : 0;
+                break;
+              }
+              default:
+                ttl = 0;
+            }
+            if (ttl > 0) {  // pin_request only if TTL != 0 (PAPER.md:633)
+              if (own(p)) {
+                pb |= bit(p);
+                if (ttl != CT_INF64) { texp[p] = now + ttl + 1; lexp = min(lexp, texp[p]); }
+              }
+            } else {
+              evict_unpin(p);
+            }
+            if (own(p)) { tev[p] = now + tr.w; lev = min(lev, tev[p]); tb |= bit(p); }
+            __syncwarp();
+          }
+      });
+      if (mf) rescan_fmin();
+    }
+    if (in_flight) continue;  // mid-iteration: events only mutate Q / stats / pins (R2)
+
+    // ---- scheduling point (R3) --------------------------------------------------------------
+    // (a) STEP reading: release expired pins of programs not waiting (PAPER.md:390-397, 638)
+    if (!eager) {
+      uint32_t mx = 0;
+      if (lexp <= now) {
+#pragma unroll
+        for (int s = 0; s < NS; ++s) mx |= ((((pb & tb) >> s) & 1u) && texp[lane + 32 * s] <= now ? 1u : 0u) << s;
+      }
+      const uint32_t cnt = __reduce_add_sync(FULL_MASK, (uint32_t)__popc(mx));
+      if (lane == 0) acc->exp += cnt;
+      for_each_set(mx, [&](int p) { evict_unpin(p); });
+    }
+    int admitted = 0;
+    bool stable = true;
+    if (__any_sync(FULL_MASK, (qb | yb) != 0)) {
+      // (b) loaded requests join the batch
+      const uint32_t cnt = __reduce_add_sync(FULL_MASK, (uint32_t)__popc(yb));
+      if (cnt) {
+        int64_t lk = 0, lp = 0;
+#pragma unroll
+        for (int s = 0; s < NS; ++s) {
+          if ((yb >> s) & 1u) {
+            const int p = lane + 32 * s;
+            fin[p] = n_it + turn_rec(p, turn[p]).y;
+            fmin = min(fmin, fin[p]);
+            lk += gblk[p];
+            lp += unc[p];
+          }
+        }
+        rb |= yb;
+        yb = 0;
+        kv_sum += (int64_t)warp_sum_u64((uint64_t)lk);
+        pf += (int64_t)warp_sum_u64((uint64_t)lp);
+        n_run += cnt;
+        n_load -= cnt;
+      }
+      // (c) admit loop (victims PAPER.md:645-655)
+      for (;;) {
+        if (!__any_sync(FULL_MASK, qb != 0)) break;
+        if (n_run + n_load >= E.max_batch) break;
+        int h = -1;
+        if (prio == CT_PRIO_PROG_FCFS) {  // lowest index among pinned-queued, else queued
+          uint32_t sel = qb & pb;
+          uint32_t slots = __reduce_or_sync(FULL_MASK, sel);
+          if (!slots) { sel = qb; slots = __reduce_or_sync(FULL_MASK, sel); }
+          const int s0 = __ffs(slots) - 1;
+          h = 32 * s0 + __ffs(__ballot_sync(FULL_MASK, (sel >> s0) & 1u)) - 1;
+        } else {  // REQ_FCFS: earliest request; PLAS: least attained service; ties: index
+          int64_t bk = CT_INF64;
+          int bp = 0x7fffffff;
+#pragma unroll
+          for (int s = 0; s < NS; ++s) {
+            const int pl = lane + 32 * s;
+            if ((qb >> s) & 1u) {
+              const int64_t k = plas ? svc[pl] : req[pl];
+              if (k < bk) { bk = k; bp = pl; }
+            }
+          }
+          const int64_t mk = warp_min64_redux(bk);
+          const int cand = bk == mk ? bp : 0x7fffffff;
+          h = (int)__reduce_min_sync(FULL_MASK, (uint32_t)cand);
+        }
+        const int4 tr = turn_rec(h, turn[h]);
+        const int64_t hctx = ctx[h];
+        const int64_t hg = gblk[h];
+        const int64_t need = (int64_t)ceil_div_magic((uint32_t)(hctx + tr.x + tr.y), bsm) - hg;
+        if (need > free_blk && (admitted == 0 || vany)) {
+          while (need > free_blk) {  // victims: latest program arrival first, never the head
+            const uint32_t cand = pb & ~(own(h) ? bit(h) : 0u);
+            const uint32_t slots = __reduce_or_sync(FULL_MASK, cand);
+            if (!slots) break;
+            const int s1 = 31 - __clz(slots);
+            const int v = 32 * s1 + 31 - __clz(__ballot_sync(FULL_MASK, (cand >> s1) & 1u));
+            evict_unpin(v);
+            if (lane == 0) acc->vict += 1;
+          }
+        }
+        if (need > free_blk) {  // HOL break
+          if (admitted > 0 && !vany &&
+              __reduce_or_sync(FULL_MASK, pb & ~(own(h) ? bit(h) : 0u)))
+            stable = false;
+          break;
+        }
+        // issue h
+        free_blk -= need;
+        const int32_t ng = (int32_t)(hg + need);
+        if (lane == 0) acc->bubble += now - req[h];
+        const bool hp = (__shfl_sync(FULL_MASK, pb, h & 31) >> (h >> 5)) & 1u;
+        const int64_t hd = dblk[h];
+        int64_t cached;
+        bool loading = false;
+        int64_t ld = 0;
+        if (hp) {
+          cached = hctx;
+          if (lane == 0) acc->hits += 1;
+        } else if (dram_on && hd > 0 && hd == (int64_t)ceil_div_magic((uint32_t)hctx, bsm)) {
+          cached = hctx;
+          loading = true;
+          ld = max(now, chan) + ceil_ps_to_us((uint64_t)(hd * E.c_h2d_ps));
+          chan = ld;
+          if (lane == 0) acc->reload += 1;
+        } else {
+          cached = 0;
+          if (lane == 0) acc->recomp += hctx;
+        }
+        const int64_t u = hctx + tr.x - cached;
+        if (lane == 0) acc->prefill += u;
+        if (own(h)) {
+          qb &= ~bit(h);
+          pb &= ~bit(h);  // a queued pin has no pending expiry (cleared at its return)
+          gblk[h] = ng;
+          unc[h] = (int32_t)u;
+          if (loading) {
+            lb |= bit(h);
+            tev[h] = ld;
+            lev = min(lev, ld);
+          } else {
+            rb |= bit(h);
+            fin[h] = n_it + tr.y;
+            fmin = min(fmin, fin[h]);
+          }
+        }
+        if (loading) {
+          ++n_load;
+        } else {
+          ++n_run;
+          kv_sum += ng;
+          pf += u;
+        }
+        ++admitted;
+        __syncwarp();
+      }
+      // (d) unschedulable: the head missed with nothing running or loading; the victim loop
+      // has already released every other pin, so no future event can free memory (C-5 5c)
+      if (admitted == 0 && n_run == 0 && n_load == 0 && __any_sync(FULL_MASK, qb != 0)) {
+        status = CT_R_UNSCHEDULABLE;
+        break;
+      }
+    }
+    // (e) start the next iteration(s) (linear cost model, R16)
+    if (n_run > 0) {
+      if (kv_sum != kv_at) {
+        kv_at = kv_sum;
+        d_cur = ceil_ps_to_us((uint64_t)(E.c0_ps + E.c_kv_ps * bs * kv_sum));
+        rd_cur = 1.0 / (double)d_cur;
+      }
+      const int64_t d = d_cur;
+      int64_t k = 1, dur;
+      if (pf > 0) {
+        dur = ceil_ps_to_us((uint64_t)(E.c0_ps + E.c_kv_ps * bs * kv_sum + E.c_pf_ps * pf));
+        pf = 0;
+      } else {
+        if (stable) {
+          // macro-step: identical iterations up to the first finish or the first boundary at
+          // or after the next external event (arrival, tool return, load done, pin expiry)
+          const int64_t mfin = warp_min64_redux(fmin);
+          const int64_t te = min(warp_min64_redux(min(lev, lexp)), t_arr);
+          const int64_t m = mfin - n_it;
+          int64_t j = m;
+          if (te != CT_INF64) {
+            const int64_t gap2 = te - now;  // >= 1
+            const double estq = (double)gap2 * rd_cur;
+            if (estq < (double)m + 2.0) {
+              int64_t jb = (int64_t)estq;
+              while (jb * d < gap2) ++jb;
+              while (jb > 1 && (jb - 1) * d >= gap2) --jb;
+              if (jb < j) j = jb;
+            }
+          }
+          k = j;
+        }
+        dur = k * d;
+      }
+      if (n_it + k > E.max_iters) { status = CT_R_EVENT_BUDGET; break; }
+      n_it += k;
+      iter_end = now + dur;
+      busy += dur;
+      if (plas) {
+#pragma unroll
+        for (int s = 0; s < NS; ++s)
+          if ((rb >> s) & 1u) svc[lane + 32 * s] += dur;  // owners accrue their running programs
+      }
+      in_flight = true;
+    }
+  }
+  if (status == CT_R_OK && D != P) status = CT_R_UNSCHEDULABLE;
+
+  // ---- per-replica summary (A-8) --------------------------------------------------------------
+  __syncwarp();
+  const int64_t ri = r - a.r_begin;
+  int64_t jsum = 0, jmax = 0, p50 = 0, p99 = 0;
+  if (status == CT_R_OK) {
+    int64_t ls = 0, lm = 0;
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+      const int p = lane + 32 * s;
+      if (p < P) { ls += req[p]; lm = max(lm, req[p]); }
+    }
+    jsum = (int64_t)warp_sum_u64((uint64_t)ls);
+    jmax = warp_max64(lm);
+    // nearest rank (R20): value v with #(x < v) < rank <= #(x <= v)
+    const int r50 = (50 * P + 99) / 100, r99 = (99 * P + 99) / 100;
+    int64_t c50 = CT_INF64, c99 = CT_INF64;
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+      const int p = lane + 32 * s;
+      if (p < P) {
+        const int64_t v = req[p];
+        int lt = 0, le = 0;
+        for (int q = 0; q < P; ++q) {
+          const int64_t x = req[q];
+          lt += x < v;
+          le += x <= v;
+        }
+        if (lt < r50 && r50 <= le) c50 = v;
+        if (lt < r99 && r99 <= le) c99 = v;
+      }
+    }
+    p50 = warp_min64_redux(c50);
+    p99 = warp_min64_redux(c99);
+  }
+  if (lane == 0) {
+    ct_replica_summary o;
+    if (status == CT_R_OK) {
+      o.status = status;
+      o.n_done = D;
+      o.turns_done = turns_done;
+      o.sum_jct_us = jsum;
+      o.max_jct_us = jmax;
+      o.p50_jct_us = p50;
+      o.p99_jct_us = p99;
+      o.sum_bubble_us = acc->bubble;
+      o.makespan_us = now - arr0;  // the last event processed is the last completion
+      o.iterations = n_it;
+      o.busy_us = busy;
+      o.prefill_tokens = acc->prefill;
+      o.recompute_tokens = acc->recomp;
+      o.pin_hits = acc->hits;
+      o.pin_expiries = acc->exp;
+      o.victims = acc->vict;
+      o.reloads = acc->reload;
+    } else {
+      int64_t* w = (int64_t*)&o;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) w[i] = 0;
+      o.status = status;
+    }
+    a.out[ri] = o;
+  }
+  if (a.jct) {
+    int64_t* jo = a.jct + ri * P;
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+      const int p = lane + 32 * s;
+      if (p < P) jo[p] = status == CT_R_OK ? req[p] : -1;
+    }
+  }
+  __syncwarp();
+}
+
 template <int NS, int MINB>
 __global__ void __launch_bounds__(128, MINB) replay_kernel(ReplayArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -1035,7 +1050,7 @@ __global__ void __launch_bounds__(128, MINB) replay_kernel(ReplayArgs a) {
     if (NS == 1)
       replay_one_w32(a, r, (Stat*)wm, lane);
     else
-      replay_one<NS>(a, r, wm, lane);
+      replay_one_ns<NS>(a, r, wm, lane);
   }
 }
 
@@ -1060,7 +1075,11 @@ static void* pick(int ns) {
         default: return (void*)replay_kernel<1, 8>;
       }
     case 2: return (void*)replay_kernel<2, 1>;
+    case 3: return (void*)replay_kernel<3, 1>;
     case 4: return (void*)replay_kernel<4, 1>;
+    case 5: return (void*)replay_kernel<5, 1>;
+    case 6: return (void*)replay_kernel<6, 1>;
+    case 7: return (void*)replay_kernel<7, 1>;
     case 8: return (void*)replay_kernel<8, 1>;
   }
   return nullptr;

@@ -116,7 +116,7 @@ ALL_POLICIES = [cf.VLLM, cf.VLLM_LMCACHE, cf.PROG_FCFS, cf.CONTINUUM, cf.ttl_gri
                 cf.Policy(cf.PRIO_PROG_FCFS, cf.PAUSE_INFERCEPT, flags=cf.FLAG_STEP_EXPIRY)]
 
 
-@pytest.mark.parametrize("P", [1, 7, 32, 33, 64, 100, 128, 200, 256])
+@pytest.mark.parametrize("P", [1, 7, 32, 33, 64, 70, 100, 128, 150, 180, 200, 256])
 def test_workloads_all_policies(ctx, P):
     n_seeds = 6 if P <= 64 else 2
     tr = traces.generate(n_seeds, P, mix="mix", ctx_cap=8192, stream=P)

@@ -1,3 +1,3 @@
-python -m pytest tests/test_gpu_parity.py -q -x 2>&1 | tail -1
-for i in 1 2; do for mb in 6 8; do echo "minb $mb"; CT_REPLAY_MINB=$mb python tools/prof_kernels.py replay cfg3 64 | tail -1 | cut -c1-100; done; done
-ncu --metrics smsp__inst_executed.sum,gpu__time_duration.sum,smsp__issue_active.avg.pct_of_peak_sustained_active,sm__warps_active.avg.pct_of_peak_sustained_active --clock-control none --csv -k regex:replay -c 1 python tools/prof_kernels.py replay cfg3 16 2>/dev/null | grep replay_kernel | awk -F'","' '{print $(NF-2), $NF}'
+python -m pytest tests/test_gpu_parity.py -q -x 2>&1 | tail -3
+python tools/prof_kernels.py replay cfg2 4096 | tail -1 | cut -c1-120
+ncu --metrics smsp__inst_executed.sum,gpu__time_duration.sum,smsp__issue_active.avg.pct_of_peak_sustained_active,sm__warps_active.avg.pct_of_peak_sustained_active --clock-control none --csv -k regex:replay -c 1 python tools/prof_kernels.py replay cfg2 512 2>/dev/null | grep replay_kernel | awk -F'","' '{print $(NF-2), $NF}'
