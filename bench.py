@@ -253,6 +253,7 @@ def main():
 
     import paper_2511_02230_b200 as ct
     from ctgen import configs as cf
+    from paper_2511_02230_b200 import dist as D
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -268,8 +269,8 @@ def main():
     w = load_workload(args.workload, args.seeds)
     sw, eng, tr = w.sweep, w.engine, w.trace
     R = sw.n_replicas
-    rb, re_ = R * rank // world, R * (rank + 1) // world
-    shard = (R + world - 1) // world
+    rb, re_ = D.shard_range(R, rank, world)
+    shard = D.shard_capacity(R, world)
     dur_np, off, ctxj, wj = fit_inputs(tr)
     J = len(ctxj)
     cp = ct.cost_params(eng.c_pf_ps, 200, eng.bs, sw.estimator.a_num, sw.estimator.a_den, 50_000,
@@ -293,12 +294,7 @@ def main():
         if timed:
             b.record(stream)
             kev.append((a, b))
-        if world > 1:
-            dist.all_gather_into_tensor(gathered, summ)
-            full = torch.cat([gathered[k * shard: k * shard + (R * (k + 1) // world - R * k // world)]
-                              for k in range(world)])
-        else:
-            full = summ
+        full = D.gather_summaries(summ, R, world, out=gathered)  # A-9: one NCCL all-gather
         cells = ct.ct_jct_stats(ctx, full, sw.n_cells)
         return cells
 
