@@ -1,13 +1,14 @@
 // ttl_fit.cu — the TTL fit: one HBM pass over duration samples.
 //
-// Kernel 1 (fit_hist): persistent warps, each streaming its own chunks of tool-grouped (CSR)
-// int32 samples with 16-B streaming loads (8 in flight per lane).  Every sample lands in the
-// warp's lane-pair-replicated shared-memory histogram over the TTL grid buckets
-// k = min(ceil(d / step), K) as (count, sum of k step - d) with fire-and-forget 32-bit shared
-// reductions (conflict-free up to 2-way), and in the thread's 64-bit register statistics
-// (sum t~, sum t~^2) of t~ = min(d, b) for the paper mode (reading R5).
-// After each chunk the warp merges its replicas and flushes with integer atomics (order
-// independent, hence deterministic).
+// Kernel 1 (fit_hist): persistent CTAs of 8 warps stream CTA-level chunks of tool-grouped (CSR)
+// int32 samples with 16-B streaming loads (register double buffering, 8 int4 in flight per lane).
+// Every sample lands in the CTA's histogram over the TTL grid buckets k = min(ceil(d / step), K)
+// as (count, sum of k step - d) with fire-and-forget 32-bit shared reductions; the histogram has
+// one replica per lane index shared by the CTA's warps, so a warp instruction never conflicts.
+// Each thread keeps the paper-mode statistics (sum t~, sum t~^2) of t~ = min(d, b) in registers
+// (reading R5).  After each chunk the replicas are merged and flushed with
+// integer atomics (order independent, hence deterministic).  Older per-warp variants remain
+// selectable for measurement (CT_FIT_VARIANT).
 // Kernel 2 (fit_scan): one CTA per tool row: block prefix scan of the bucket counts and sums in
 // shared memory, then per turn bucket j n U(k) in 128-bit integers (extension C-4) and a warp
 // argmax with the smallest k on ties; the pooled row sums the tool rows; tools with n_f < N take
@@ -32,14 +33,19 @@ struct FitVariant {
 static const FitVariant kVariants[] = {{16, false, 16}, {16, true, 16}, {8, false, 8},
                                        {8, true, 8},    {32, false, 16}, {16, true, 8},
                                        {8, true, 4},    {4, false, 8},   {4, false, 4},
-                                       {8, false, 4}};
-static int g_variant = -1;  // default 2: measured best on B200 (DESIGN.md §8 variant table)
+                                       {8, false, 4},   {32, false, 4},   // 10: CTA-shared, U 4
+                                       {32, false, 8},                    // 11: CTA-shared, U 8
+                                       {32, false, 8},                    // 12: 11 + 32-bit sums
+                                       {32, false, 4},                    // 13: 12 with U 4
+                                       {32, false, 6}};                   // 14: 12 with U 6
+static int g_variant = -1;  // default 12: measured best on B200 (DESIGN.md §8 variant table)
 
 static int variant() {
+  static_assert(sizeof kVariants / sizeof kVariants[0] == 15, "variant table / hist_fn mismatch");
   if (g_variant < 0) {
     const char* e = getenv("CT_FIT_VARIANT");
-    int v = e ? atoi(e) : 2;
-    g_variant = (v >= 0 && v < (int)(sizeof kVariants / sizeof kVariants[0])) ? v : 2;
+    int v = e ? atoi(e) : 12;
+    g_variant = (v >= 0 && v < (int)(sizeof kVariants / sizeof kVariants[0])) ? v : 12;
   }
   return g_variant;
 }
@@ -218,7 +224,31 @@ __global__ void __launch_bounds__(FIT_THREADS) fit_hist_kernel(FitArgs a) {
 // while the footprint per warp is 1/FW of a lane-private histogram.  Chunks are CTA-level.
 constexpr int FW = 8;
 
-template <bool IDENT, int U>
+// CTA-kernel sample: count at [base + 256 b], remainder at +128 (one address, immediate offset);
+// the caller keeps 4 independent 64-bit sum-of-squares accumulators (ILP for the accumulate form
+// of IMAD.WIDE) and, when b < 2^26, a 32-bit sum accumulator flushed every 32 samples.
+template <bool IDENT, typename S1>
+__device__ __forceinline__ void sample_cta(const Lane& L, uint32_t base, int32_t d, S1& s1,
+                                           uint64_t& s2) {
+  const uint32_t x = (uint32_t)d + L.xoff;
+  uint32_t q;
+  if (IDENT) {
+    q = x;
+  } else {
+    uint64_t p = __umulhi(x, L.mlo);
+    mad_wide(p, x, L.mhi);
+    q = (uint32_t)(p >> 32);
+  }
+  const uint32_t b = min(q, L.K);
+  const uint32_t addr = base + b * 256u;
+  red_shared(addr, 1u);
+  red_shared(addr + 128u, b * L.step - (uint32_t)d);
+  const uint32_t t = min((uint32_t)d, L.b_us);
+  s1 += t;
+  mad_wide(s2, t, t);
+}
+
+template <bool IDENT, int U, bool FAST32>
 __global__ void __launch_bounds__(32 * FW) fit_hist_cta_kernel(FitArgs a) {
   extern __shared__ __align__(16) uint32_t hsm[];
   const int K = a.K;
@@ -254,6 +284,22 @@ __global__ void __launch_bounds__(32 * FW) fit_hist_cta_kernel(FitArgs a) {
     const int4* v = (const int4*)(a.dur + va);
     const int64_t nv = (vb - va) >> 2;
     constexpr int T = 32 * FW;
+    const uint32_t base = L.cnt_base;
+    uint64_t q1 = 0, q2 = 0, q3 = 0;  // extra sum-of-squares accumulators (ILP)
+    uint32_t s1w = 0;                  // 32-bit partial sum, flushed per 4U samples (b < 2^26)
+    auto run4 = [&](const int4& x) {
+      if (FAST32) {
+        sample_cta<IDENT>(L, base, x.x, s1w, s2);
+        sample_cta<IDENT>(L, base, x.y, s1w, q1);
+        sample_cta<IDENT>(L, base, x.z, s1w, q2);
+        sample_cta<IDENT>(L, base, x.w, s1w, q3);
+      } else {
+        sample_cta<IDENT>(L, base, x.x, s1, s2);
+        sample_cta<IDENT>(L, base, x.y, s1, q1);
+        sample_cta<IDENT>(L, base, x.z, s1, q2);
+        sample_cta<IDENT>(L, base, x.w, s1, q3);
+      }
+    };
     int64_t i = tid;
     int4 A[U], B[U];
     bool have_a = i + (U - 1) * T < nv;
@@ -269,12 +315,8 @@ __global__ void __launch_bounds__(32 * FW) fit_hist_cta_kernel(FitArgs a) {
         for (int u = 0; u < U; ++u) B[u] = __ldcs(v + ib + u * T);
       }
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        sample<IDENT, 64, false>(L, A[u].x, s1, s2);
-        sample<IDENT, 64, false>(L, A[u].y, s1, s2);
-        sample<IDENT, 64, false>(L, A[u].z, s1, s2);
-        sample<IDENT, 64, false>(L, A[u].w, s1, s2);
-      }
+      for (int u = 0; u < U; ++u) run4(A[u]);
+      if (FAST32) { s1 += s1w; s1w = 0; }
       i = ib;
       if (!have_b) break;
       const int64_t ia = ib + U * T;
@@ -284,21 +326,15 @@ __global__ void __launch_bounds__(32 * FW) fit_hist_cta_kernel(FitArgs a) {
         for (int u = 0; u < U; ++u) A[u] = __ldcs(v + ia + u * T);
       }
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        sample<IDENT, 64, false>(L, B[u].x, s1, s2);
-        sample<IDENT, 64, false>(L, B[u].y, s1, s2);
-        sample<IDENT, 64, false>(L, B[u].z, s1, s2);
-        sample<IDENT, 64, false>(L, B[u].w, s1, s2);
-      }
+      for (int u = 0; u < U; ++u) run4(B[u]);
+      if (FAST32) { s1 += s1w; s1w = 0; }
       i = ia;
     }
     for (; i < nv; i += T) {
-      const int4 x = __ldcs(v + i);
-      sample<IDENT, 64, false>(L, x.x, s1, s2);
-      sample<IDENT, 64, false>(L, x.y, s1, s2);
-      sample<IDENT, 64, false>(L, x.z, s1, s2);
-      sample<IDENT, 64, false>(L, x.w, s1, s2);
+      run4(__ldcs(v + i));
+      if (FAST32) { s1 += s1w; s1w = 0; }
     }
+    s2 += q1 + q2 + q3;
     const uint64_t w1 = warp_sum_u64(s1), w2 = warp_sum_u64(s2 & 0xffffffffull),
                    w3 = warp_sum_u64(s2 >> 32);
     if (lane == 0) { red[tid >> 5][0] = w1; red[tid >> 5][1] = w2; red[tid >> 5][2] = w3; }
@@ -349,8 +385,11 @@ static void* hist_fn(int v) {
     case 7: return (void*)fit_hist_kernel<IDENT, 4, false, 8>;
     case 8: return (void*)fit_hist_kernel<IDENT, 4, false, 4>;
     case 9: return (void*)fit_hist_kernel<IDENT, 8, false, 4>;
-    case 10: return (void*)fit_hist_cta_kernel<IDENT, 4>;
-    default: return (void*)fit_hist_cta_kernel<IDENT, 8>;
+    case 10: return (void*)fit_hist_cta_kernel<IDENT, 4, false>;
+    case 11: return (void*)fit_hist_cta_kernel<IDENT, 8, false>;
+    case 12: return (void*)fit_hist_cta_kernel<IDENT, 8, true>;  // b < 2^26 fast sums
+    case 13: return (void*)fit_hist_cta_kernel<IDENT, 4, true>;
+    default: return (void*)fit_hist_cta_kernel<IDENT, 6, true>;
   }
 }
 
@@ -454,13 +493,16 @@ __global__ void __launch_bounds__(SCAN_THREADS) fit_scan_kernel(ScanArgs a) {
 
 cudaError_t launch_fit_hist(const FitArgs& a, int grid, cudaStream_t s) {
   const int smem = fit_hist_smem(a.K);
-  void* k = a.step == 1 ? hist_fn<true>(variant()) : hist_fn<false>(variant());
+  int v = variant();
+  if (v >= 12 && a.b_us >= (1ll << 26)) v = 11;  // 32-bit partial sums need b < 2^26 µs
+  void* k = a.step == 1 ? hist_fn<true>(v) : hist_fn<false>(v);
   void* args[] = {(void*)&a};
   return cudaLaunchKernel(k, dim3(grid), dim3(fit_hist_threads()), args, smem, s);
 }
 
 int fit_hist_occupancy(int smem) {
-  for (void* k : {hist_fn<true>(variant()), hist_fn<false>(variant())})
+  for (void* k : {hist_fn<true>(variant()), hist_fn<false>(variant()), hist_fn<true>(11),
+                  hist_fn<false>(11)})
     if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
       return 0;
   int nb = 0;
