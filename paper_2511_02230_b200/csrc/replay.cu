@@ -35,6 +35,22 @@ int replay_smem_per_warp(int ns, int F) {
 // parallel, and only order-dependent work (finishes, DRAM write-through, estimator updates,
 // admission) is serialised in program-index order with the operands broadcast by shuffles.
 // Same semantics as replay_one<NS> (C-5/C-6), checked byte for byte by the tests.
+// Iterations in one macro-step: the smallest j <= m (m = iterations until the first finish)
+// whose end dur1 + (j-1) d is at or after the next external event at offset gap (INF-safe).
+// rd ~ 1/d estimates ceil((gap - dur1) / d); two integer corrections make it exact.
+__device__ __forceinline__ int64_t macro_iters(int64_t m, int64_t gap, int64_t dur1, int64_t d,
+                                               double rd) {
+  if (gap >= CT_INF64 / 2) return m;
+  const int64_t g = gap - dur1;
+  if (g <= 0) return 1;
+  const double est = (double)g * rd;
+  if (est >= (double)m + 1.0) return m;
+  int64_t c = (int64_t)est;
+  while (c * d < g) ++c;
+  while (c > 0 && (c - 1) * d >= g) --c;
+  return min(m, 1 + c);
+}
+
 struct Acc {  // per-replica summary counters (P <= 32 path)
   int64_t bubble, prefill, recomp, busy;
   int32_t hits, exp, vict, reload;
@@ -389,36 +405,23 @@ __device__ __forceinline__ void replay_one_w32(const ReplayArgs& a, int64_t r, S
         rd_cur = 1.0 / (double)d_cur;
       }
       const int64_t d = d_cur;
-      int64_t k = 1, dur;
-      if (pf > 0) {
-        dur = ceil_ps_to_us((uint64_t)(E.c0_ps + E.c_kv_ps * bs * kv_sum + E.c_pf_ps * pf));
-        pf = 0;
-      } else {
-        if (stable) {
-          // macro-step: identical iterations up to the first finish or the first boundary at
-          // or after the next external event (arrival, tool return, load done, pin expiry)
-          const int64_t mfin = warp_min64_redux(st == S_RUN ? fin : CT_INF64);
-          const int64_t te = warp_min64_redux(min(tev, texp));
-          if (eager) t_plan = te;  // = the next loop's program-event minimum (nothing changes)
-          const int64_t m = mfin - n_it;
-          int64_t j = m;
-          if (te != CT_INF64) {
-            const int64_t gap2 = te - now;  // >= 1
-            const double estq = (double)gap2 * rd_cur;
-            if (estq < (double)m + 2.0) {
-              int64_t jb = (int64_t)estq;
-              while (jb * d < gap2) ++jb;
-              while (jb > 1 && (jb - 1) * d >= gap2) --jb;
-              if (jb < j) j = jb;
-            }
-          }
-          k = j;
+      // the first iteration carries the prefill of newly admitted requests (R16)
+      const int64_t dur1 =
+          pf > 0 ? ceil_ps_to_us((uint64_t)(E.c0_ps + E.c_kv_ps * bs * kv_sum + E.c_pf_ps * pf)) : d;
+      pf = 0;
+      int64_t k = 1;
+      if (stable) {
+        // macro-step: the first iteration plus identical decode iterations, up to the first
+        // finish or the first boundary at or after the next external event
+        const int64_t mfin = warp_min64_redux(st == S_RUN ? fin : CT_INF64);
+        const int64_t te = warp_min64_redux(min(tev, texp));
+        if (eager) t_plan = te;  // = the next loop's program-event minimum (nothing changes)
+        k = macro_iters(mfin - n_it, te - now, dur1, d, rd_cur);
 #ifdef CT_DEBUG_LOOPS
-          ++dbg_macro;
+        ++dbg_macro;
 #endif
-        }
-        dur = k * d;
       }
+      const int64_t dur = dur1 + (k - 1) * d;
       if (n_it + k > E.max_iters) { status = CT_R_EVENT_BUDGET; break; }
       n_it += k;
       iter_end = now + dur;
@@ -923,32 +926,19 @@ __device__ __forceinline__ void replay_one_ns(const ReplayArgs& a, int64_t r, un
         rd_cur = 1.0 / (double)d_cur;
       }
       const int64_t d = d_cur;
-      int64_t k = 1, dur;
-      if (pf > 0) {
-        dur = ceil_ps_to_us((uint64_t)(E.c0_ps + E.c_kv_ps * bs * kv_sum + E.c_pf_ps * pf));
-        pf = 0;
-      } else {
-        if (stable) {
-          // macro-step: identical iterations up to the first finish or the first boundary at
-          // or after the next external event (arrival, tool return, load done, pin expiry)
-          const int64_t mfin = warp_min64_redux(fmin);
-          const int64_t te = min(warp_min64_redux(min(lev, lexp)), t_arr);
-          const int64_t m = mfin - n_it;
-          int64_t j = m;
-          if (te != CT_INF64) {
-            const int64_t gap2 = te - now;  // >= 1
-            const double estq = (double)gap2 * rd_cur;
-            if (estq < (double)m + 2.0) {
-              int64_t jb = (int64_t)estq;
-              while (jb * d < gap2) ++jb;
-              while (jb > 1 && (jb - 1) * d >= gap2) --jb;
-              if (jb < j) j = jb;
-            }
-          }
-          k = j;
-        }
-        dur = k * d;
+      // the first iteration carries the prefill of newly admitted requests (R16)
+      const int64_t dur1 =
+          pf > 0 ? ceil_ps_to_us((uint64_t)(E.c0_ps + E.c_kv_ps * bs * kv_sum + E.c_pf_ps * pf)) : d;
+      pf = 0;
+      int64_t k = 1;
+      if (stable) {
+        // macro-step: the first iteration plus identical decode iterations, up to the first
+        // finish or the first boundary at or after the next external event
+        const int64_t mfin = warp_min64_redux(fmin);
+        const int64_t te = min(warp_min64_redux(min(lev, lexp)), t_arr);
+        k = macro_iters(mfin - n_it, te - now, dur1, d, rd_cur);
       }
+      const int64_t dur = dur1 + (k - 1) * d;
       if (n_it + k > E.max_iters) { status = CT_R_EVENT_BUDGET; break; }
       n_it += k;
       iter_end = now + dur;

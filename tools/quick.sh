@@ -1,1 +1,4 @@
-for v in 10; do echo "variant $v"; CT_FIT_VARIANT=$v ncu --metrics gpu__time_duration.sum,smsp__issue_active.avg.pct_of_peak_sustained_active,sm__warps_active.avg.pct_of_peak_sustained_active,l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed,l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_atom.sum,l1tex__data_pipe_lsu_wavefronts_mem_shared_op_atom.sum,smsp__inst_executed.sum,smsp__pcsamp_warps_issue_stalled_barrier,smsp__pcsamp_warps_issue_stalled_wait,smsp__pcsamp_warps_issue_stalled_long_scoreboard,smsp__pcsamp_warps_issue_stalled_short_scoreboard,smsp__pcsamp_warps_issue_stalled_mio_throttle,smsp__pcsamp_warps_issue_stalled_lg_throttle,smsp__pcsamp_warps_issue_stalled_selected,smsp__pcsamp_warps_issue_stalled_not_selected,smsp__pcsamp_warps_issue_stalled_dispatch_stall,smsp__pcsamp_warps_issue_stalled_math_pipe_throttle --clock-control none --csv -k regex:fit_hist_cta -s 1 -c 1 python tools/prof_kernels.py fit 28 2>/dev/null | grep "fit_hist" | tee /dev/stderr | awk -F'","' '{print $(NF-2), $NF}'; done
+python -m pytest tests/test_gpu_parity.py -q -x 2>&1 | tail -2
+for i in 1 2; do python tools/prof_kernels.py replay cfg3 64 | tail -1 | cut -c1-100; done
+python tools/prof_kernels.py replay cfg2 4096 | tail -1 | cut -c1-100
+ncu --metrics smsp__inst_executed.sum,gpu__time_duration.sum,smsp__issue_active.avg.pct_of_peak_sustained_active --clock-control none --csv -k regex:replay -c 1 python tools/prof_kernels.py replay cfg3 16 2>/dev/null | grep replay_kernel | awk -F'","' '{print $(NF-2), $NF}'
