@@ -284,3 +284,34 @@ def synthetic_samples_torch(log2n: int, n_tools: int = 32, seed: int = 1234, dev
         med = float(TOOLS[f % N_TOOLS][3])
         dur[a:b] = torch.clamp(med * torch.exp(0.8 * z), 1, 1.2e8).to(torch.int32)
     return dur, off
+
+
+def turn_scaling(tr: TraceSet, k: int) -> TraceSet:
+    """Turn-scaling transform of the robustness study.
+
+    Every program's turn list is repeated k times and every token count is divided by k
+    (integer division, minimum 1), so total token volume is kept within rounding.  Tool calls
+    and durations repeat with their turns; the last turn of each non-final copy calls the
+    program's first tool with its first duration (the original final turn has no tool).
+    """
+    if k < 1:
+        raise ValueError("k >= 1")
+    if k == 1:
+        return tr
+    progs = np.zeros_like(tr.programs)
+    rows = []
+    for i in range(len(tr.programs)):
+        t0, nt = int(tr.programs["turn0"][i]), int(tr.programs["nturns"][i])
+        base = tr.turns[t0:t0 + nt]
+        first_tool = (int(base[0, 2]), int(base[0, 3])) if nt > 1 else (0, 100_000)
+        progs[i] = (tr.programs["arr_q"][i], len(rows), nt * k)
+        for c in range(k):
+            for j in range(nt):
+                new = max(int(base[j, 0]) // k, 1 if j == 0 else 0)
+                dec = max(int(base[j, 1]) // k, 1)
+                tool, dur = int(base[j, 2]), int(base[j, 3])
+                if j == nt - 1 and c < k - 1:
+                    tool, dur = first_tool
+                rows.append((new, dec, tool, dur))
+    turns = np.array(rows, dtype=np.int32).reshape(-1, 4)
+    return TraceSet(progs, turns, tr.n_seeds, tr.n_programs, tr.n_tools, tr.pclass)
