@@ -621,6 +621,7 @@ __device__ __forceinline__ void replay_one_ns(const ReplayArgs& a, int64_t r, un
       dfree += dblk[v];
       if (nb > 0 && nb <= dfree) { keep = (int32_t)nb; dfree -= nb; }
     }
+    __syncwarp();  // every lane has read v's fields before the owner rewrites them
     if (own(v)) {
       gblk[v] = 0;
       if (dram_on) dblk[v] = keep;
@@ -728,12 +729,14 @@ __device__ __forceinline__ void replay_one_ns(const ReplayArgs& a, int64_t r, un
           const int64_t g = gblk[p];
           --n_run;
           kv_sum -= g;
+          __syncwarp();
           if (own(p)) { rb &= ~bit(p); fin[p] = CT_INF64; ctx[p] = nctx; }
           __syncwarp();
           const int nt = prog[p].nturns;
           if (tp == nt - 1) {  // last request: free its KV, the program completes
             free_blk += g;
             dfree += dblk[p];
+            __syncwarp();
             if (own(p)) { gblk[p] = 0; dblk[p] = 0; req[p] = now - arrival(p); }
             ++D;
             turns_done += nt;
@@ -886,6 +889,7 @@ __device__ __forceinline__ void replay_one_ns(const ReplayArgs& a, int64_t r, un
         }
         const int64_t u = hctx + tr.x - cached;
         if (lane == 0) acc->prefill += u;
+        __syncwarp();  // every lane has read h's fields before the owner rewrites them
         if (own(h)) {
           qb &= ~bit(h);
           pb &= ~bit(h);  // a queued pin has no pending expiry (cleared at its return)

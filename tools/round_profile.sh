@@ -12,4 +12,8 @@ ncu --set full --clock-control none --import-source on -k regex:replay_kernel -c
     -o $OUT/${R}_replay_cfg3 python tools/prof_kernels.py replay cfg3 16 > $OUT/${R}_ncu_replay.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:fit_hist -s 1 -c 1 \
     -o $OUT/${R}_fit_hist python tools/prof_kernels.py fit 28 > $OUT/${R}_ncu_fit.log 2>&1
+for t in memcheck racecheck synccheck initcheck; do
+  echo "== $t" >> $OUT/${R}_sanitizer.txt
+  timeout 600 compute-sanitizer --tool $t python tools/sanitize.py 2>&1 | grep -E "SUMMARY|sanitize run" >> $OUT/${R}_sanitizer.txt
+done
 ls -la $OUT

@@ -1,0 +1,21 @@
+"""Small fit + replay + stats run for compute-sanitizer (memcheck / racecheck / synccheck)."""
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np, torch
+import paper_2511_02230_b200 as ct
+from ctgen import configs as cf, traces
+ctx = ct.Context(0)
+for P, mix in ((16, "mix"), (70, "mix")):
+    tr = traces.generate(2, P, mix=mix, ctx_cap=8192, stream=P)
+    fitted = np.tile(np.array([[0, 200_000, 3_000_000]], np.int64), (tr.n_tools, 1))
+    eng = cf.Engine(**{**cf.ENGINE_8B.__dict__, "dram_blocks": 40 * P})
+    pols = [cf.VLLM_LMCACHE, cf.CONTINUUM, cf.ttl_grid(500_000), cf.AUTELLIX, cf.INFERCEPT,
+            cf.Policy(cf.PRIO_PROG_FCFS, cf.PAUSE_FITTED, flags=cf.FLAG_STEP_EXPIRY)]
+    sw = cf.Sweep(2, [300_000], [600, 3000], pols, fitted=fitted)
+    s, j = ct.ct_simulate_batch(ctx, ct.DeviceTrace(tr), sw, eng, jct=True)
+    c = ct.ct_jct_stats(ctx, s, sw.n_cells)
+dur, off = traces.tool_samples(tr)
+cp = ct.cost_params(13_400_000, 200, 16, 1, 10, 50_000, 256, [2000, 8000], [1, 2])
+ct.ct_fit_ttl(ctx, torch.from_numpy(dur).cuda(), off, cp, cf.Estimator())
+torch.cuda.synchronize()
+print("sanitize run ok")
