@@ -345,7 +345,8 @@ int ct_fit_ttl(ct_ctx* c, const ct_samples* sm, const ct_cost_params* cp,
   const bool cta = ct::fit_hist_cta_chunks();
   const int R = cta ? 1 : ct::fit_hist_repl();
   const int per_thread_div = cta ? 256 : 32;
-  int64_t CH = cta ? (1ll << 17) : (1ll << 16);
+  const bool ranges = ct::fit_hist_ranges();
+  int64_t CH = ranges ? (1ll << 20) : cta ? (1ll << 17) : (1ll << 16);
   const int64_t rdiv = cta ? 32 : R;
   while (CH > 256 && (CH / rdiv + 64) * (uint64_t)cp->grid_step_us >= (1ull << 32)) CH >>= 1;
   while (CH > 256 && !cta && CH / R + 64 >= (1 << 16)) CH >>= 1;
@@ -387,8 +388,10 @@ int ct_fit_ttl(ct_ctx* c, const ct_samples* sm, const ct_cost_params* cp,
     if (c->fit_occ < 1) return fail(CT_ECUDA, "fit_hist kernel cannot be resident");
     // warp variants: every warp takes its own chunks; CTA variant: one chunk per CTA
     const int wpb = ct::fit_hist_cta_chunks() ? 1 : ct::fit_hist_threads() / 32;
-    const int grid = (int)std::min<int64_t>((int64_t)c->sm_count * c->fit_occ,
-                                            (fa.n_chunks + wpb - 1) / wpb);
+    // range variant: >= 2^15 samples per CTA (each CTA zeroes and flushes a full histogram)
+    const int64_t items = ranges ? (fa.tool_off[F] - fa.tool_off[0] + (1 << 15) - 1) >> 15
+                                 : (fa.n_chunks + wpb - 1) / wpb;
+    const int grid = (int)std::min<int64_t>((int64_t)c->sm_count * c->fit_occ, items);
     if (c->timing) CT_CUDA(cudaEventRecord(c->ev[2], s));
     cudaError_t e = ct::launch_fit_hist(fa, grid, s);
     if (e != cudaSuccess) return cuda_fail(e, "fit_hist launch");

@@ -67,6 +67,7 @@ cudaError_t launch_fit_scan(const ScanArgs& a, cudaStream_t s);
 int fit_hist_threads();
 int fit_hist_repl();  // histogram replicas per warp of the selected variant
 bool fit_hist_cta_chunks();  // work items are CTA-level chunks (CTA-shared histogram)
+bool fit_hist_ranges();      // CTA b takes one contiguous sample range (pieces of <= ch)
 int fit_hist_smem(int K);
 int fit_hist_occupancy(int smem);  // resident CTAs per SM
 

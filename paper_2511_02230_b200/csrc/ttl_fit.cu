@@ -1,13 +1,14 @@
 // ttl_fit.cu — the TTL fit: one HBM pass over duration samples.
 //
-// Kernel 1 (fit_hist): persistent CTAs of 8 warps stream CTA-level chunks of tool-grouped (CSR)
-// int32 samples with 16-B streaming loads (register double buffering, 8 int4 in flight per lane).
+// Kernel 1 (fit_hist): one CTA of 8 warps per resident slot streams one contiguous range of the
+// tool-grouped (CSR) int32 samples with 16-B streaming loads (register double buffering, 8 int4
+// in flight per lane), cut into pieces at tool boundaries.
 // Every sample lands in the CTA's histogram over the TTL grid buckets k = min(ceil(d / step), K)
 // as (count, sum of k step - d) with fire-and-forget 32-bit shared reductions; the histogram has
 // one replica per lane index shared by the CTA's warps, so a warp instruction never conflicts.
 // Each thread keeps the paper-mode statistics (sum t~, sum t~^2) of t~ = min(d, b) in registers
 // (reading R5).  After each chunk the replicas are merged and flushed with
-// integer atomics (order independent, hence deterministic).  Older per-warp variants remain
+// integer atomics (order independent, hence deterministic).  Older chunked variants remain
 // selectable for measurement (CT_FIT_VARIANT).
 // Kernel 2 (fit_scan): one CTA per tool row: block prefix scan of the bucket counts and sums in
 // shared memory, then per turn bucket j n U(k) in 128-bit integers (extension C-4) and a warp
@@ -37,20 +38,23 @@ static const FitVariant kVariants[] = {{16, false, 16}, {16, true, 16}, {8, fals
                                        {32, false, 8},                    // 11: CTA-shared, U 8
                                        {32, false, 8},                    // 12: 11 + 32-bit sums
                                        {32, false, 4},                    // 13: 12 with U 4
-                                       {32, false, 6}};                   // 14: 12 with U 6
-static int g_variant = -1;  // default 12: measured best on B200 (DESIGN.md §8 variant table)
+                                       {32, false, 6},                    // 14: 12 with U 6
+                                       {32, false, 8},                    // 15: 12, CTA ranges
+                                       {32, false, 8}};                   // 16: 11, CTA ranges
+static int g_variant = -1;  // default 15: measured best on B200 (DESIGN.md §8 variant table)
 
 static int variant() {
-  static_assert(sizeof kVariants / sizeof kVariants[0] == 15, "variant table / hist_fn mismatch");
+  static_assert(sizeof kVariants / sizeof kVariants[0] == 17, "variant table / hist_fn mismatch");
   if (g_variant < 0) {
     const char* e = getenv("CT_FIT_VARIANT");
-    int v = e ? atoi(e) : 12;
-    g_variant = (v >= 0 && v < (int)(sizeof kVariants / sizeof kVariants[0])) ? v : 12;
+    int v = e ? atoi(e) : 15;
+    g_variant = (v >= 0 && v < (int)(sizeof kVariants / sizeof kVariants[0])) ? v : 15;
   }
   return g_variant;
 }
 
 static bool cta_variant() { return variant() >= 10; }
+bool fit_hist_ranges() { return variant() >= 15; }
 int fit_hist_threads() { return cta_variant() ? 256 : FIT_THREADS; }
 int fit_hist_repl() { return kVariants[variant()].repl; }
 bool fit_hist_cta_chunks() { return cta_variant(); }
@@ -248,29 +252,29 @@ __device__ __forceinline__ void sample_cta(const Lane& L, uint32_t base, int32_t
   mad_wide(s2, t, t);
 }
 
-template <bool IDENT, int U, bool FAST32>
-__global__ void __launch_bounds__(32 * FW) fit_hist_cta_kernel(FitArgs a) {
-  extern __shared__ __align__(16) uint32_t hsm[];
-  const int K = a.K;
-  const int tid = threadIdx.x, lane = tid & 31;
-  const int words = (K + 1) * 64;
+__device__ __forceinline__ Lane cta_lane(const FitArgs& a, uint32_t* hsm) {
   Lane L;
-  L.rs_base = (uint32_t)__cvta_generic_to_shared(hsm) + 4 * lane + 128;  // remainders
-  L.cnt_base = L.rs_base - 128;                                           // counts
+  L.rs_base = (uint32_t)__cvta_generic_to_shared(hsm) + 4 * (threadIdx.x & 31) + 128;  // remainders
+  L.cnt_base = L.rs_base - 128;                                                        // counts
   L.cnt_inc = 1u;
-  L.K = (uint32_t)K;
+  L.K = (uint32_t)a.K;
   L.step = (uint32_t)a.step;
   L.mhi = (uint32_t)(a.step_magic >> 32);
   L.mlo = (uint32_t)a.step_magic;
   L.xoff = L.step - 1;
   L.b_us = (uint32_t)a.b_us;
-  __shared__ unsigned long long red[FW][3];
+  return L;
+}
 
-  for (int64_t c = blockIdx.x; c < a.n_chunks; c += gridDim.x) {
-    int tool = 0;
-    while (a.chunk_off[tool + 1] <= c) ++tool;
-    const int64_t beg = a.tool_off[tool] + (c - a.chunk_off[tool]) * a.ch;
-    const int64_t end = min(beg + a.ch, a.tool_off[tool + 1]);
+// One CTA work piece: samples [beg, end) of one tool -> zeroed CTA histogram -> flush.
+template <bool IDENT, int U, bool FAST32>
+__device__ __forceinline__ void cta_piece(const FitArgs& a, const Lane& L, uint32_t* hsm,
+                                          unsigned long long (*red)[3], int tool, int64_t beg,
+                                          int64_t end) {
+  const int K = a.K;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int words = (K + 1) * 64;
+  {
     for (int i = tid; i < words; i += 32 * FW) hsm[i] = 0;
     __syncthreads();
     uint64_t s1 = 0, s2 = 0;
@@ -372,6 +376,47 @@ __global__ void __launch_bounds__(32 * FW) fit_hist_cta_kernel(FitArgs a) {
   }
 }
 
+template <bool IDENT, int U, bool FAST32>
+__global__ void __launch_bounds__(32 * FW) fit_hist_cta_kernel(FitArgs a) {
+  extern __shared__ __align__(16) uint32_t hsm[];
+  __shared__ unsigned long long red[FW][3];
+  const Lane L = cta_lane(a, hsm);
+  for (int64_t c = blockIdx.x; c < a.n_chunks; c += gridDim.x) {
+    int tool = 0;
+    while (a.chunk_off[tool + 1] <= c) ++tool;
+    const int64_t beg = a.tool_off[tool] + (c - a.chunk_off[tool]) * a.ch;
+    const int64_t end = min(beg + a.ch, a.tool_off[tool + 1]);
+    cta_piece<IDENT, U, FAST32>(a, L, hsm, red, tool, beg, end);
+  }
+}
+
+// Contiguous-range variant: CTA b streams samples [bnd(b), bnd(b+1)) of the whole CSR array
+// (boundaries 4-aligned, so only tool boundaries have scalar heads/tails), cut into pieces at
+// tool boundaries and every ch samples (the 32-bit bin bound).  A CTA therefore zeroes and
+// flushes its histogram ~once instead of once per 2^17-sample chunk.
+template <bool IDENT, int U, bool FAST32>
+__global__ void __launch_bounds__(32 * FW) fit_hist_seg_kernel(FitArgs a) {
+  extern __shared__ __align__(16) uint32_t hsm[];
+  __shared__ unsigned long long red[FW][3];
+  const Lane L = cta_lane(a, hsm);
+  const int64_t s0 = a.tool_off[0], s1 = a.tool_off[a.F];
+  const int64_t per = (s1 - s0 + gridDim.x - 1) / gridDim.x;
+  auto bnd = [&](int64_t b) -> int64_t {
+    if (b == 0) return s0;
+    if (b >= (int64_t)gridDim.x) return s1;
+    return min(s1, max(s0, (s0 + b * per) & ~(int64_t)3));
+  };
+  int64_t lo = bnd(blockIdx.x);
+  const int64_t hi = bnd((int64_t)blockIdx.x + 1);
+  int tool = 0;
+  while (lo < hi) {
+    while (a.tool_off[tool + 1] <= lo) ++tool;
+    const int64_t end = min(min(hi, a.tool_off[tool + 1]), lo + a.ch);
+    cta_piece<IDENT, U, FAST32>(a, L, hsm, red, tool, lo, end);
+    lo = end;
+  }
+}
+
 template <bool IDENT>
 static void* hist_fn(int v) {
   switch (v) {
@@ -389,7 +434,9 @@ static void* hist_fn(int v) {
     case 11: return (void*)fit_hist_cta_kernel<IDENT, 8, false>;
     case 12: return (void*)fit_hist_cta_kernel<IDENT, 8, true>;  // b < 2^26 fast sums
     case 13: return (void*)fit_hist_cta_kernel<IDENT, 4, true>;
-    default: return (void*)fit_hist_cta_kernel<IDENT, 6, true>;
+    case 14: return (void*)fit_hist_cta_kernel<IDENT, 6, true>;
+    case 15: return (void*)fit_hist_seg_kernel<IDENT, 8, true>;   // contiguous CTA ranges
+    default: return (void*)fit_hist_seg_kernel<IDENT, 8, false>;
   }
 }
 
@@ -494,7 +541,10 @@ __global__ void __launch_bounds__(SCAN_THREADS) fit_scan_kernel(ScanArgs a) {
 cudaError_t launch_fit_hist(const FitArgs& a, int grid, cudaStream_t s) {
   const int smem = fit_hist_smem(a.K);
   int v = variant();
-  if (v >= 12 && a.b_us >= (1ll << 26)) v = 11;  // 32-bit partial sums need b < 2^26 µs
+  if (a.b_us >= (1ll << 26)) {  // 32-bit partial sums need b < 2^26 µs
+    if (v == 12 || v == 13 || v == 14) v = 11;
+    if (v == 15) v = 16;
+  }
   void* k = a.step == 1 ? hist_fn<true>(v) : hist_fn<false>(v);
   void* args[] = {(void*)&a};
   return cudaLaunchKernel(k, dim3(grid), dim3(fit_hist_threads()), args, smem, s);
@@ -502,7 +552,7 @@ cudaError_t launch_fit_hist(const FitArgs& a, int grid, cudaStream_t s) {
 
 int fit_hist_occupancy(int smem) {
   for (void* k : {hist_fn<true>(variant()), hist_fn<false>(variant()), hist_fn<true>(11),
-                  hist_fn<false>(11)})
+                  hist_fn<false>(11), hist_fn<true>(16), hist_fn<false>(16)})
     if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
       return 0;
   int nb = 0;

@@ -1,4 +1,4 @@
-for v in 12 13 14 12 13 14; do echo "variant $v"; CT_FIT_VARIANT=$v python - <<'PY'
+for v in ${VARIANTS:-12 15 12 15}; do echo "variant $v"; CT_FIT_VARIANT=$v python - <<'PY'
 import torch, numpy as np, sys
 sys.path.insert(0, '.')
 import paper_2511_02230_b200 as ct
@@ -12,4 +12,4 @@ for i in range(12):
 m = np.median(ms[2:]); print("fit_hist %.1f us %.0f GB/s (min %.1f)" % (m*1e3, 4*2**28/(m*1e-3)/1e9, min(ms)*1e3))
 PY
 done
-CT_FIT_VARIANT=12 python -m pytest tests/test_gpu_parity.py tests/test_gpu_fullsize.py -q -x -k fit 2>&1 | tail -1
+CT_FIT_VARIANT=${PVAR:-12} python -m pytest tests/test_gpu_parity.py tests/test_gpu_fullsize.py -q -x -k fit 2>&1 | tail -1
