@@ -40,10 +40,13 @@ class Engine:
     max_batch: int = 256
     dram_blocks: int = 0
     max_iters: int = (1 << 62)
+    kv_growth: int = 0      # 0: reserve the request at admission (R12); 1: vLLM growth (R27-R30)
+    prefill_chunk: int = 0  # reserved (chunked prefill), must be 0
 
     def as_array(self) -> np.ndarray:
         return np.array([self.c0_ps, self.c_pf_ps, self.c_kv_ps, self.c_h2d_ps, self.bs,
-                         self.max_batch, self.dram_blocks, self.max_iters], dtype=np.int64)
+                         self.max_batch, self.dram_blocks, self.max_iters, self.kv_growth,
+                         self.prefill_chunk], dtype=np.int64)
 
 
 ENGINE_8B = Engine(c0_ps=2_000_000_000, c_pf_ps=13_400_000, c_kv_ps=16, c_h2d_ps=40_000_000)

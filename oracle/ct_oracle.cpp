@@ -7,7 +7,8 @@
 //
 // Parameter vectors (int64):
 //   est  = {L_q, b_us, T_default_us, N, a_num, a_den, ttl_max_us, 0}
-//   eng  = {c0_ps, c_pf_ps, c_kv_ps, c_h2d_ps, bs, max_batch, dram_blocks, max_iters}
+//   eng  = {c0_ps, c_pf_ps, c_kv_ps, c_h2d_ps, bs, max_batch, dram_blocks, max_iters,
+//           kv_growth, prefill_chunk}
 //   pol  = {priority, pause, dram, flags, t_pin_us, t_thresh_us, 0, 0}
 //   cost = {c_pf_ps, c_pin_ps, bs, a_num, a_den, grid_step_us, K, J}
 // Summary (int64[16]) per replica:
@@ -204,7 +205,9 @@ struct Prog {
   int64_t expiry = 0, req_arr = 0, t_ret = 0, load_done = 0, emitted = 0;
   int64_t arrival = 0, completion = -1;
   int64_t service = 0;  // attained engine time (Autellix PLAS)
+  int64_t bubble = 0;   // this program's waiting time before admissions (NEXT-3 series)
   bool first = false;
+  bool preempted = false;  // recompute-preempted, back in Q (NEXT-2, R28)
 };
 
 struct Row { int64_t n = 0, s1 = 0; u128 s2 = 0; };
@@ -242,6 +245,7 @@ struct Sim {
   int64_t arrival_time(int i) const { return (int64_t)(((i128)prog_arr_q(i) * gap) >> 20); }
 
   bool dram_on() const { return pol[2] != 0 && eng[6] > 0; }
+  bool growth() const { return eng[8] != 0; }  // NEXT-2 block-by-block KV growth (R27)
   bool eager() const { return (pol[3] & FLAG_STEP_EXPIRY) == 0; }
 
   // evict(v): free GPU blocks; DRAM write-through when the tier is on (R18).
@@ -306,18 +310,62 @@ struct Sim {
   }
 
   int head() {  // argmax priority over Q
+    // preempted requests first (reading R29); they exist only with KV growth
+    bool any_pre = false;
+    for (int i = 0; i < P; ++i) any_pre |= p[i].st == QUEUED && p[i].preempted;
+    auto cand = [&](int i) { return p[i].st == QUEUED && (!any_pre || p[i].preempted); };
     int best = -1;
     if (pol[0] == PRIO_PROG_FCFS) {
-      for (int i = 0; i < P; ++i) if (p[i].st == QUEUED && p[i].pinned) return i;
-      for (int i = 0; i < P; ++i) if (p[i].st == QUEUED) return i;
+      if (!any_pre)
+        for (int i = 0; i < P; ++i) if (cand(i) && p[i].pinned) return i;
+      for (int i = 0; i < P; ++i) if (cand(i)) return i;
     } else if (pol[0] == PRIO_REQ_FCFS) {
       for (int i = 0; i < P; ++i)
-        if (p[i].st == QUEUED && (best < 0 || p[i].req_arr < p[best].req_arr)) best = i;
+        if (cand(i) && (best < 0 || p[i].req_arr < p[best].req_arr)) best = i;
     } else {  // PLAS: least attained service first, ties by program arrival
       for (int i = 0; i < P; ++i)
-        if (p[i].st == QUEUED && (best < 0 || p[i].service < p[best].service)) best = i;
+        if (cand(i) && (best < 0 || p[i].service < p[best].service)) best = i;
     }
     return best;
+  }
+
+  // Priority among RUNNING requests (reading R28): true iff a ranks above b.
+  bool run_before(int a, int b) const {
+    if (pol[0] == PRIO_REQ_FCFS && p[a].req_arr != p[b].req_arr) return p[a].req_arr < p[b].req_arr;
+    if (pol[0] == PRIO_PLAS && p[a].service != p[b].service) return p[a].service < p[b].service;
+    return a < b;
+  }
+
+  // vLLM recompute preemption (R28): drop the GPU KV, back to Q marked preempted.
+  void preempt(int v) {
+    free_blk += p[v].gblk;
+    p[v].gblk = 0;
+    p[v].st = QUEUED;
+    p[v].preempted = true;
+    p[v].req_arr = now;
+  }
+
+  // Growth step (R27/R28): every running request needs a slot for its next token, i.e.
+  // ceil((ctx + new + emitted + 1) / bs) blocks; served in priority order; when no block is
+  // free the lowest-priority running request (possibly itself) is preempted.
+  void grow_running() {
+    const int64_t bs = eng[4];
+    std::vector<int> order;
+    for (int i = 0; i < P; ++i) if (p[i].st == RUNNING) order.push_back(i);
+    std::sort(order.begin(), order.end(), [&](int a, int b) { return run_before(a, b); });
+    for (int i : order) {
+      if (p[i].st != RUNNING) continue;  // preempted earlier in this pass
+      const int32_t* tr = turn_rec(i, p[i].turn);
+      const int64_t need = ceil_div(p[i].ctx + tr[0] + p[i].emitted + 1, bs) - p[i].gblk;
+      while (need > free_blk) {
+        int v = -1;
+        for (int j = 0; j < P; ++j)
+          if (p[j].st == RUNNING && (v < 0 || run_before(v, j))) v = j;
+        preempt(v);
+        if (v == i) break;
+      }
+      if (p[i].st == RUNNING && need > 0) { free_blk -= need; p[i].gblk += need; }
+    }
   }
 
   bool schedule() {  // returns false when the replica stops (unschedulable / budget)
@@ -327,9 +375,11 @@ struct Sim {
       if (p[i].pinned && p[i].st != QUEUED && now > p[i].expiry) {
         evict(i); p[i].pinned = false; expiries++;
       }
+    // (a2) KV growth of the running requests (NEXT-2, R27/R28)
+    if (growth()) grow_running();
     // (b) loaded requests join the batch
     for (int i = 0; i < P; ++i)
-      if (p[i].st == READY) { p[i].st = RUNNING; p[i].first = true; p[i].emitted = 0; }
+      if (p[i].st == READY) { p[i].st = RUNNING; p[i].first = true; }
     // (c) admit loop (victims PAPER.md:645-655)
     int admitted = 0;
     for (;;) {
@@ -341,7 +391,9 @@ struct Sim {
       if (nq == 0 || nb >= eng[5]) break;
       int h = head();
       const int32_t* tr = turn_rec(h, p[h].turn);
-      int64_t need = ceil_div(p[h].ctx + tr[0] + tr[1], bs) - p[h].gblk;
+      // R12: reserve the whole request; R27 (growth): up to the slot of the next token
+      const int64_t upto = growth() ? p[h].emitted + 1 : tr[1];
+      int64_t need = ceil_div(p[h].ctx + tr[0] + upto, bs) - p[h].gblk;
       if (need > free_blk && (admitted == 0 || (pol[3] & FLAG_VICTIMS_ANY))) {
         while (need > free_blk) {
           int v = -1;
@@ -354,6 +406,7 @@ struct Sim {
       free_blk -= need;
       p[h].gblk += need;
       bubble += now - p[h].req_arr;
+      p[h].bubble += now - p[h].req_arr;
       int64_t cached;
       bool loading = false;
       if (p[h].pinned) {
@@ -365,13 +418,17 @@ struct Sim {
         chan_free = p[h].load_done;
         reloads++;
       } else {
-        cached = 0; recompute += p[h].ctx;
+        cached = 0;
       }
-      int64_t uncached = p[h].ctx + tr[0] - cached;
+      // recomputed: the context without a cached copy, plus (R30) the prompt and emitted
+      // tokens a preemption dropped
+      recompute += p[h].ctx - cached + (p[h].preempted ? tr[0] + p[h].emitted : 0);
+      p[h].preempted = false;
+      int64_t uncached = p[h].ctx + tr[0] + p[h].emitted - cached;
       prefill += uncached;
       unc[h] = uncached;
       if (loading) p[h].st = LOADING;
-      else { p[h].st = RUNNING; p[h].first = true; p[h].emitted = 0; }
+      else { p[h].st = RUNNING; p[h].first = true; }
       admitted++;
     }
     // (d) unschedulable: nothing can ever free memory for the head
@@ -427,7 +484,7 @@ struct Sim {
     return true;
   }
 
-  void run(int64_t* summary, int64_t* jct) {
+  void run(int64_t* summary, int64_t* jct, int64_t* bub) {
     p.assign(P, Prog());
     unc.assign(P, 0);
     tool.assign(F, Row());
@@ -465,6 +522,7 @@ struct Sim {
           p[i].turn += 1;
           p[i].st = QUEUED;
           p[i].req_arr = now;
+          p[i].emitted = 0;
         }
       // LoadDone
       for (int i = 0; i < P; ++i)
@@ -495,6 +553,7 @@ struct Sim {
     if (status != ST_OK) {
       summary[0] = (int64_t)(uint32_t)status;
       if (jct) for (int i = 0; i < P; ++i) jct[i] = -1;
+      if (bub) for (int i = 0; i < P; ++i) bub[i] = -1;
       return;
     }
     std::vector<int64_t> js(P);
@@ -506,6 +565,7 @@ struct Sim {
       min_arr = std::min(min_arr, p[i].arrival);
       max_comp = std::max(max_comp, p[i].completion);
       if (jct) jct[i] = js[i];
+      if (bub) bub[i] = p[i].bubble;
     }
     std::vector<int64_t> s = js;
     std::sort(s.begin(), s.end());
@@ -535,12 +595,13 @@ int or_simulate(const void* progs, const int32_t* turns, int64_t n_turns, int S,
                 const int64_t* gap_us, int n_rate, const int64_t* kv_blocks, int n_kv,
                 const int64_t* policies, int n_pol, const int64_t* est, const int64_t* eng,
                 const int64_t* fitted, int J, int64_t r_begin, int64_t r_end, int n_threads,
-                int64_t* summary, int64_t* jct) {
+                int64_t* summary, int64_t* jct, int64_t* bubble) {
   (void)n_turns;
   if (P < 1 || S < 1 || n_rate < 1 || n_kv < 1 || n_pol < 1 || r_begin < 0 || r_end < r_begin)
     return -1;
   if (r_end > (int64_t)S * n_rate * n_kv * n_pol) return -1;
   if (eng[0] < 1 || eng[4] < 1 || eng[5] < 1) return -1;
+  if (eng[8] < 0 || eng[8] > 1 || eng[9] != 0) return -1;
   auto one = [&](int64_t r) {
     int64_t pol_i = r % n_pol, kv_i = (r / n_pol) % n_kv, rate_i = (r / ((int64_t)n_pol * n_kv)) % n_rate;
     int64_t seed = r / ((int64_t)n_pol * n_kv * n_rate);
@@ -553,7 +614,8 @@ int or_simulate(const void* progs, const int32_t* turns, int64_t n_turns, int S,
     sim.est = est; sim.eng = eng; sim.fitted = fitted;
     sim.seed = (int)seed;
     int64_t k = r - r_begin;
-    sim.run(summary + 16 * k, jct ? jct + (int64_t)P * k : nullptr);
+    sim.run(summary + 16 * k, jct ? jct + (int64_t)P * k : nullptr,
+            bubble ? bubble + (int64_t)P * k : nullptr);
   };
   int64_t n = r_end - r_begin;
   if (n_threads <= 1 || n < 2) {

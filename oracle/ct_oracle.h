@@ -53,7 +53,8 @@ int or_fit(const int32_t* dur, const int64_t* tool_off, int F,
 
 /* Replay replicas [r_begin, r_end) of a sweep.
  * progs: 16-B records {i64 arr_q, i32 turn0, i32 nturns} [S*P]; turns: i32[T][4].
- * summary: int64[16] per replica; jct: int64[P] per replica (or NULL).
+ * summary: int64[16] per replica; jct, bubble: int64[P] per replica (or NULL); bubble is
+ * each program's total waiting time before admissions (NEXT-3 per-program bubble series).
  * Returns 0, or a negative value on invalid input. */
 int or_simulate(const void* progs, const int32_t* turns, int64_t n_turns,
                 int S, int P, int F,
@@ -61,7 +62,7 @@ int or_simulate(const void* progs, const int32_t* turns, int64_t n_turns,
                 const int64_t* policies, int n_pol, const int64_t* est,
                 const int64_t* eng, const int64_t* fitted, int J,
                 int64_t r_begin, int64_t r_end, int n_threads,
-                int64_t* summary, int64_t* jct);
+                int64_t* summary, int64_t* jct, int64_t* bubble);
 
 /* Per sweep cell sums over seeds (cells = rate x kv x policy). out: int64[8] per cell. */
 int or_jct_stats(const int64_t* summary, int64_t n_replicas, int n_cells, int64_t* out);

@@ -54,7 +54,7 @@ def lib():
         _lib.or_fit.argtypes = [p, p, C.c_int, p, p, p, p, p, p, p, p]
         _lib.or_simulate.restype = C.c_int
         _lib.or_simulate.argtypes = [p, p, i64, C.c_int, C.c_int, C.c_int, p, C.c_int, p, C.c_int,
-                                     p, C.c_int, p, p, p, C.c_int, i64, i64, C.c_int, p, p]
+                                     p, C.c_int, p, p, p, C.c_int, i64, i64, C.c_int, p, p, p]
         _lib.or_jct_stats.restype = C.c_int
         _lib.or_jct_stats.argtypes = [p, i64, C.c_int, p]
     return _lib
@@ -132,10 +132,11 @@ def fit(dur: np.ndarray, tool_off: np.ndarray, cost, ctx_j, w_j, est, avg=(0, 0)
 
 
 def simulate(trace, sweep, engine, r_begin: int = 0, r_end: int | None = None,
-             n_threads: int = 1, want_jct: bool = True):
+             n_threads: int = 1, want_jct: bool = True, want_bubble: bool = False):
     """Replay replicas [r_begin, r_end) of `sweep` over `trace` (ctgen types).
 
-    Returns (summary int64[R,16], jct int64[R,P] or None).
+    Returns (summary int64[R,16], jct int64[R,P] or None), plus bubble int64[R,P] (each
+    program's total waiting time) as a third element when want_bubble.
     """
     if r_end is None:
         r_end = sweep.n_replicas
@@ -155,14 +156,16 @@ def simulate(trace, sweep, engine, r_begin: int = 0, r_end: int | None = None,
         J = 1
     summ = np.zeros((R, 16), np.int64)
     jct = np.zeros((R, trace.n_programs), np.int64) if want_jct else None
+    bub = np.zeros((R, trace.n_programs), np.int64) if want_bubble else None
     rc = lib().or_simulate(_ptr(progs), _ptr(turns), turns.shape[0], trace.n_seeds,
                            trace.n_programs, trace.n_tools, _ptr(gap), len(gap), _ptr(kv), len(kv),
                            _ptr(pol), len(sweep.policies), _ptr(est), _ptr(eng), _ptr(fitted), J,
                            r_begin, r_end, n_threads, _ptr(summ),
-                           _ptr(jct) if jct is not None else None)
+                           _ptr(jct) if jct is not None else None,
+                           _ptr(bub) if bub is not None else None)
     if rc != 0:
         raise ValueError("or_simulate rejected its input (%d)" % rc)
-    return summ, jct
+    return (summ, jct, bub) if want_bubble else (summ, jct)
 
 
 def jct_stats(summary: np.ndarray, n_cells: int) -> np.ndarray:

@@ -12,6 +12,11 @@ Semantics followed (C-5/C-6, Alg. 1 and §5.3):
   * requests admitted at iteration boundaries; admission reserves all blocks
   * program-level FCFS (pinned first) or request FCFS priority; HOL break
   * victims: pinned programs with the largest index, only when nothing was admitted
+  * engine kv_growth = 1 (NEXT-2, R27-R30): a request holds blocks for its tokens
+    so far plus the one it is about to produce; before every scheduling pass each running
+    request tops up, best-ranked first, and when the pool is dry the worst-ranked running
+    request is thrown back to the queue (recompute), keeping its output so far; thrown-back
+    requests are served first
 """
 from __future__ import annotations
 
@@ -27,7 +32,8 @@ def simulate(trace, gap_us, kv, pol, est, eng, fitted=None, horizon=200000):
     P = trace.n_programs
     progs = trace.programs
     T = trace.turns
-    c0, cpf, ckv, ch2d, bs, maxb, dram_cap, max_it = [int(x) for x in eng]
+    c0, cpf, ckv, ch2d, bs, maxb, dram_cap, max_it, growth, chunk = [int(x) for x in eng]
+    assert chunk == 0
     prio, pause, dram, flags, t_pin, t_thresh = [int(x) for x in pol[:6]]
     dram_on = dram != 0 and dram_cap > 0
     victims_any = bool(flags & 1)
@@ -42,7 +48,8 @@ def simulate(trace, gap_us, kv, pol, est, eng, fitted=None, horizon=200000):
 
     # per-program state as plain dicts
     S = [dict(where="out", turn=0, ctx=0, blk=0, dblk=0, pin=None, waited_since=None,
-              tool_back=None, load_at=None, left=0, fresh=0, done_at=None, served=0)
+              tool_back=None, load_at=None, left=0, fresh=0, done_at=None, served=0, out=0,
+              thrown=False, waited=0)
          for _ in range(P)]
     free = kv
     dfree = dram_cap if dram_on else 0
@@ -50,7 +57,8 @@ def simulate(trace, gap_us, kv, pol, est, eng, fitted=None, horizon=200000):
     stats = {"g": [0, 0, 0]}
     n_done = 0
     turns_done = 0
-    cnt = dict(iters=0, busy=0, bubble=0, prefill=0, recompute=0, hits=0, exp=0, vict=0, reload=0)
+    cnt = dict(iters=0, busy=0, bubble=0, prefill=0, recompute=0, hits=0, exp=0, vict=0, reload=0,
+               thrown=0)
     engine_until = None  # end time of the iteration in flight
     batch = []
 
@@ -113,6 +121,7 @@ def simulate(trace, gap_us, kv, pol, est, eng, fitted=None, horizon=200000):
                 s["turn"] += 1
                 s["where"] = "queue"
                 s["waited_since"] = now
+                s["out"] = 0
                 fired = True
         # 3) KV loads complete
         for i in range(P):
@@ -131,6 +140,7 @@ def simulate(trace, gap_us, kv, pol, est, eng, fitted=None, horizon=200000):
             for i in sorted(batch):
                 s = S[i]
                 s["left"] -= 1
+                s["out"] += 1
                 if s["left"] == 0:
                     new, dec, f, d = rec(i, s["turn"])
                     s["ctx"] += new + dec
@@ -154,6 +164,31 @@ def simulate(trace, gap_us, kv, pol, est, eng, fitted=None, horizon=200000):
                         s["where"] = "tool"
         # 6) scheduling pass at an event instant with no iteration in flight (R3)
         if engine_until is None and fired:
+            def rank(i):  # smaller ranks first
+                if prio == 0:
+                    return (i,)
+                if prio == 1:
+                    return (S[i]["waited_since"], i)
+                return (S[i]["served"], i)
+
+            if growth:
+                for i in sorted(batch, key=rank):
+                    if i not in batch:
+                        continue
+                    s = S[i]
+                    new = rec(i, s["turn"])[0]
+                    want = -(-(s["ctx"] + new + s["out"] + 1) // bs)
+                    while want - s["blk"] > free:
+                        v = max(batch, key=rank)
+                        free += S[v]["blk"]
+                        S[v].update(blk=0, where="queue", thrown=True, waited_since=now)
+                        batch.remove(v)
+                        cnt["thrown"] += 1
+                        if v == i:
+                            break
+                    if i in batch and want > s["blk"]:
+                        free -= want - s["blk"]
+                        s["blk"] = want
             for i in range(P):
                 if S[i]["where"] == "loaded":
                     S[i]["where"] = "run"
@@ -164,6 +199,9 @@ def simulate(trace, gap_us, kv, pol, est, eng, fitted=None, horizon=200000):
                 busy = len(batch) + sum(1 for i in range(P) if S[i]["where"] == "loading")
                 if not waiting or busy >= maxb:
                     break
+                thrown = [i for i in waiting if S[i]["thrown"]]
+                if thrown:
+                    waiting = thrown
                 if prio == 0:
                     pinned_w = [i for i in waiting if S[i]["pin"] is not None]
                     h = min(pinned_w) if pinned_w else min(waiting)
@@ -173,7 +211,7 @@ def simulate(trace, gap_us, kv, pol, est, eng, fitted=None, horizon=200000):
                     h = min(waiting, key=lambda i: (S[i]["served"], i))
                 s = S[h]
                 new, dec, _, _ = rec(h, s["turn"])
-                total = -(-(s["ctx"] + new + dec) // bs)
+                total = -(-(s["ctx"] + new + (s["out"] + 1 if growth else dec)) // bs)
                 need = total - s["blk"]
                 if need > free and (admitted == 0 or victims_any):
                     for v in sorted((i for i in range(P) if S[i]["pin"] is not None and i != h),
@@ -188,6 +226,7 @@ def simulate(trace, gap_us, kv, pol, est, eng, fitted=None, horizon=200000):
                 free -= need
                 s["blk"] = total
                 cnt["bubble"] += now - s["waited_since"]
+                s["waited"] += now - s["waited_since"]
                 if s["pin"] is not None:
                     cached = s["ctx"]
                     s["pin"] = None
@@ -202,11 +241,12 @@ def simulate(trace, gap_us, kv, pol, est, eng, fitted=None, horizon=200000):
                     s["where"] = "loading"
                 else:
                     cached = 0
-                    cnt["recompute"] += s["ctx"]
                     s["where"] = "run"
-                s["fresh"] = s["ctx"] + new - cached
+                cnt["recompute"] += s["ctx"] - cached + (new + s["out"] if s["thrown"] else 0)
+                s["thrown"] = False
+                s["fresh"] = s["ctx"] + new + s["out"] - cached
                 cnt["prefill"] += s["fresh"]
-                s["left"] = dec
+                s["left"] = dec - s["out"]
                 if s["where"] == "run":
                     batch.append(h)
                 admitted += 1
@@ -234,4 +274,5 @@ def simulate(trace, gap_us, kv, pol, est, eng, fitted=None, horizon=200000):
         return "horizon", None, None
     jct = [S[i]["done_at"] - arr[i] for i in range(P)]
     makespan = max(S[i]["done_at"] for i in range(P)) - min(arr)
-    return "ok", jct, dict(cnt, makespan=makespan, turns=turns_done)
+    return "ok", jct, dict(cnt, makespan=makespan, turns=turns_done,
+                           waited=[S[i]["waited"] for i in range(P)])
