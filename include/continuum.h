@@ -117,6 +117,11 @@ typedef struct {            /* linear engine cost model (R16) */
   int64_t max_batch;        /* running + loading requests, >= 1 */
   int64_t dram_blocks;      /* DRAM tier capacity in blocks, 0 = no tier */
   int64_t max_iters;        /* engine-iteration budget per replica (CT_R_EVENT_BUDGET) */
+  int64_t kv_growth;        /* 0: admission reserves the whole request, ceil((ctx+new+decode)/bs)
+                               blocks (R12); 1: vLLM-style block-by-block growth with
+                               recompute preemption and the preempted rank of PAPER.md:541
+                               (NEXT-2, R27-R30) */
+  int64_t prefill_chunk;    /* reserved for chunked prefill; must be 0 */
 } ct_engine_params;
 
 typedef struct {            /* 48 B */
@@ -223,6 +228,21 @@ int ct_fit_ttl(ct_ctx* ctx, const ct_samples* samples, const ct_cost_params* cos
 int ct_simulate_batch(ct_ctx* ctx, const ct_trace_set* traces, const ct_sweep* sweep,
                       const ct_engine_params* eng, int64_t replica_begin, int64_t replica_end,
                       ct_replica_summary* out, int64_t* jct_us, void* stream);
+
+/* Optional per-program outputs of a replay (all [dev], n = replica_end - replica_begin).
+ * summary is required; jct_us and bubble_us may be NULL.  bubble_us[i*P + p] is program p's
+ * total time waiting in Q before its admissions (the per-program bubble series of PAPER.md
+ * Fig. waiting_time_analysis_comparison, NEXT-3); -1 for replicas whose status is not OK. */
+typedef struct {
+  ct_replica_summary* summary;
+  int64_t* jct_us;
+  int64_t* bubble_us;
+} ct_replay_outputs;
+
+/* ct_simulate_batch with the optional per-program bubble output.  Same errors. */
+int ct_simulate_batch_ex(ct_ctx* ctx, const ct_trace_set* traces, const ct_sweep* sweep,
+                         const ct_engine_params* eng, int64_t replica_begin, int64_t replica_end,
+                         const ct_replay_outputs* out, void* stream);
 
 /* Same as ct_simulate_batch but with HOST buffers: programs/turns in traces->programs/turns are
  * host pointers, out/jct_us are host pointers.  Copies in, runs, copies out and synchronises the

@@ -18,8 +18,12 @@ MAX_J = 64
 
 # every symbol include/continuum.h declares (checked by tests/test_abi.py)
 EXPORTS = ["ct_version", "ct_last_error", "ct_ctx_create", "ct_ctx_destroy", "ct_fit_ttl",
-           "ct_simulate_batch", "ct_simulate_batch_host", "ct_jct_stats", "ct_last_launch",
-           "ct_ctx_set_timing"]
+           "ct_simulate_batch", "ct_simulate_batch_ex", "ct_simulate_batch_host", "ct_jct_stats",
+           "ct_last_launch", "ct_ctx_set_timing"]
+
+
+class ReplayOutputs(C.Structure):
+    _fields_ = [("summary", vp), ("jct_us", vp), ("bubble_us", vp)]
 
 
 class TraceSet(C.Structure):
@@ -34,7 +38,8 @@ class EstimatorParams(C.Structure):
 
 class EngineParams(C.Structure):
     _fields_ = [("c0_ps", i64), ("c_pf_ps", i64), ("c_kv_ps", i64), ("c_h2d_ps", i64), ("bs", i64),
-                ("max_batch", i64), ("dram_blocks", i64), ("max_iters", i64)]
+                ("max_batch", i64), ("dram_blocks", i64), ("max_iters", i64), ("kv_growth", i64),
+                ("prefill_chunk", i64)]
 
 
 class Policy(C.Structure):
@@ -68,7 +73,7 @@ class LaunchInfo(C.Structure):
                 ("fit_hist_ms", C.c_float)]
 
 
-assert C.sizeof(Policy) == 48 and C.sizeof(EngineParams) == 64 and C.sizeof(EstimatorParams) == 64
+assert C.sizeof(Policy) == 48 and C.sizeof(EngineParams) == 80 and C.sizeof(EstimatorParams) == 64
 
 _lib = None
 
@@ -88,13 +93,16 @@ def lib() -> C.CDLL:
                                  C.POINTER(EstimatorParams), C.POINTER(TtlTable), vp]
         L.ct_simulate_batch.argtypes = [vp, C.POINTER(TraceSet), C.POINTER(Sweep),
                                         C.POINTER(EngineParams), i64, i64, vp, vp, vp]
+        L.ct_simulate_batch_ex.argtypes = [vp, C.POINTER(TraceSet), C.POINTER(Sweep),
+                                           C.POINTER(EngineParams), i64, i64,
+                                           C.POINTER(ReplayOutputs), vp]
         L.ct_simulate_batch_host.argtypes = [vp, C.POINTER(TraceSet), C.POINTER(Sweep),
                                              C.POINTER(EngineParams), i64, i64, vp, vp, vp]
         L.ct_jct_stats.argtypes = [vp, vp, i64, i32, vp, vp]
         L.ct_last_launch.argtypes = [vp, C.POINTER(LaunchInfo)]
         L.ct_ctx_set_timing.argtypes = [vp, C.c_int]
         for f in ("ct_ctx_create", "ct_ctx_destroy", "ct_fit_ttl", "ct_simulate_batch",
-                  "ct_simulate_batch_host", "ct_jct_stats", "ct_last_launch", "ct_ctx_set_timing"):
+                  "ct_simulate_batch_ex", "ct_simulate_batch_host", "ct_jct_stats", "ct_last_launch", "ct_ctx_set_timing"):
             getattr(L, f).restype = C.c_int
         _lib = L
     return _lib

@@ -120,10 +120,13 @@ def _fitted_tensor(sweep, device):
 # ---- the three calls ----------------------------------------------------------------------
 def ct_simulate_batch(ctx: Context, trace: DeviceTrace, sweep, engine, replica_begin: int = 0,
                       replica_end: int | None = None, out: torch.Tensor | None = None,
-                      jct: torch.Tensor | bool | None = None, stream=None):
+                      jct: torch.Tensor | bool | None = None, stream=None,
+                      bubble: torch.Tensor | bool | None = None):
     """Replay replicas [replica_begin, replica_end) on the GPU.
 
-    Returns (summary int64[R, 16] device tensor, jct int64[R, P] device tensor or None).
+    Returns (summary int64[R, 16] device tensor, jct int64[R, P] device tensor or None), plus
+    the per-program bubble int64[R, P] as a third element when `bubble` is given
+    (ct_simulate_batch_ex).
     """
     if replica_end is None:
         replica_end = sweep.n_replicas
@@ -138,12 +141,22 @@ def ct_simulate_batch(ctx: Context, trace: DeviceTrace, sweep, engine, replica_b
     sw = _SweepStruct(sweep, _fitted_tensor(sweep, dev))
     ts = trace.struct()
     eng = engine_params(engine)
-    rc = L.lib().ct_simulate_batch(ctx.handle, C.byref(ts), C.byref(sw.s), C.byref(eng),
-                                   int(replica_begin), int(replica_end), out.data_ptr(),
-                                   jct.data_ptr() if jct is not None else None,
-                                   _stream_ptr(stream))
-    L.check(rc, "ct_simulate_batch")
-    return out, jct
+    if bubble is None or bubble is False:
+        rc = L.lib().ct_simulate_batch(ctx.handle, C.byref(ts), C.byref(sw.s), C.byref(eng),
+                                       int(replica_begin), int(replica_end), out.data_ptr(),
+                                       jct.data_ptr() if jct is not None else None,
+                                       _stream_ptr(stream))
+        L.check(rc, "ct_simulate_batch")
+        return out, jct
+    if bubble is True:
+        bubble = torch.empty((max(R, 0), trace.n_programs), dtype=torch.int64, device=dev)
+    o = L.ReplayOutputs(out.data_ptr(), jct.data_ptr() if jct is not None else None,
+                        bubble.data_ptr())
+    rc = L.lib().ct_simulate_batch_ex(ctx.handle, C.byref(ts), C.byref(sw.s), C.byref(eng),
+                                      int(replica_begin), int(replica_end), C.byref(o),
+                                      _stream_ptr(stream))
+    L.check(rc, "ct_simulate_batch_ex")
+    return out, jct, bubble
 
 
 def ct_simulate_batch_host(ctx: Context, trace, sweep, engine, replica_begin: int = 0,

@@ -151,7 +151,16 @@ int ct_last_launch(ct_ctx* c, ct_launch_info* info) {
 int ct_simulate_batch(ct_ctx* c, const ct_trace_set* tr, const ct_sweep* sw,
                       const ct_engine_params* eng, int64_t rb, int64_t re,
                       ct_replica_summary* out, int64_t* jct, void* stream) {
-  if (!c || !tr || !sw || !eng) return fail(CT_EINVAL, "NULL argument");
+  const ct_replay_outputs o = {out, jct, nullptr};
+  return ct_simulate_batch_ex(c, tr, sw, eng, rb, re, &o, stream);
+}
+
+int ct_simulate_batch_ex(ct_ctx* c, const ct_trace_set* tr, const ct_sweep* sw,
+                         const ct_engine_params* eng, int64_t rb, int64_t re,
+                         const ct_replay_outputs* outs, void* stream) {
+  if (!c || !tr || !sw || !eng || !outs) return fail(CT_EINVAL, "NULL argument");
+  ct_replica_summary* out = outs->summary;
+  int64_t* jct = outs->jct_us;
   const int P = tr->n_programs, F = tr->n_tools;
   if (P < 1 || P > CT_MAX_PROGRAMS) return fail(CT_EINVAL, "n_programs %d not in [1, %d]", P, CT_MAX_PROGRAMS);
   if (F < 1 || F > CT_MAX_TOOLS) return fail(CT_EINVAL, "n_tools %d not in [1, %d]", F, CT_MAX_TOOLS);
@@ -170,6 +179,8 @@ int ct_simulate_batch(ct_ctx* c, const ct_trace_set* tr, const ct_sweep* sw,
   if (E.c0_ps >= (1ll << 48) || E.c_pf_ps >= (1ll << 40) || E.c_kv_ps >= (1ll << 30) ||
       E.c_h2d_ps >= (1ll << 40) || E.bs >= (1 << 20) || E.dram_blocks >= (1ll << 30))
     return fail(CT_EINVAL, "engine constants exceed the int64 fixed-point bounds");
+  if (E.kv_growth != 0 && E.kv_growth != 1) return fail(CT_EINVAL, "kv_growth must be 0 or 1");
+  if (E.prefill_chunk != 0) return fail(CT_EINVAL, "prefill_chunk is reserved and must be 0");
   bool need_est = false, need_fit = false, need_h2d = false;
   for (int i = 0; i < sw->n_policies; ++i) {
     const ct_policy& p = sw->policies[i];
@@ -228,20 +239,22 @@ int ct_simulate_batch(ct_ctx* c, const ct_trace_set* tr, const ct_sweep* sw,
   a.r_end = re;
   a.out = out;
   a.jct = jct;
+  a.bubble = outs->bubble_us;
   a.counter = c->counter;
   a.bs_magic = E.bs == 1 ? 0
                          : (uint64_t)(((((unsigned __int128)1) << 64) + (uint64_t)E.bs - 1) /
                                       (unsigned __int128)(uint64_t)E.bs);
   const int ns = (P + 31) / 32;  // slots per lane
+  const bool growth = E.kv_growth != 0;
   const int wpb = 4;
-  a.smem_per_warp = ct::replay_smem_per_warp(ns, F);
+  a.smem_per_warp = ct::replay_smem_per_warp(ns, F, growth);
   const int smem = a.smem_per_warp * wpb;
-  int occ = ct::replay_occupancy(ns, wpb, smem);
+  int occ = ct::replay_occupancy(ns, growth, wpb, smem);
   if (occ < 1) return fail(CT_ECUDA, "replay kernel cannot be resident (smem %d)", smem);
   const int64_t need_blocks = (re - rb + wpb - 1) / wpb;
   const int grid = (int)std::min<int64_t>((int64_t)c->sm_count * occ, need_blocks);
   if (c->timing) CT_CUDA(cudaEventRecord(c->ev[0], s));
-  cudaError_t e = ct::launch_replay(a, ns, wpb, grid, s);
+  cudaError_t e = ct::launch_replay(a, ns, growth, wpb, grid, s);
   if (e != cudaSuccess) return cuda_fail(e, "replay launch");
   if (c->timing) CT_CUDA(cudaEventRecord(c->ev[1], s));
   c->replay_timed = c->timing;

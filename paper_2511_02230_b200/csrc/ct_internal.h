@@ -22,18 +22,20 @@ struct ReplayArgs {
   int64_t r_begin, r_end;
   ct_replica_summary* out;
   int64_t* jct;
+  int64_t* bubble;  // per-program waiting time [R * P] or NULL (NEXT-3)
   unsigned long long* counter;
   int smem_per_warp;
   uint64_t bs_magic;  // ceil(2^64 / bs) (0 when bs == 1)
 };
 
 // Bytes of shared memory one replica (one warp) needs for `ns` slots per lane and F tools.
-int replay_smem_per_warp(int ns, int F);
+// KV growth (NEXT-2) always runs the shared-memory path, also for P <= 32.
+int replay_smem_per_warp(int ns, int F, bool growth);
 // Launch the persistent replay kernel; returns the cudaError of the launch.
-cudaError_t launch_replay(const ReplayArgs& a, int ns, int warps_per_block, int grid,
+cudaError_t launch_replay(const ReplayArgs& a, int ns, bool growth, int warps_per_block, int grid,
                           cudaStream_t s);
 // Max resident blocks per SM for the given configuration.
-int replay_occupancy(int ns, int warps_per_block, int smem_per_block);
+int replay_occupancy(int ns, bool growth, int warps_per_block, int smem_per_block);
 
 struct FitArgs {
   const int32_t* dur;

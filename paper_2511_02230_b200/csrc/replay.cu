@@ -19,10 +19,10 @@ namespace ct {
 
 enum : int { S_OUT = 0, S_QUEUED = 1, S_RUN = 2, S_LOAD = 3, S_READY = 4, S_TOOL = 5, S_DONE = 6 };
 
-int replay_smem_per_warp(int ns, int F) {
-  if (ns == 1) return (32 * (F + 1) + 48 + 15) & ~15;  // registers hold the programs; SMEM: estimator + Acc
+int replay_smem_per_warp(int ns, int F, bool growth) {
+  if (ns == 1 && !growth) return (32 * (F + 1) + 48 + 15) & ~15;  // registers hold the programs; SMEM: estimator + Acc
   int pm = 32 * ns;
-  int b = 60 * pm;
+  int b = (growth ? 72 : 60) * pm;  // KV growth adds grow_at (8 B) and emt (4 B) per program
   b = (b + 15) & ~15;
   b += 32 * (F + 1) + 48;  // estimator rows + Acc
   return (b + 15) & ~15;
@@ -101,6 +101,9 @@ __device__ __forceinline__ void replay_one_w32(const ReplayArgs& a, int64_t r, S
     arr = (pr.arr_q * gap) >> 20;
   }
   const int64_t arr0 = shfl64(arr, 0);  // programs arrive in index order: min arrival
+  // per-program bubble series (NEXT-3), accumulated in place by the owner lane (the address
+  // is recomputed at each use: no register is held for it across the event loop)
+  if (a.bubble && live) a.bubble[(r - a.r_begin) * P + lane] = 0;
   int st = S_OUT;
   int64_t tev = arr;          // arrival (OUT), tool return (TOOL), load done (LOAD); INF otherwise
   int64_t texp = CT_INF64;    // expiry + 1 while pinned in a tool call
@@ -369,6 +372,7 @@ __device__ __forceinline__ void replay_one_w32(const ReplayArgs& a, int64_t r, S
       const int64_t u = hctx + hnew - cached;
       if (lane == 0) acc->prefill += u;
       if (lane == h) {
+        if (a.bubble) a.bubble[(r - a.r_begin) * P + lane] += now - req;
         pin = false;
         texp = CT_INF64;
         gblk = ng;
@@ -484,6 +488,7 @@ __device__ __forceinline__ void replay_one_w32(const ReplayArgs& a, int64_t r, S
     a.out[ri] = o;
   }
   if (a.jct && live) a.jct[ri * P + lane] = status == CT_R_OK ? req : -1;
+  if (a.bubble && live && status != CT_R_OK) a.bubble[ri * P + lane] = -1;
   __syncwarp();
 }
 
@@ -495,7 +500,7 @@ __device__ __forceinline__ void replay_one_w32(const ReplayArgs& a, int64_t r, S
 // programs changes.  The next event, the macro-step bound and the first finish are therefore one
 // REDUX minimum each, and only lanes that own a due program scan their slots.  Same semantics as
 // replay_one_w32 (C-5/C-6), checked byte for byte by the tests.
-template <int NS>
+template <int NS, bool GROW>
 __device__ __forceinline__ void replay_one_ns(const ReplayArgs& a, int64_t r, unsigned char* wm,
                                               int lane) {
   constexpr int PM = 32 * NS;
@@ -509,7 +514,12 @@ __device__ __forceinline__ void replay_one_ns(const ReplayArgs& a, int64_t r, un
   int32_t* dblk = gblk + PM;           // DRAM copy blocks
   int32_t* unc = dblk + PM;            // uncached tokens of the current request
   int32_t* turn = unc + PM;            // current turn
-  Stat* stats = (Stat*)(wm + ((60 * PM + 15) & ~15));
+  // KV growth (NEXT-2, R27-R30) only: next iteration boundary at which the running request
+  // needs one more block (INF otherwise) and tokens emitted before a preemption
+  constexpr bool grow_on = GROW;  // == (a.eng.kv_growth != 0), fixed per instantiation
+  int64_t* grow_at = (int64_t*)(turn + PM);
+  int32_t* emt = (int32_t*)(grow_at + PM);
+  Stat* stats = (Stat*)(wm + (((grow_on ? 72 : 60) * PM + 15) & ~15));
   Acc* acc = (Acc*)(stats + a.F + 1);
 
   const int P = a.P, F = a.F;
@@ -550,6 +560,17 @@ __device__ __forceinline__ void replay_one_ns(const ReplayArgs& a, int64_t r, un
     dblk[p] = 0;
     unc[p] = 0;
     turn[p] = 0;
+    if (grow_on) {
+      grow_at[p] = CT_INF64;
+      emt[p] = 0;
+    }
+  }
+  // per-program bubble series (NEXT-3): accumulated in place by the owner lane
+  int64_t* bub = a.bubble ? a.bubble + (r - a.r_begin) * P : nullptr;
+  if (bub) {
+#pragma unroll
+    for (int s = 0; s < NS; ++s)
+      if (lane + 32 * s < P) bub[lane + 32 * s] = 0;
   }
   if (need_stats)
     for (int i = lane; i < 4 * (F + 1); i += 32) ((int64_t*)stats)[i] = 0;
@@ -558,7 +579,9 @@ __device__ __forceinline__ void replay_one_ns(const ReplayArgs& a, int64_t r, un
 
   // per-lane sets over this lane's slots and cached minima
   uint32_t qb = 0, pb = 0, rb = 0, lb = 0, yb = 0, tb = 0;
+  uint32_t xb = 0;  // preempted (KV growth)
   int64_t lev = CT_INF64, lexp = CT_INF64, fmin = CT_INF64;
+  int64_t gmin = CT_INF64;  // cached minimum of grow_at over this lane's programs
   auto own = [&](int p) { return lane == (p & 31); };
   auto bit = [&](int p) { return 1u << (p >> 5); };
   auto turn_rec = [&](int p, int t) -> int4 { return __ldg(&a.turns[prog[p].turn0 + t]); };
@@ -596,6 +619,53 @@ __device__ __forceinline__ void replay_one_ns(const ReplayArgs& a, int64_t r, un
     for (int s = 0; s < NS; ++s) m = min(m, fin[lane + 32 * s]);
     fmin = m;
   };
+  auto rescan_gmin = [&]() {
+    int64_t m = CT_INF64;
+#pragma unroll
+    for (int s = 0; s < NS; ++s) m = min(m, grow_at[lane + 32 * s]);
+    gmin = m;
+  };
+  // Priority among running requests (R28): program index (program FCFS), else (request
+  // arrival | attained service, index); pick_best = highest priority, pick_worst = lowest.
+  auto run_key = [&](int p) -> int64_t { return plas ? svc[p] : req[p]; };
+  auto pick_best = [&](uint32_t m) -> int {
+    if (prio == CT_PRIO_PROG_FCFS) {
+      const uint32_t slots = __reduce_or_sync(FULL_MASK, m);
+      const int s0 = __ffs(slots) - 1;
+      return 32 * s0 + __ffs(__ballot_sync(FULL_MASK, (m >> s0) & 1u)) - 1;
+    }
+    int64_t bk = CT_INF64;
+    int bp = 0x7fffffff;
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+      const int pl = lane + 32 * s;
+      if ((m >> s) & 1u) {
+        const int64_t k = run_key(pl);
+        if (k < bk) { bk = k; bp = pl; }
+      }
+    }
+    const int64_t mk = warp_min64_redux(bk);
+    return (int)__reduce_min_sync(FULL_MASK, (uint32_t)(bk == mk ? bp : 0x7fffffff));
+  };
+  auto pick_worst = [&](uint32_t m) -> int {
+    if (prio == CT_PRIO_PROG_FCFS) {
+      const uint32_t slots = __reduce_or_sync(FULL_MASK, m);
+      const int s1 = 31 - __clz(slots);
+      return 32 * s1 + 31 - __clz(__ballot_sync(FULL_MASK, (m >> s1) & 1u));
+    }
+    int64_t wk = -1;
+    int wp = -1;
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+      const int pl = lane + 32 * s;
+      if ((m >> s) & 1u) {
+        const int64_t k = run_key(pl);
+        if (k >= wk) { wk = k; wp = pl; }  // later slot = higher index wins ties
+      }
+    }
+    const int64_t mk = warp_max64(wk);
+    return (int)__reduce_max_sync(FULL_MASK, (uint32_t)(wk == mk ? wp + 1 : 0)) - 1;
+  };
 
   int64_t now = 0, iter_end = 0, n_it = 0, busy = 0;
   bool in_flight = false;
@@ -629,6 +699,36 @@ __device__ __forceinline__ void replay_one_ns(const ReplayArgs& a, int64_t r, un
         pb &= ~bit(v);
         if (texp[v] != CT_INF64) { texp[v] = CT_INF64; rescan_lexp(); }
       }
+    }
+    __syncwarp();
+  };
+  // owner: first boundary after n_it at which a running request holding ceil(x / bs) blocks
+  // for x tokens needs another one (R27); INF when it finishes first
+  auto set_grow = [&](int p, int64_t x, int64_t fp) {
+    const int64_t B = (int64_t)ceil_div_magic((uint32_t)x, bsm);
+    const int64_t nx = n_it + (B * bs - x) + 1;
+    grow_at[p] = nx < fp ? nx : CT_INF64;
+    gmin = min(gmin, grow_at[p]);
+  };
+  // vLLM recompute preemption of running request v (R28): its GPU KV is dropped and it
+  // re-enters Q marked preempted, remembering the tokens it has emitted.  Uniform.
+  auto preempt = [&](int v) {
+    const int64_t g = gblk[v];
+    const int64_t fv = fin[v];
+    const int dec = turn_rec(v, turn[v]).y;
+    free_blk += g;
+    kv_sum -= g;
+    --n_run;
+    __syncwarp();
+    if (own(v)) {
+      rb &= ~bit(v);
+      qb |= bit(v);
+      xb |= bit(v);
+      emt[v] = (int32_t)(dec - (fv - n_it));
+      fin[v] = CT_INF64;
+      grow_at[v] = CT_INF64;
+      gblk[v] = 0;
+      req[v] = now;
     }
     __syncwarp();
   };
@@ -794,6 +894,40 @@ __device__ __forceinline__ void replay_one_ns(const ReplayArgs& a, int64_t r, un
       if (lane == 0) acc->exp += cnt;
       for_each_set(mx, [&](int p) { evict_unpin(p); });
     }
+    // (a2) KV growth (NEXT-2, R27/R28): running requests that need a block for their next
+    // token, best-ranked first; when the pool is dry the worst-ranked running request is
+    // preempted (possibly the requester itself)
+    if (grow_on && __any_sync(FULL_MASK, gmin <= n_it)) {
+      uint32_t mg = 0;
+      if (gmin <= n_it) {
+#pragma unroll
+        for (int s = 0; s < NS; ++s) mg |= (grow_at[lane + 32 * s] == n_it ? 1u : 0u) << s;
+      }
+      for (;;) {
+        mg &= rb;  // drop candidates preempted as victims
+        if (!__any_sync(FULL_MASK, mg != 0)) break;
+        const int i = pick_best(mg);
+        if (own(i)) mg &= ~bit(i);
+        bool alive = true;
+        while (free_blk < 1) {
+          const int v = pick_worst(rb);
+          preempt(v);
+          if (v == i) { alive = false; break; }
+        }
+        if (alive) {
+          --free_blk;
+          ++kv_sum;
+          if (own(i)) {
+            gblk[i] += 1;
+            const int64_t nx = n_it + bs;  // the next block boundary is bs tokens later
+            grow_at[i] = nx < fin[i] ? nx : CT_INF64;
+          }
+        }
+        __syncwarp();
+      }
+      rescan_gmin();
+      rescan_fmin();
+    }
     int admitted = 0;
     bool stable = true;
     if (__any_sync(FULL_MASK, (qb | yb) != 0)) {
@@ -805,7 +939,15 @@ __device__ __forceinline__ void replay_one_ns(const ReplayArgs& a, int64_t r, un
         for (int s = 0; s < NS; ++s) {
           if ((yb >> s) & 1u) {
             const int p = lane + 32 * s;
-            fin[p] = n_it + turn_rec(p, turn[p]).y;
+            const int4 tj = turn_rec(p, turn[p]);
+            if (grow_on) {  // a preempted request reloaded from DRAM resumes after emt tokens
+              const int32_t e = emt[p];
+              fin[p] = n_it + tj.y - e;
+              emt[p] = 0;
+              set_grow(p, (int64_t)ctx[p] + tj.x + e + 1, fin[p]);
+            } else {
+              fin[p] = n_it + tj.y;
+            }
             fmin = min(fmin, fin[p]);
             lk += gblk[p];
             lp += unc[p];
@@ -823,8 +965,11 @@ __device__ __forceinline__ void replay_one_ns(const ReplayArgs& a, int64_t r, un
         if (!__any_sync(FULL_MASK, qb != 0)) break;
         if (n_run + n_load >= E.max_batch) break;
         int h = -1;
+        // preempted requests rank first (R29); only KV growth preempts
+        const bool any_x = grow_on && __any_sync(FULL_MASK, (qb & xb) != 0);
+        const uint32_t cq = any_x ? (qb & xb) : qb;
         if (prio == CT_PRIO_PROG_FCFS) {  // lowest index among pinned-queued, else queued
-          uint32_t sel = qb & pb;
+          uint32_t sel = any_x ? cq : (qb & pb);
           uint32_t slots = __reduce_or_sync(FULL_MASK, sel);
           if (!slots) { sel = qb; slots = __reduce_or_sync(FULL_MASK, sel); }
           const int s0 = __ffs(slots) - 1;
@@ -835,7 +980,7 @@ __device__ __forceinline__ void replay_one_ns(const ReplayArgs& a, int64_t r, un
 #pragma unroll
           for (int s = 0; s < NS; ++s) {
             const int pl = lane + 32 * s;
-            if ((qb >> s) & 1u) {
+            if ((cq >> s) & 1u) {
               const int64_t k = plas ? svc[pl] : req[pl];
               if (k < bk) { bk = k; bp = pl; }
             }
@@ -847,7 +992,11 @@ __device__ __forceinline__ void replay_one_ns(const ReplayArgs& a, int64_t r, un
         const int4 tr = turn_rec(h, turn[h]);
         const int64_t hctx = ctx[h];
         const int64_t hg = gblk[h];
-        const int64_t need = (int64_t)ceil_div_magic((uint32_t)(hctx + tr.x + tr.y), bsm) - hg;
+        // R12: reserve the whole request; R27/R30 (growth): up to the slot of its next token
+        const int32_t he = grow_on ? emt[h] : 0;
+        const bool hx = grow_on && ((__shfl_sync(FULL_MASK, xb, h & 31) >> (h >> 5)) & 1u);
+        const int64_t need =
+            (int64_t)ceil_div_magic((uint32_t)(hctx + tr.x + (grow_on ? he + 1 : tr.y)), bsm) - hg;
         if (need > free_blk && (admitted == 0 || vany)) {
           while (need > free_blk) {  // victims: latest program arrival first, never the head
             const uint32_t cand = pb & ~(own(h) ? bit(h) : 0u);
@@ -869,6 +1018,7 @@ __device__ __forceinline__ void replay_one_ns(const ReplayArgs& a, int64_t r, un
         free_blk -= need;
         const int32_t ng = (int32_t)(hg + need);
         if (lane == 0) acc->bubble += now - req[h];
+        if (bub && own(h)) bub[h] += now - req[h];
         const bool hp = (__shfl_sync(FULL_MASK, pb, h & 31) >> (h >> 5)) & 1u;
         const int64_t hd = dblk[h];
         int64_t cached;
@@ -885,14 +1035,16 @@ __device__ __forceinline__ void replay_one_ns(const ReplayArgs& a, int64_t r, un
           if (lane == 0) acc->reload += 1;
         } else {
           cached = 0;
-          if (lane == 0) acc->recomp += hctx;
         }
-        const int64_t u = hctx + tr.x - cached;
+        // recomputed: context without a cached copy + (R30) what a preemption dropped
+        if (lane == 0) acc->recomp += hctx - cached + (hx ? tr.x + he : 0);
+        const int64_t u = hctx + tr.x + he - cached;
         if (lane == 0) acc->prefill += u;
         __syncwarp();  // every lane has read h's fields before the owner rewrites them
         if (own(h)) {
           qb &= ~bit(h);
           pb &= ~bit(h);  // a queued pin has no pending expiry (cleared at its return)
+          xb &= ~bit(h);
           gblk[h] = ng;
           unc[h] = (int32_t)u;
           if (loading) {
@@ -901,8 +1053,12 @@ __device__ __forceinline__ void replay_one_ns(const ReplayArgs& a, int64_t r, un
             lev = min(lev, ld);
           } else {
             rb |= bit(h);
-            fin[h] = n_it + tr.y;
+            fin[h] = n_it + tr.y - he;
             fmin = min(fmin, fin[h]);
+            if (grow_on) {
+              emt[h] = 0;
+              set_grow(h, hctx + tr.x + he + 1, fin[h]);
+            }
           }
         }
         if (loading) {
@@ -938,7 +1094,7 @@ __device__ __forceinline__ void replay_one_ns(const ReplayArgs& a, int64_t r, un
       if (stable) {
         // macro-step: the first iteration plus identical decode iterations, up to the first
         // finish or the first boundary at or after the next external event
-        const int64_t mfin = warp_min64_redux(fmin);
+        const int64_t mfin = warp_min64_redux(grow_on ? min(fmin, gmin) : fmin);
         const int64_t te = min(warp_min64_redux(min(lev, lexp)), t_arr);
         k = macro_iters(mfin - n_it, te - now, dur1, d, rd_cur);
       }
@@ -1027,10 +1183,16 @@ __device__ __forceinline__ void replay_one_ns(const ReplayArgs& a, int64_t r, un
       if (p < P) jo[p] = status == CT_R_OK ? req[p] : -1;
     }
   }
+  if (bub && status != CT_R_OK) {
+#pragma unroll
+    for (int s = 0; s < NS; ++s)
+      if (lane + 32 * s < P) bub[lane + 32 * s] = -1;
+  }
   __syncwarp();
 }
 
-template <int NS, int MINB>
+// GROW: KV growth (NEXT-2), always through the shared-memory path (also P <= 32).
+template <int NS, int MINB, bool GROW = false>
 __global__ void __launch_bounds__(128, MINB) replay_kernel(ReplayArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x & 31;
@@ -1041,10 +1203,10 @@ __global__ void __launch_bounds__(128, MINB) replay_kernel(ReplayArgs a) {
     idx = __shfl_sync(FULL_MASK, idx, 0);
     const int64_t r = a.r_begin + (int64_t)idx;
     if (r >= a.r_end) break;
-    if (NS == 1)
+    if (NS == 1 && !GROW)
       replay_one_w32(a, r, (Stat*)wm, lane);
     else
-      replay_one_ns<NS>(a, r, wm, lane);
+      replay_one_ns<NS, GROW>(a, r, wm, lane);
   }
 }
 
@@ -1059,7 +1221,20 @@ static int minb() {
   return g_minb;
 }
 
-static void* pick(int ns) {
+static void* pick(int ns, bool growth) {
+  if (growth) {
+    switch (ns) {
+      case 1: return (void*)replay_kernel<1, 1, true>;
+      case 2: return (void*)replay_kernel<2, 1, true>;
+      case 3: return (void*)replay_kernel<3, 1, true>;
+      case 4: return (void*)replay_kernel<4, 1, true>;
+      case 5: return (void*)replay_kernel<5, 1, true>;
+      case 6: return (void*)replay_kernel<6, 1, true>;
+      case 7: return (void*)replay_kernel<7, 1, true>;
+      case 8: return (void*)replay_kernel<8, 1, true>;
+    }
+    return nullptr;
+  }
   switch (ns) {
     case 1:
       switch (minb()) {
@@ -1079,8 +1254,8 @@ static void* pick(int ns) {
   return nullptr;
 }
 
-int replay_occupancy(int ns, int warps_per_block, int smem_per_block) {
-  void* k = pick(ns);
+int replay_occupancy(int ns, bool growth, int warps_per_block, int smem_per_block) {
+  void* k = pick(ns, growth);
   if (!k) return 0;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_per_block);
   int nb = 0;
@@ -1088,9 +1263,9 @@ int replay_occupancy(int ns, int warps_per_block, int smem_per_block) {
   return nb;
 }
 
-cudaError_t launch_replay(const ReplayArgs& a, int ns, int warps_per_block, int grid,
+cudaError_t launch_replay(const ReplayArgs& a, int ns, bool growth, int warps_per_block, int grid,
                           cudaStream_t s) {
-  void* k = pick(ns);
+  void* k = pick(ns, growth);
   if (!k) return cudaErrorInvalidValue;
   int smem = a.smem_per_warp * warps_per_block;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
