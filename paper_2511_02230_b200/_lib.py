@@ -9,7 +9,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libcontinuum.so")
+LIB_PATH = os.environ.get("CT_LIB_PATH") or os.path.join(HERE, "libcontinuum.so")  # override: experiments only
 
 i32, i64, u64, vp = C.c_int32, C.c_int64, C.c_uint64, C.c_void_p
 

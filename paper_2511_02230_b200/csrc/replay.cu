@@ -36,19 +36,20 @@ int replay_smem_per_warp(int ns, int F, bool growth) {
 // admission) is serialised in program-index order with the operands broadcast by shuffles.
 // Same semantics as replay_one<NS> (C-5/C-6), checked byte for byte by the tests.
 // Iterations in one macro-step: the smallest j <= m (m = iterations until the first finish)
-// whose end dur1 + (j-1) d is at or after the next external event at offset gap (INF-safe).
-// rd ~ 1/d estimates ceil((gap - dur1) / d); two integer corrections make it exact.
+// whose end dur1 + (j-1) d is at or after the next external event at offset gap (INF-safe),
+// i.e. min(m, 1 + ceil(g / d)) with g = gap - dur1.  Past the integer test g <= (m-1) d the
+// quotient is below m (a few thousand at most), so the float estimate g * rd (rd ~ 1/d, one
+// MUFU.RCP per batch change) is within one of it and two integer corrections make it exact.
 __device__ __forceinline__ int64_t macro_iters(int64_t m, int64_t gap, int64_t dur1, int64_t d,
-                                               double rd) {
+                                               float rd) {
   if (gap >= CT_INF64 / 2) return m;
   const int64_t g = gap - dur1;
   if (g <= 0) return 1;
-  const double est = (double)g * rd;
-  if (est >= (double)m + 1.0) return m;
-  int64_t c = (int64_t)est;
+  if (g > (m - 1) * d) return m;
+  int64_t c = (int64_t)((float)g * rd);
   while (c * d < g) ++c;
   while (c > 0 && (c - 1) * d >= g) --c;
-  return min(m, 1 + c);
+  return 1 + c;
 }
 
 struct Acc {  // per-replica summary counters (P <= 32 path)
@@ -116,39 +117,42 @@ __device__ __forceinline__ void replay_one_w32(const ReplayArgs& a, int64_t r, S
 
   int64_t now = 0, iter_end = 0, n_it = 0;
   bool in_flight = false;
-  int64_t free_blk = a.kv[kv_i];
-  int64_t dfree = dram_on ? E.dram_blocks : 0, chan = 0;
+  // block counts are < 2^30 (host-validated): 32-bit registers
+  int32_t free_blk = (int32_t)a.kv[kv_i];
+  int32_t dfree = dram_on ? (int32_t)E.dram_blocks : 0;
+  int64_t chan = 0;
   int32_t D = 0, turns_done = 0;  // completed programs and their turns (P <= 32)
   int n_run = 0, n_load = 0;  // n_load counts LOADING and READY
-  int64_t kv_sum = 0, pf = 0;
+  int32_t kv_sum = 0;
+  int64_t pf = 0;
   int status = CT_R_OK;
   // summary counters live in shared memory (lane 0 updates them) to keep registers for occupancy
   Acc* acc = (Acc*)(stats + F + 1);
   if (lane == 0) *acc = Acc{0, 0, 0, 0, 0, 0, 0, 0};
-  int64_t busy = 0;
   // duration of a no-prefill iteration for the current batch (depends on kv_sum only) and its
   // reciprocal for the macro-step division, recomputed only when kv_sum changes
-  int64_t kv_at = -1, d_cur = 0;
-  double rd_cur = 0.0;
+  int32_t kv_at = -1;
+  int64_t d_cur = 0;
+  float rd_cur = 0.0f;
   // next program-event time computed by the last macro-step plan; valid until an event fires
   int64_t t_plan = -1;
 
   // evict(v): free its GPU blocks; DRAM write-through when the tier is on (R18).  Uniform.
   auto evict = [&](int v) {
-    const int64_t g = __shfl_sync(FULL_MASK, gblk, v);
+    const int32_t g = __shfl_sync(FULL_MASK, gblk, v);
     free_blk += g;
     int32_t keep = 0;
     if (dram_on) {
       const uint32_t vctx = __shfl_sync(FULL_MASK, (uint32_t)ctx, v);
       const int64_t nb = ceil_div_magic(vctx, bsm);
       dfree += __shfl_sync(FULL_MASK, dblk, v);
-      if (nb > 0 && nb <= dfree) { keep = (int32_t)nb; dfree -= nb; }
+      if (nb > 0 && nb <= dfree) { keep = (int32_t)nb; dfree -= (int32_t)nb; }
     }
     if (lane == v) { gblk = 0; dblk = keep; pin = false; texp = CT_INF64; }
   };
 
 #ifdef CT_DEBUG_LOOPS
-  int64_t dbg_loops = 0, dbg_sched = 0, dbg_macro = 0;
+  int64_t dbg_loops = 0, dbg_sched = 0, dbg_macro = 0, dbg_mid = 0;
 #endif
   for (;;) {
 #ifdef CT_DEBUG_LOOPS
@@ -176,7 +180,7 @@ __device__ __forceinline__ void replay_one_w32(const ReplayArgs& a, int64_t r, S
             }
           } else {
             const bool mine = texp == now;
-            free_blk += (int64_t)__reduce_add_sync(FULL_MASK, mine ? (uint32_t)gblk : 0u);
+            free_blk += (int32_t)__reduce_add_sync(FULL_MASK, mine ? (uint32_t)gblk : 0u);
             if (mine) { gblk = 0; pin = false; texp = CT_INF64; }
           }
         }
@@ -281,6 +285,9 @@ __device__ __forceinline__ void replay_one_w32(const ReplayArgs& a, int64_t r, S
         }
       }
     }
+#ifdef CT_DEBUG_LOOPS
+    if (in_flight) ++dbg_mid;
+#endif
     if (in_flight) continue;  // mid-iteration: events only mutate Q / stats / pins (R2)
 
     // ---- scheduling point (R3) --------------------------------------------------------------
@@ -307,7 +314,7 @@ __device__ __forceinline__ void replay_one_w32(const ReplayArgs& a, int64_t r, S
       const bool join = st == S_READY;
       const uint32_t m = __ballot_sync(FULL_MASK, join);
       if (m) {
-        kv_sum += (int64_t)__reduce_add_sync(FULL_MASK, join ? (uint32_t)gblk : 0u);
+        kv_sum += (int32_t)__reduce_add_sync(FULL_MASK, join ? (uint32_t)gblk : 0u);
         pf += (int64_t)__reduce_add_sync(FULL_MASK, join ? (uint32_t)unc : 0u);
         n_run += __popc(m);
         n_load -= __popc(m);
@@ -347,7 +354,7 @@ __device__ __forceinline__ void replay_one_w32(const ReplayArgs& a, int64_t r, S
         break;
       }
       // issue h
-      free_blk -= need;
+      free_blk -= (int32_t)need;
       const int32_t ng = hg + (int32_t)need;
       const int64_t hreq = shfl64(req, h);
       if (lane == 0) acc->bubble += now - hreq;
@@ -406,7 +413,7 @@ __device__ __forceinline__ void replay_one_w32(const ReplayArgs& a, int64_t r, S
       if (kv_sum != kv_at) {
         kv_at = kv_sum;
         d_cur = ceil_ps_to_us((uint64_t)(E.c0_ps + E.c_kv_ps * bs * kv_sum));
-        rd_cur = 1.0 / (double)d_cur;
+        rd_cur = __frcp_rn((float)d_cur);
       }
       const int64_t d = d_cur;
       // the first iteration carries the prefill of newly admitted requests (R16)
@@ -429,7 +436,7 @@ __device__ __forceinline__ void replay_one_w32(const ReplayArgs& a, int64_t r, S
       if (n_it + k > E.max_iters) { status = CT_R_EVENT_BUDGET; break; }
       n_it += k;
       iter_end = now + dur;
-      busy += dur;
+      if (lane == 0) acc->busy += dur;  // cold: kept in shared memory, not a register
       if (plas && st == S_RUN) svc += dur;  // every running request accrues the iterations
       in_flight = true;
     }
@@ -467,7 +474,7 @@ __device__ __forceinline__ void replay_one_w32(const ReplayArgs& a, int64_t r, S
       o.sum_bubble_us = acc->bubble;
       o.makespan_us = now - arr0;  // the last event processed is the last completion
       o.iterations = n_it;
-      o.busy_us = busy;
+      o.busy_us = acc->busy;
       o.prefill_tokens = acc->prefill;
       o.recompute_tokens = acc->recomp;
       o.pin_hits = acc->hits;
@@ -478,6 +485,7 @@ __device__ __forceinline__ void replay_one_w32(const ReplayArgs& a, int64_t r, S
       o.reloads = dbg_loops;
       o.victims = dbg_sched;
       o.pin_hits = dbg_macro;
+      o.recompute_tokens = dbg_mid;
 #endif
     } else {
       int64_t* w = (int64_t*)&o;
@@ -679,7 +687,7 @@ __device__ __forceinline__ void replay_one_ns(const ReplayArgs& a, int64_t r, un
   int64_t kv_sum = 0, pf = 0;
   int status = CT_R_OK;
   int64_t kv_at = -1, d_cur = 0;
-  double rd_cur = 0.0;
+  float rd_cur = 0.0f;
 
   // evict(v): free its GPU blocks, DRAM write-through when the tier is on (R18); unpin.  Uniform.
   auto evict_unpin = [&](int v) {
@@ -1083,7 +1091,7 @@ __device__ __forceinline__ void replay_one_ns(const ReplayArgs& a, int64_t r, un
       if (kv_sum != kv_at) {
         kv_at = kv_sum;
         d_cur = ceil_ps_to_us((uint64_t)(E.c0_ps + E.c_kv_ps * bs * kv_sum));
-        rd_cur = 1.0 / (double)d_cur;
+        rd_cur = __frcp_rn((float)d_cur);
       }
       const int64_t d = d_cur;
       // the first iteration carries the prefill of newly admitted requests (R16)

@@ -10,4 +10,4 @@ w = cf.config3(n_seeds=4)
 s, _ = ct.ct_simulate_batch(ctx, ct.DeviceTrace(w.trace), w.sweep, w.engine)
 s = s.cpu().numpy()
 turns = s[:, 1].sum()
-print("loops/turn %.2f sched/turn %.2f macro/turn %.2f" % (s[:, 15].sum() / turns, s[:, 14].sum() / turns, s[:, 12].sum() / turns))
+print("loops/turn %.2f sched/turn %.2f macro/turn %.2f mid/turn %.2f" % (s[:, 15].sum() / turns, s[:, 14].sum() / turns, s[:, 12].sum() / turns, s[:, 11].sum() / turns))
