@@ -134,8 +134,6 @@ __device__ __forceinline__ void replay_one_w32(const ReplayArgs& a, int64_t r, S
   int32_t kv_at = -1;
   int64_t d_cur = 0;
   float rd_cur = 0.0f;
-  // next program-event time computed by the last macro-step plan; valid until an event fires
-  int64_t t_plan = -1;
 
   // evict(v): free its GPU blocks; DRAM write-through when the tier is on (R18).  Uniform.
   auto evict = [&](int v) {
@@ -159,33 +157,42 @@ __device__ __forceinline__ void replay_one_w32(const ReplayArgs& a, int64_t r, S
     ++dbg_loops;
 #endif
     // ---- next event (R1, R3) --------------------------------------------------------------
-    const int64_t t_prog = t_plan >= 0 ? t_plan : warp_min64_redux(eager ? min(tev, texp) : tev);
-    t_plan = -1;
-    int64_t t = t_prog;
-    if (in_flight) t = min(t, iter_end);
-    if (t == CT_INF64) break;
+    // With an iteration in flight nothing can be scheduled before its end (R2), so every
+    // program event up to iter_end is applied in one pass at the boundary, each program's own
+    // events in R1 order: their effects commute (per-program state, block and statistics sums),
+    // except DRAM write-through, which is applied in (time, index) order.  Idle, the next event
+    // instant is one REDUX minimum.
+    int64_t t;
+    if (in_flight) {
+      t = iter_end;
+    } else {
+      t = warp_min64_redux(eager ? min(tev, texp) : tev);
+      if (t == CT_INF64) break;
+    }
     now = t;
 
-    if (t_prog == now) {
-      // PinExpiry (EAGER, R4/R15): first µs with now > expiry while not in Q
+    if (__any_sync(FULL_MASK, (eager ? min(tev, texp) : tev) <= now)) {
+      // PinExpiry (EAGER, R4/R15): first µs with now > expiry while not in Q; it precedes the
+      // program's own tool return at the same µs (R1)
       if (eager) {
-        uint32_t m = __ballot_sync(FULL_MASK, texp == now);
+        const bool xd = texp <= now && texp <= tev;
+        uint32_t m = __ballot_sync(FULL_MASK, xd);
         if (m) {
           if (lane == 0) acc->exp += __popc(m);
-          if (dram_on) {  // write-through order matters: index order
+          if (dram_on) {  // write-through order matters: (time, index) order
             while (m) {
-              const int p = __ffs(m) - 1;
-              m &= m - 1;
+              const int64_t tm = warp_min64_redux((m >> lane) & 1u ? texp : CT_INF64);
+              const int p = __ffs(__ballot_sync(FULL_MASK, ((m >> lane) & 1u) && texp == tm)) - 1;
+              m &= ~(1u << p);
               evict(p);
             }
           } else {
-            const bool mine = texp == now;
-            free_blk += (int32_t)__reduce_add_sync(FULL_MASK, mine ? (uint32_t)gblk : 0u);
-            if (mine) { gblk = 0; pin = false; texp = CT_INF64; }
+            free_blk += (int32_t)__reduce_add_sync(FULL_MASK, xd ? (uint32_t)gblk : 0u);
+            if (xd) { gblk = 0; pin = false; texp = CT_INF64; }
           }
         }
       }
-      const bool due = tev == now;
+      const bool due = tev <= now;
       // ToolReturn == OnRequestArrive of a seen program
       const bool ret = due && st == S_TOOL;
       if (need_stats) {
@@ -215,7 +222,7 @@ __device__ __forceinline__ void replay_one_w32(const ReplayArgs& a, int64_t r, S
         ++turn;
         rec = __ldg((const int4*)a.turns + turn0 + turn);
         st = S_QUEUED;
-        req = now;
+        req = tev;  // the event's own instant
         tev = CT_INF64;
         texp = CT_INF64;  // a retained pin has no expiry event while waiting
       }
@@ -224,7 +231,7 @@ __device__ __forceinline__ void replay_one_w32(const ReplayArgs& a, int64_t r, S
       // ProgramArrival
       if (due && st == S_OUT) {
         st = S_QUEUED;
-        req = now;
+        req = tev;
         tev = CT_INF64;
         rec = __ldg((const int4*)a.turns + turn0);
       }
@@ -426,7 +433,6 @@ __device__ __forceinline__ void replay_one_w32(const ReplayArgs& a, int64_t r, S
         // finish or the first boundary at or after the next external event
         const int64_t mfin = warp_min64_redux(st == S_RUN ? fin : CT_INF64);
         const int64_t te = warp_min64_redux(min(tev, texp));
-        if (eager) t_plan = te;  // = the next loop's program-event minimum (nothing changes)
         k = macro_iters(mfin - n_it, te - now, dur1, d, rd_cur);
 #ifdef CT_DEBUG_LOOPS
         ++dbg_macro;
