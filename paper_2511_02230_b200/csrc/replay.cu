@@ -749,30 +749,55 @@ __device__ __forceinline__ void replay_one_ns(const ReplayArgs& a, int64_t r, un
 
   for (;;) {
     // ---- next event (R1, R3) --------------------------------------------------------------
-    const int64_t t_prog = warp_min64_redux(eager ? min(lev, lexp) : lev);
-    int64_t t = min(t_prog, t_arr);
-    if (in_flight) t = min(t, iter_end);
-    if (t == CT_INF64) break;
+    // In flight: every event up to iter_end is applied in one pass at the boundary (as in
+    // replay_one_w32: effects commute, DRAM write-through in (time, index) order).
+    int64_t t;
+    if (in_flight) {
+      t = iter_end;
+    } else {
+      t = min(warp_min64_redux(eager ? min(lev, lexp) : lev), t_arr);
+      if (t == CT_INF64) break;
+    }
     now = t;
 
-    if (t_prog == now) {
-      // PinExpiry (EAGER): first µs with now > expiry while not in Q (R4/R15)
-      if (eager && __any_sync(FULL_MASK, lexp == now)) {
+    {
+      // PinExpiry (EAGER): first µs with now > expiry while not in Q (R4/R15);
+      // it precedes the program's own tool return at the same µs (R1)
+      if (eager && __any_sync(FULL_MASK, lexp <= now)) {
         uint32_t me = 0;
-        if (lexp == now) {
+        if (lexp <= now) {
 #pragma unroll
-          for (int s = 0; s < NS; ++s) me |= (texp[lane + 32 * s] == now ? 1u : 0u) << s;
+          for (int s = 0; s < NS; ++s) {
+            const int p = lane + 32 * s;
+            me |= (texp[p] <= now && texp[p] <= tev[p] ? 1u : 0u) << s;
+          }
         }
         const uint32_t cnt = __reduce_add_sync(FULL_MASK, (uint32_t)__popc(me));
         if (lane == 0) acc->exp += cnt;
-        for_each_set(me, [&](int p) { evict_unpin(p); });
+        if (dram_on) {  // write-through order matters: (time, index)
+          while (__any_sync(FULL_MASK, me != 0)) {
+            int64_t lm = CT_INF64;
+#pragma unroll
+            for (int s = 0; s < NS; ++s)
+              if ((me >> s) & 1u) lm = min(lm, texp[lane + 32 * s]);
+            const int64_t tm = warp_min64_redux(lm);
+            uint32_t mt = 0;
+#pragma unroll
+            for (int s = 0; s < NS; ++s)
+              mt |= (((me >> s) & 1u) && texp[lane + 32 * s] == tm ? 1u : 0u) << s;
+            me &= ~mt;
+            for_each_set(mt, [&](int p) { evict_unpin(p); });
+          }
+        } else {
+          for_each_set(me, [&](int p) { evict_unpin(p); });
+        }
       }
       // ToolReturn (OnRequestArrive of a seen program) and LoadDone
-      if (__any_sync(FULL_MASK, lev == now)) {
+      if (__any_sync(FULL_MASK, lev <= now)) {
         uint32_t md = 0;
-        if (lev == now) {
+        if (lev <= now) {
 #pragma unroll
-          for (int s = 0; s < NS; ++s) md |= (tev[lane + 32 * s] == now ? 1u : 0u) << s;
+          for (int s = 0; s < NS; ++s) md |= (tev[lane + 32 * s] <= now ? 1u : 0u) << s;
         }
         const uint32_t mret = md & tb, mld = md & lb;
         if (need_stats) {
@@ -802,7 +827,7 @@ __device__ __forceinline__ void replay_one_ns(const ReplayArgs& a, int64_t r, un
             const int p = lane + 32 * s;
             if ((mret >> s) & 1u) {
               turn[p] += 1;
-              req[p] = now;
+              req[p] = tev[p];  // the event's own instant
               tev[p] = CT_INF64;
               if (texp[p] != CT_INF64) { texp[p] = CT_INF64; rescan_e = true; }  // retained pin
             }
@@ -819,9 +844,9 @@ __device__ __forceinline__ void replay_one_ns(const ReplayArgs& a, int64_t r, un
       }
     }
     // ProgramArrival (programs arrive in index order)
-    while (t_arr == now) {
+    while (t_arr <= now) {
       const int p = next_arr;
-      if (own(p)) { qb |= bit(p); req[p] = now; }
+      if (own(p)) { qb |= bit(p); req[p] = t_arr; }
       ++next_arr;
       t_arr = next_arr < P ? arrival(next_arr) : CT_INF64;
     }
