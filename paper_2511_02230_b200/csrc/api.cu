@@ -32,7 +32,7 @@ struct ct_ctx {
   void* h_jct = nullptr;
   size_t h_jct_cap = 0;
   ct_launch_info last{};
-  int fit_occ = 0, fit_occ_smem = -1;
+  int fit_occ = 0, fit_occ_smem = -1, fit_occ_v = -1;
   bool timing = false;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};  // replay start/end, fit start/end
   bool replay_timed = false, fit_timed = false;
@@ -355,10 +355,11 @@ int ct_fit_ttl(ct_ctx* c, const ct_samples* sm, const ct_cost_params* cp,
   // < 2^32, 16-bit packed counts < 2^16) and a lane <= CH/32 + 2 (64-bit sum of squares < 2^64)
   // CTA-shared variant: CTA chunks of CH samples over 256 threads, a lane-index replica sees
   // <= CH/32 + 64 samples and a thread <= CH/256 + 8.
-  const bool cta = ct::fit_hist_cta_chunks();
-  const int R = cta ? 1 : ct::fit_hist_repl();
+  const ct::FitPlan plan = ct::fit_plan(K, est->b_us);
+  const bool cta = plan.cta;
+  const int R = cta ? 1 : plan.repl;
   const int per_thread_div = cta ? 256 : 32;
-  const bool ranges = ct::fit_hist_ranges();
+  const bool ranges = plan.ranges;
   int64_t CH = ranges ? (1ll << 20) : cta ? (1ll << 17) : (1ll << 16);
   const int64_t rdiv = cta ? 32 : R;
   while (CH > 256 && (CH / rdiv + 64) * (uint64_t)cp->grid_step_us >= (1ull << 32)) CH >>= 1;
@@ -390,23 +391,43 @@ int ct_fit_ttl(ct_ctx* c, const ct_samples* sm, const ct_cost_params* cp,
   // M = ceil(2^64 / step) < 2^63 for step >= 2; step == 1 runs the identity instantiation
   fa.step_magic = cp->grid_step_us == 1 ? 0 : (uint64_t)((((unsigned __int128)1 << 64) + cp->grid_step_us - 1) / cp->grid_step_us);
   fa.b_us = est->b_us;
+  if (cp->grid_step_us >= 2) {  // Granlund-Montgomery: floor(x / d) for every x < 2^32
+    const uint32_t d = (uint32_t)cp->grid_step_us;
+    const int fl = 31 - __builtin_clz(d);
+    if ((d & (d - 1)) == 0) {
+      fa.div_m = 1u << (32 - fl), fa.div_sh = 0, fa.div_add = 0;  // x >> fl
+    } else {
+      const uint64_t num = 1ull << (32 + fl);
+      uint32_t pm = (uint32_t)(num / d), rem = (uint32_t)(num % d);
+      if (d - rem < (1u << fl)) {
+        fa.div_m = pm + 1, fa.div_sh = fl, fa.div_add = 0;
+      } else {
+        pm += pm;
+        const uint32_t tr = rem + rem;
+        if (tr >= d || tr < rem) pm += 1;
+        fa.div_m = pm + 1, fa.div_sh = fl, fa.div_add = 1;
+      }
+    }
+  }
   fa.hcnt = (unsigned long long*)c->fit;
   fa.hsum = fa.hcnt + (size_t)(F + 1) * (K + 1);
   fa.stat = fa.hsum + (size_t)(F + 1) * (K + 1);
   if (fa.n_chunks > 0) {
-    if (c->fit_occ_smem != ct::fit_hist_smem(K)) {
-      c->fit_occ = ct::fit_hist_occupancy(ct::fit_hist_smem(K));
-      c->fit_occ_smem = ct::fit_hist_smem(K);
+    if (c->fit_occ_smem != plan.smem || c->fit_occ_v != plan.v) {
+      c->fit_occ = ct::fit_hist_occupancy(plan);
+      c->fit_occ_smem = plan.smem;
+      c->fit_occ_v = plan.v;
     }
     if (c->fit_occ < 1) return fail(CT_ECUDA, "fit_hist kernel cannot be resident");
     // warp variants: every warp takes its own chunks; CTA variant: one chunk per CTA
-    const int wpb = ct::fit_hist_cta_chunks() ? 1 : ct::fit_hist_threads() / 32;
+    const int wpb = plan.cta ? 1 : plan.threads / 32;
     // range variant: >= 2^15 samples per CTA (each CTA zeroes and flushes a full histogram)
     const int64_t items = ranges ? (fa.tool_off[F] - fa.tool_off[0] + (1 << 15) - 1) >> 15
                                  : (fa.n_chunks + wpb - 1) / wpb;
     const int grid = (int)std::min<int64_t>((int64_t)c->sm_count * c->fit_occ, items);
     if (c->timing) CT_CUDA(cudaEventRecord(c->ev[2], s));
-    cudaError_t e = ct::launch_fit_hist(fa, grid, s);
+    fa.stages = plan.stages;
+    cudaError_t e = ct::launch_fit_hist(fa, plan, grid, s);
     if (e != cudaSuccess) return cuda_fail(e, "fit_hist launch");
     if (c->timing) CT_CUDA(cudaEventRecord(c->ev[3], s));
     c->fit_timed = c->timing;

@@ -45,8 +45,10 @@ struct FitArgs {
   int64_t chunk_off[CT_MAX_TOOLS + 1];  // first chunk index of each tool
   int F, K;
   int64_t step;          // grid step (µs)
-  uint64_t step_magic;   // ceil(2^40 / step) for the bucket quotient
+  uint64_t step_magic;   // ceil(2^64 / step) for the bucket quotient (per-warp kernels)
+  uint32_t div_m, div_sh, div_add;  // floor(x / step) for 32-bit x (CTA kernels, step >= 2)
   int64_t b_us;
+  int stages;  // TMA ring depth (TMA-staged variant)
   unsigned long long* hcnt;  // [(F+1) * (K+1)] bucket counts, row F pooled over tools
   unsigned long long* hsum;  // [(F+1) * (K+1)] bucket sums (buckets < K)
   unsigned long long* stat;  // [(F+1) * 6]: n, s1, s2 limbs (32-bit limb sums in u64 slots)
@@ -64,14 +66,17 @@ struct ScanArgs {
   int64_t* stats_out;
 };
 
-cudaError_t launch_fit_hist(const FitArgs& a, int grid, cudaStream_t s);
+// Kernel variant, launch shape and shared memory of the histogram pass for grid size K and
+// clamp b (ttl_fit.cu: CT_FIT_VARIANT overrides the default for experiments).
+struct FitPlan {
+  int v, threads, smem, repl, stages;
+  bool cta;     // CTA-shared lane-indexed histogram (work items are CTA-level)
+  bool ranges;  // one contiguous sample range per CTA, pieces of <= ch samples
+};
+FitPlan fit_plan(int K, int64_t b_us);
+int fit_hist_occupancy(const FitPlan& p);  // resident CTAs per SM
+cudaError_t launch_fit_hist(const FitArgs& a, const FitPlan& p, int grid, cudaStream_t s);
 cudaError_t launch_fit_scan(const ScanArgs& a, cudaStream_t s);
-int fit_hist_threads();
-int fit_hist_repl();  // histogram replicas per warp of the selected variant
-bool fit_hist_cta_chunks();  // work items are CTA-level chunks (CTA-shared histogram)
-bool fit_hist_ranges();      // CTA b takes one contiguous sample range (pieces of <= ch)
-int fit_hist_smem(int K);
-int fit_hist_occupancy(int smem);  // resident CTAs per SM
 
 cudaError_t launch_jct_stats(const ct_replica_summary* s, int64_t n, int32_t n_cells,
                              ct_cell_stats* out, cudaStream_t st);

@@ -14,6 +14,7 @@
 // shared memory, then per turn bucket j n U(k) in 128-bit integers (extension C-4) and a warp
 // argmax with the smallest k on ties; the pooled row sums the tool rows; tools with n_f < N take
 // the pooled result; thread 0 also evaluates CalcTTL on the row's statistics.
+#include <algorithm>
 #include <cstdlib>
 
 #include "ct_device.cuh"
@@ -21,6 +22,15 @@
 
 namespace ct {
 
+// TMA-staged variant (fit_hist_tma_kernel)
+constexpr int TMA_THREADS = 1024;
+constexpr int TMA_CW = 31;                     // consumer warps
+constexpr int TMA_CT = 32 * TMA_CW;            // consumer threads
+constexpr int TMA_U = 2;                       // int4 per consumer thread per stage
+constexpr int TMA_STAGE = TMA_CT * 16 * TMA_U;  // bytes per stage (every consumer thread busy)
+constexpr int TMA_MAX_STAGES = 8;
+// per-warp TMA variant (fit_hist_wtma_kernel): warps, bytes per chunk, ring slots per warp
+constexpr int WTMA_W = 20, WTMA_B = 2048, WTMA_S = 3;
 constexpr int FIT_WARPS = 2;                 // warps per CTA; every warp is independent
 constexpr int FIT_THREADS = 32 * FIT_WARPS;
 
@@ -40,29 +50,59 @@ static const FitVariant kVariants[] = {{16, false, 16}, {16, true, 16}, {8, fals
                                        {32, false, 4},                    // 13: 12 with U 4
                                        {32, false, 6},                    // 14: 12 with U 6
                                        {32, false, 8},                    // 15: 12, CTA ranges
-                                       {32, false, 8}};                   // 16: 11, CTA ranges
+                                       {32, false, 8},                    // 16: 11, CTA ranges
+                                       {32, false, 0},                    // 17: 15, TMA-staged
+                                       {32, false, 0},                    // 18: 16, TMA-staged
+                                       {32, false, 0},                    // 19: 15, per-warp TMA
+                                       {32, false, 0}};                   // 20: 16, per-warp TMA
+constexpr int N_VARIANTS = sizeof kVariants / sizeof kVariants[0];
 static int g_variant = -1;  // default 15: measured best on B200 (DESIGN.md §8 variant table)
 
 static int variant() {
-  static_assert(sizeof kVariants / sizeof kVariants[0] == 17, "variant table / hist_fn mismatch");
+  static_assert(N_VARIANTS == 21, "variant table / hist_fn mismatch");
   if (g_variant < 0) {
     const char* e = getenv("CT_FIT_VARIANT");
     int v = e ? atoi(e) : 15;
-    g_variant = (v >= 0 && v < (int)(sizeof kVariants / sizeof kVariants[0])) ? v : 15;
+    g_variant = (v >= 0 && v < N_VARIANTS) ? v : 15;
   }
   return g_variant;
 }
 
-static bool cta_variant() { return variant() >= 10; }
-bool fit_hist_ranges() { return variant() >= 15; }
-int fit_hist_threads() { return cta_variant() ? 256 : FIT_THREADS; }
-int fit_hist_repl() { return kVariants[variant()].repl; }
-bool fit_hist_cta_chunks() { return cta_variant(); }
 static int smem_words(int K, const FitVariant& fv) {
   return (K + 1) * (fv.repl + (fv.pack ? fv.repl / 2 : fv.repl));
 }
-int fit_hist_smem(int K) {
-  return cta_variant() ? (K + 1) * 64 * 4 : FIT_WARPS * 4 * smem_words(K, kVariants[variant()]);
+constexpr int SMEM_LIMIT = 232448 - 2048;  // B200 opt-in per-block shared memory, minus static
+
+// Variant choice for one call: the selected variant, its 32-bit-sum-free twin when b >= 2^26 µs,
+// fewer TMA stages or the per-warp 4-replica kernel when the histogram does not fit.
+FitPlan fit_plan(int K, int64_t b_us) {
+  int v = variant();
+  if (b_us >= (1ll << 26)) {  // 32-bit partial sums need b < 2^26 µs
+    if (v == 12 || v == 13 || v == 14) v = 11;
+    if (v == 15) v = 16;
+    if (v == 17) v = 18;
+    if (v == 19) v = 20;
+  }
+  FitPlan p;
+  p.stages = 0;
+  const int hist = (K + 1) * 64 * 4;
+  if (v >= 19) {
+    if (hist + WTMA_W * WTMA_S * (WTMA_B + 8) > SMEM_LIMIT) v = 8;
+  } else if (v >= 17) {
+    p.stages = std::min(TMA_MAX_STAGES, (SMEM_LIMIT - hist) / (TMA_STAGE + 16));
+    if (p.stages < 2) v = 8;
+  } else if (v >= 10 && hist > SMEM_LIMIT) {
+    v = 8;
+  }
+  p.v = v;
+  p.cta = v >= 10;
+  p.ranges = v >= 15;
+  p.repl = kVariants[v].repl;
+  p.threads = v >= 19 ? 32 * WTMA_W : v >= 17 ? TMA_THREADS : v >= 10 ? 256 : FIT_THREADS;
+  p.smem = v >= 19   ? hist + WTMA_W * WTMA_S * (WTMA_B + 8)
+           : v >= 17 ? hist + p.stages * (TMA_STAGE + 16)
+                     : v >= 10 ? hist : FIT_WARPS * 4 * smem_words(K, kVariants[v]);
+  return p;
 }
 
 __device__ __forceinline__ void red_shared(uint32_t addr, uint32_t v) {
@@ -76,6 +116,7 @@ __device__ __forceinline__ void mad_wide(uint64_t& acc, uint32_t a, uint32_t b) 
 struct Lane {
   uint32_t rs_base, cnt_base, cnt_inc;  // shared-window addresses of this lane's replica
   uint32_t K, step, mhi, mlo, xoff, b_us;
+  uint32_t dm, dsh, dadd;  // 32-bit Granlund-Montgomery divisor (CTA-shared kernels)
 };
 
 // One sample d of the lane.  Bucket k = min(ceil(d / step), K) (a hit for tau_k iff d <= k step);
@@ -231,6 +272,10 @@ constexpr int FW = 8;
 // CTA-kernel sample: count at [base + 256 b], remainder at +128 (one address, immediate offset);
 // the caller keeps 4 independent 64-bit sum-of-squares accumulators (ILP for the accumulate form
 // of IMAD.WIDE) and, when b < 2^26, a 32-bit sum accumulator flushed every 32 samples.
+//
+// The quotient uses a 32-bit Granlund-Montgomery divisor (one IMAD.HI plus shifts and adds on
+// the ALU pipe; FitArgs.div_*), exact for every 32-bit x: the fma pipe, which also carries the
+// remainder and the sum of squares, is the kernel's busiest.
 template <bool IDENT, typename S1>
 __device__ __forceinline__ void sample_cta(const Lane& L, uint32_t base, int32_t d, S1& s1,
                                            uint64_t& s2) {
@@ -239,12 +284,11 @@ __device__ __forceinline__ void sample_cta(const Lane& L, uint32_t base, int32_t
   if (IDENT) {
     q = x;
   } else {
-    uint64_t p = __umulhi(x, L.mlo);
-    mad_wide(p, x, L.mhi);
-    q = (uint32_t)(p >> 32);
+    const uint32_t t = __umulhi(x, L.dm);
+    q = L.dadd ? ((((x - t) >> 1) + t) >> L.dsh) : (t >> L.dsh);
   }
   const uint32_t b = min(q, L.K);
-  const uint32_t addr = base + b * 256u;
+  const uint32_t addr = base + (b << 8);
   red_shared(addr, 1u);
   red_shared(addr + 128u, b * L.step - (uint32_t)d);
   const uint32_t t = min((uint32_t)d, L.b_us);
@@ -263,6 +307,9 @@ __device__ __forceinline__ Lane cta_lane(const FitArgs& a, uint32_t* hsm) {
   L.mlo = (uint32_t)a.step_magic;
   L.xoff = L.step - 1;
   L.b_us = (uint32_t)a.b_us;
+  L.dm = a.div_m;
+  L.dsh = a.div_sh;
+  L.dadd = a.div_add;
   return L;
 }
 
@@ -417,6 +464,314 @@ __global__ void __launch_bounds__(32 * FW) fit_hist_seg_kernel(FitArgs a) {
   }
 }
 
+// ---------------------------------------------------------------------------------------------
+// TMA-staged variant: one CTA of 32 warps per SM.  Warp 31's elected lane streams the CTA's
+// contiguous sample range into a ring of `stages` 31-KB shared-memory buffers with 1-D bulk
+// copies (cp.async.bulk ... mbarrier::complete_tx), so up to stages x 31 KB per SM are in flight
+// without holding registers; warps 0-30 consume each buffer (ld.shared.v4) into the same
+// lane-indexed CTA histogram as the register-staged kernels and release it through an "empty"
+// mbarrier.  Pieces (tool boundaries, the 32-bit bin bound) are cut exactly as in
+// fit_hist_seg_kernel; producer and consumers walk the same piece/stage schedule.
+
+__device__ __forceinline__ void mbar_init(uint32_t a, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t a, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}\n" ::"r"(a), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t a) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(a) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t a, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t mbar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+      "l"(src), "r"(bytes), "r"(mbar)
+      : "memory");
+}
+__device__ __forceinline__ void consumer_bar() {  // named barrier over the consumer warps only
+  asm volatile("bar.sync 1, %0;" ::"n"(TMA_CT) : "memory");
+}
+
+template <bool IDENT, bool FAST32>
+__global__ void __launch_bounds__(TMA_THREADS, 1) fit_hist_tma_kernel(FitArgs a) {
+  extern __shared__ __align__(128) uint32_t hsm[];
+  __shared__ unsigned long long red[TMA_CW][3];
+  const int K = a.K, S = a.stages;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int words = (K + 1) * 64;
+  unsigned char* ring = (unsigned char*)(hsm + words);  // 16-B aligned: words is a multiple of 64
+  const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(ring);
+  const uint32_t full0 = ring_s + S * TMA_STAGE;  // S full barriers, then S empty barriers
+  const uint32_t empty0 = full0 + 8 * S;
+  if (tid == 0) {
+    for (int i = 0; i < S; ++i) {
+      mbar_init(full0 + 8 * i, 1);
+      mbar_init(empty0 + 8 * i, TMA_CW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const Lane L = cta_lane(a, hsm);
+  const int64_t s0 = a.tool_off[0], s1e = a.tool_off[a.F];
+  const int64_t per = (s1e - s0 + gridDim.x - 1) / gridDim.x;
+  auto bnd = [&](int64_t b) -> int64_t {
+    if (b == 0) return s0;
+    if (b >= (int64_t)gridDim.x) return s1e;
+    return min(s1e, max(s0, (s0 + b * per) & ~(int64_t)3));
+  };
+  const int64_t lo0 = bnd(blockIdx.x), hi = bnd((int64_t)blockIdx.x + 1);
+
+  if (warp == TMA_CW) {  // ---- producer ----
+    if (lane == 0) {
+      int slot = 0;
+      uint32_t ph = 0;
+      int64_t issued = 0;
+      int64_t lo = lo0;
+      int tool = 0;
+      while (lo < hi) {
+        while (a.tool_off[tool + 1] <= lo) ++tool;
+        const int64_t end = min(min(hi, a.tool_off[tool + 1]), lo + a.ch);
+        int64_t va = (lo + 3) & ~(int64_t)3;
+        if (va > end) va = end;
+        const int64_t vb = va + ((end - va) & ~(int64_t)3);
+        const unsigned char* src = (const unsigned char*)(a.dur + va);
+        for (int64_t off = 0, nb = 4 * (vb - va); off < nb; off += TMA_STAGE) {
+          const uint32_t bytes = (uint32_t)min((int64_t)TMA_STAGE, nb - off);
+          if (issued >= S) mbar_wait(empty0 + 8 * slot, ph ^ 1u);
+          mbar_expect_tx(full0 + 8 * slot, bytes);
+          bulk_g2s(ring_s + slot * TMA_STAGE, src + off, bytes, full0 + 8 * slot);
+          ++issued;
+          if (++slot == S) { slot = 0; ph ^= 1u; }
+        }
+        lo = end;
+      }
+    }
+    return;
+  }
+
+  // ---- consumers ----
+  int slot = 0;
+  uint32_t ph = 0;
+  int64_t lo = lo0;
+  int tool = 0;
+  while (lo < hi) {
+    while (a.tool_off[tool + 1] <= lo) ++tool;
+    const int64_t beg = lo;
+    const int64_t end = min(min(hi, a.tool_off[tool + 1]), lo + a.ch);
+    lo = end;
+    for (int i = tid; i < words; i += TMA_CT) hsm[i] = 0;
+    consumer_bar();
+    uint64_t s1 = 0, s2 = 0, q1 = 0, q2 = 0, q3 = 0;
+    int64_t va = (beg + 3) & ~(int64_t)3;
+    if (va > end) va = end;
+    const int64_t vb = va + ((end - va) & ~(int64_t)3);
+    if (tid < 32) {  // scalar head and tail (< 4 samples each)
+      if (beg + lane < va) sample<IDENT, 64, false>(L, __ldg(&a.dur[beg + lane]), s1, s2);
+      if (vb + lane < end) sample<IDENT, 64, false>(L, __ldg(&a.dur[vb + lane]), s1, s2);
+    }
+    const uint32_t base = L.cnt_base;
+    for (int64_t off = 0, nb = 4 * (vb - va); off < nb; off += TMA_STAGE) {
+      const int n4 = (int)(min((int64_t)TMA_STAGE, nb - off) >> 4);
+      mbar_wait(full0 + 8 * slot, ph);
+      const uint32_t buf = ring_s + slot * TMA_STAGE;
+      uint32_t s1w = 0;
+      for (int i = tid; i < n4; i += TMA_CT) {
+        int4 x;
+        asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(x.x), "=r"(x.y), "=r"(x.z), "=r"(x.w)
+                     : "r"(buf + 16 * i));
+        if (FAST32) {
+          sample_cta<IDENT>(L, base, x.x, s1w, s2);
+          sample_cta<IDENT>(L, base, x.y, s1w, q1);
+          sample_cta<IDENT>(L, base, x.z, s1w, q2);
+          sample_cta<IDENT>(L, base, x.w, s1w, q3);
+        } else {
+          sample_cta<IDENT>(L, base, x.x, s1, s2);
+          sample_cta<IDENT>(L, base, x.y, s1, q1);
+          sample_cta<IDENT>(L, base, x.z, s1, q2);
+          sample_cta<IDENT>(L, base, x.w, s1, q3);
+        }
+      }
+      if (FAST32) s1 += s1w;  // <= 4 TMA_U samples per thread per stage: < 2^29 when b < 2^26
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty0 + 8 * slot);
+      if (++slot == S) { slot = 0; ph ^= 1u; }
+    }
+    s2 += q1 + q2 + q3;
+    const uint64_t w1 = warp_sum_u64(s1), w2 = warp_sum_u64(s2 & 0xffffffffull),
+                   w3 = warp_sum_u64(s2 >> 32);
+    if (lane == 0) { red[warp][0] = w1; red[warp][1] = w2; red[warp][2] = w3; }
+    consumer_bar();
+    if (tid < 6) {  // tid 0-2: the tool's row, 3-5: the pooled row F
+      const int q = tid % 3;
+      uint64_t sum = 0;
+      for (int w = 0; w < TMA_CW; ++w) sum += red[w][q];
+      unsigned long long* st = a.stat + (tid < 3 ? tool : a.F) * 6;
+      if (q == 0) atomicAdd(st, (unsigned long long)(end - beg));
+      if (sum) atomicAdd(st + 1 + q, (unsigned long long)sum);
+    }
+    for (int b = tid; b <= K; b += TMA_CT) {  // merge the 32 lane replicas of every bucket
+      const uint4* pc = (const uint4*)(hsm + b * 64);
+      uint64_t cn = 0, rr = 0;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const uint4 x = pc[q], y = pc[8 + q];
+        cn += (uint64_t)x.x + x.y + x.z + x.w;
+        rr += (uint64_t)y.x + y.y + y.z + y.w;
+      }
+      if (cn) {
+        const uint64_t sm = b < K ? (uint64_t)b * L.step * cn - rr : 0;
+#pragma unroll
+        for (int row2 = 0; row2 < 2; ++row2) {
+          const int64_t o = (int64_t)(row2 ? a.F : tool) * (K + 1) + b;
+          atomicAdd(&a.hcnt[o], (unsigned long long)cn);
+          if (sm) atomicAdd(&a.hsum[o], (unsigned long long)sm);
+        }
+      }
+    }
+    consumer_bar();
+  }
+}
+
+// Per-warp TMA variant: no producer warp and no cross-warp stage barrier.  The body of each
+// piece is cut into WB-byte chunks dealt round-robin to the CTA's WW warps; every warp keeps
+// WS of its own chunks in flight in a private ring (lane 0 issues the 1-D bulk copy, the warp
+// waits on that slot's mbarrier), so a warp stalls only on its own data.  The histogram and the
+// piece schedule are those of fit_hist_tma_kernel.
+
+// WW warps per CTA, WB bytes per chunk, WS ring slots per warp
+template <bool IDENT, bool FAST32, int WW, int WB, int WS>
+__global__ void __launch_bounds__(32 * WW, 1) fit_hist_wtma_kernel(FitArgs a) {
+  extern __shared__ __align__(128) uint32_t hsm[];
+  __shared__ unsigned long long red[WW][3];
+  const int K = a.K;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int words = (K + 1) * 64;
+  const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(hsm + words) + warp * (WS * WB);
+  const uint32_t bar0 = (uint32_t)__cvta_generic_to_shared(hsm + words) + WW * WS * WB + warp * (8 * WS);
+  if (lane == 0) {
+    for (int i = 0; i < WS; ++i) mbar_init(bar0 + 8 * i, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  const Lane L = cta_lane(a, hsm);
+  const int64_t s0 = a.tool_off[0], s1e = a.tool_off[a.F];
+  const int64_t per = (s1e - s0 + gridDim.x - 1) / gridDim.x;
+  auto bnd = [&](int64_t b) -> int64_t {
+    if (b == 0) return s0;
+    if (b >= (int64_t)gridDim.x) return s1e;
+    return min(s1e, max(s0, (s0 + b * per) & ~(int64_t)3));
+  };
+  int64_t lo = bnd(blockIdx.x);
+  const int64_t hi = bnd((int64_t)blockIdx.x + 1);
+  uint32_t phase = 0;  // bit i: parity of this warp's slot i
+  int tool = 0;
+  const uint32_t base = L.cnt_base;
+  while (lo < hi) {
+    while (a.tool_off[tool + 1] <= lo) ++tool;
+    const int64_t beg = lo;
+    const int64_t end = min(min(hi, a.tool_off[tool + 1]), lo + a.ch);
+    lo = end;
+    int64_t va = (beg + 3) & ~(int64_t)3;
+    if (va > end) va = end;
+    const int64_t vb = va + ((end - va) & ~(int64_t)3);
+    const unsigned char* src = (const unsigned char*)(a.dur + va);
+    const int64_t nb = 4 * (vb - va);
+    const int64_t nch = (nb + WB - 1) / WB;  // chunks of this piece; warp w takes w, w + WW, ...
+    auto issue = [&](int64_t c, int slot) {
+      const uint32_t bytes = (uint32_t)min((int64_t)WB, nb - c * WB);
+      mbar_expect_tx(bar0 + 8 * slot, bytes);
+      bulk_g2s(ring_s + slot * WB, src + c * WB, bytes, bar0 + 8 * slot);
+    };
+    if (lane == 0)  // prefetch before the histogram is zeroed: the copies overlap the barrier
+      for (int k = 0; k < WS; ++k)
+        if (warp + (int64_t)k * WW < nch) issue(warp + (int64_t)k * WW, k);
+    for (int i = tid; i < words; i += 32 * WW) hsm[i] = 0;
+    __syncthreads();
+    uint64_t s1 = 0, s2 = 0, q1 = 0, q2 = 0, q3 = 0;
+    if (tid < 32) {  // scalar head and tail (< 4 samples each)
+      if (beg + lane < va) sample<IDENT, 64, false>(L, __ldg(&a.dur[beg + lane]), s1, s2);
+      if (vb + lane < end) sample<IDENT, 64, false>(L, __ldg(&a.dur[vb + lane]), s1, s2);
+    }
+    int slot = 0;
+    for (int64_t c = warp; c < nch; c += WW) {
+      mbar_wait(bar0 + 8 * slot, (phase >> slot) & 1u);
+      phase ^= 1u << slot;
+      const int n4 = (int)(min((int64_t)WB, nb - c * WB) >> 4);
+      const uint32_t buf = ring_s + slot * WB;
+      uint32_t s1w = 0;
+#pragma unroll
+      for (int u = 0; u < WB / 512; ++u) {
+        const int i = lane + 32 * u;
+        if (i < n4) {
+          int4 x;
+          asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];"
+                       : "=r"(x.x), "=r"(x.y), "=r"(x.z), "=r"(x.w)
+                       : "r"(buf + 16 * i));
+          if (FAST32) {
+            sample_cta<IDENT>(L, base, x.x, s1w, s2);
+            sample_cta<IDENT>(L, base, x.y, s1w, q1);
+            sample_cta<IDENT>(L, base, x.z, s1w, q2);
+            sample_cta<IDENT>(L, base, x.w, s1w, q3);
+          } else {
+            sample_cta<IDENT>(L, base, x.x, s1, s2);
+            sample_cta<IDENT>(L, base, x.y, s1, q1);
+            sample_cta<IDENT>(L, base, x.z, s1, q2);
+            sample_cta<IDENT>(L, base, x.w, s1, q3);
+          }
+        }
+      }
+      if (FAST32) s1 += s1w;  // 4 WB/512 = 16 samples per lane per chunk: < 2^30 when b < 2^26
+      __syncwarp();
+      const int64_t cn = c + (int64_t)WS * WW;
+      if (lane == 0 && cn < nch) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // our reads before the refill
+        issue(cn, slot);
+      }
+      if (++slot == WS) slot = 0;
+    }
+    // warps that received fewer chunks left some slots' phases unused: keep them consistent
+    s2 += q1 + q2 + q3;
+    const uint64_t w1 = warp_sum_u64(s1), w2 = warp_sum_u64(s2 & 0xffffffffull),
+                   w3 = warp_sum_u64(s2 >> 32);
+    if (lane == 0) { red[warp][0] = w1; red[warp][1] = w2; red[warp][2] = w3; }
+    __syncthreads();
+    if (tid < 6) {  // tid 0-2: the tool's row, 3-5: the pooled row F
+      const int q = tid % 3;
+      uint64_t sum = 0;
+      for (int w = 0; w < WW; ++w) sum += red[w][q];
+      unsigned long long* st = a.stat + (tid < 3 ? tool : a.F) * 6;
+      if (q == 0) atomicAdd(st, (unsigned long long)(end - beg));
+      if (sum) atomicAdd(st + 1 + q, (unsigned long long)sum);
+    }
+    for (int b = tid; b <= K; b += 32 * WW) {  // merge the 32 lane replicas of every bucket
+      const uint4* pc = (const uint4*)(hsm + b * 64);
+      uint64_t cn = 0, rr = 0;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const uint4 x = pc[q], y = pc[8 + q];
+        cn += (uint64_t)x.x + x.y + x.z + x.w;
+        rr += (uint64_t)y.x + y.y + y.z + y.w;
+      }
+      if (cn) {
+        const uint64_t sm = b < K ? (uint64_t)b * L.step * cn - rr : 0;
+#pragma unroll
+        for (int row2 = 0; row2 < 2; ++row2) {
+          const int64_t o = (int64_t)(row2 ? a.F : tool) * (K + 1) + b;
+          atomicAdd(&a.hcnt[o], (unsigned long long)cn);
+          if (sm) atomicAdd(&a.hsum[o], (unsigned long long)sm);
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
 template <bool IDENT>
 static void* hist_fn(int v) {
   switch (v) {
@@ -436,7 +791,11 @@ static void* hist_fn(int v) {
     case 13: return (void*)fit_hist_cta_kernel<IDENT, 4, true>;
     case 14: return (void*)fit_hist_cta_kernel<IDENT, 6, true>;
     case 15: return (void*)fit_hist_seg_kernel<IDENT, 8, true>;   // contiguous CTA ranges
-    default: return (void*)fit_hist_seg_kernel<IDENT, 8, false>;
+    case 16: return (void*)fit_hist_seg_kernel<IDENT, 8, false>;
+    case 17: return (void*)fit_hist_tma_kernel<IDENT, true>;      // TMA-staged ranges
+    case 18: return (void*)fit_hist_tma_kernel<IDENT, false>;
+    case 19: return (void*)fit_hist_wtma_kernel<IDENT, true, WTMA_W, WTMA_B, WTMA_S>;  // per-warp TMA
+    default: return (void*)fit_hist_wtma_kernel<IDENT, false, WTMA_W, WTMA_B, WTMA_S>;
   }
 }
 
@@ -538,25 +897,18 @@ __global__ void __launch_bounds__(SCAN_THREADS) fit_scan_kernel(ScanArgs a) {
   }
 }
 
-cudaError_t launch_fit_hist(const FitArgs& a, int grid, cudaStream_t s) {
-  const int smem = fit_hist_smem(a.K);
-  int v = variant();
-  if (a.b_us >= (1ll << 26)) {  // 32-bit partial sums need b < 2^26 µs
-    if (v == 12 || v == 13 || v == 14) v = 11;
-    if (v == 15) v = 16;
-  }
-  void* k = a.step == 1 ? hist_fn<true>(v) : hist_fn<false>(v);
+cudaError_t launch_fit_hist(const FitArgs& a, const FitPlan& p, int grid, cudaStream_t s) {
+  void* k = a.step == 1 ? hist_fn<true>(p.v) : hist_fn<false>(p.v);
   void* args[] = {(void*)&a};
-  return cudaLaunchKernel(k, dim3(grid), dim3(fit_hist_threads()), args, smem, s);
+  return cudaLaunchKernel(k, dim3(grid), dim3(p.threads), args, p.smem, s);
 }
 
-int fit_hist_occupancy(int smem) {
-  for (void* k : {hist_fn<true>(variant()), hist_fn<false>(variant()), hist_fn<true>(11),
-                  hist_fn<false>(11), hist_fn<true>(16), hist_fn<false>(16)})
-    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
+int fit_hist_occupancy(const FitPlan& p) {
+  for (void* k : {hist_fn<true>(p.v), hist_fn<false>(p.v)})
+    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, p.smem) != cudaSuccess)
       return 0;
   int nb = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, hist_fn<false>(variant()), fit_hist_threads(), smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, hist_fn<false>(p.v), p.threads, p.smem);
   return nb;
 }
 

@@ -222,3 +222,16 @@ def test_jct_stats_parity(ctx):
     cs = ct.ct_jct_stats(ctx, s, sw.n_cells).cpu().numpy()
     ocs = O.jct_stats(s.cpu().numpy(), sw.n_cells)
     assert np.array_equal(cs, ocs)
+
+
+@pytest.mark.parametrize("K", [300, 512, 1024])
+def test_fit_large_grids(ctx, K):
+    """Grids whose CTA-shared histogram needs fewer TMA stages (K 300, 512) or does not fit in
+    shared memory at all (K 1024: per-warp 4-replica fallback)."""
+    rng = np.random.default_rng(K)
+    sizes = [5, 100_003, 7, 250_000, 1]
+    off = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+    dur = rng.integers(0, 60_000_000, int(off[-1])).astype(np.int32)
+    g, o = fit_both(ctx, dur, off, K, 50_000, 3, 13_400_000, 40, cf.Estimator())
+    for x, y in zip(g, o):
+        assert np.array_equal(x, y)

@@ -1,4 +1,4 @@
-for v in ${VARIANTS:-12 15 12 15}; do echo "variant $v"; CT_FIT_VARIANT=$v python - <<'PY'
+for v in ${VARIANTS:-15 17 15 17}; do echo "variant $v"; CT_FIT_VARIANT=$v python - <<'PY'
 import torch, numpy as np, sys
 sys.path.insert(0, '.')
 import paper_2511_02230_b200 as ct
