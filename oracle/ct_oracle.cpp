@@ -206,7 +206,9 @@ struct Prog {
   int64_t arrival = 0, completion = -1;
   int64_t service = 0;  // attained engine time (Autellix PLAS)
   int64_t bubble = 0;   // this program's waiting time before admissions (NEXT-3 series)
-  bool first = false;
+  int64_t prem = 0;     // prefill tokens of the current request not yet computed
+  int64_t chunk = 0;    // prefill tokens computed in the iteration in flight
+  bool emit = false;    // emits a token at the end of the iteration in flight
   bool preempted = false;  // recompute-preempted, back in Q (NEXT-2, R28)
 };
 
@@ -246,6 +248,25 @@ struct Sim {
 
   bool dram_on() const { return pol[2] != 0 && eng[6] > 0; }
   bool growth() const { return eng[8] != 0; }  // NEXT-2 block-by-block KV growth (R27)
+  int64_t budget() const { return eng[9]; }     // NEXT-2 chunked prefill token budget (R31), 0 = off
+
+  // R31/R32: token budget left after the running requests: one token per decoding request,
+  // then the prefilling ones in rank order (R28) take min(remaining prefill, budget left).
+  // Sets chunk for every running request; returns the budget left for admissions.
+  int64_t assign_running() {
+    int64_t left = budget();
+    for (int i = 0; i < P; ++i)
+      if (p[i].st == RUNNING && p[i].prem == 0) left -= 1;
+    std::vector<int> order;
+    for (int i = 0; i < P; ++i)
+      if (p[i].st == RUNNING) { p[i].chunk = 0; if (p[i].prem > 0) order.push_back(i); }
+    std::sort(order.begin(), order.end(), [&](int a, int b) { return run_before(a, b); });
+    for (int i : order) {
+      p[i].chunk = std::min(p[i].prem, std::max<int64_t>(left, 0));
+      left -= p[i].chunk;
+    }
+    return left;
+  }
   bool eager() const { return (pol[3] & FLAG_STEP_EXPIRY) == 0; }
 
   // evict(v): free GPU blocks; DRAM write-through when the tier is on (R18).
@@ -379,7 +400,9 @@ struct Sim {
     if (growth()) grow_running();
     // (b) loaded requests join the batch
     for (int i = 0; i < P; ++i)
-      if (p[i].st == READY) { p[i].st = RUNNING; p[i].first = true; }
+      if (p[i].st == READY) { p[i].st = RUNNING; p[i].prem = unc[i]; }
+    // chunked prefill (R31/R32): the running requests take their share of the budget first
+    int64_t left = budget() > 0 ? assign_running() : 1;
     // (c) admit loop (victims PAPER.md:645-655)
     int admitted = 0;
     for (;;) {
@@ -389,6 +412,7 @@ struct Sim {
         nb += p[i].st == RUNNING || p[i].st == LOADING || p[i].st == READY;
       }
       if (nq == 0 || nb >= eng[5]) break;
+      if (budget() > 0 && left <= 0) break;  // R32: no token budget left this iteration
       int h = head();
       const int32_t* tr = turn_rec(h, p[h].turn);
       // R12: reserve the whole request; R27 (growth): up to the slot of the next token
@@ -427,8 +451,16 @@ struct Sim {
       int64_t uncached = p[h].ctx + tr[0] + p[h].emitted - cached;
       prefill += uncached;
       unc[h] = uncached;
-      if (loading) p[h].st = LOADING;
-      else { p[h].st = RUNNING; p[h].first = true; }
+      if (loading) {
+        p[h].st = LOADING;
+      } else {
+        p[h].st = RUNNING;
+        p[h].prem = uncached;
+        if (budget() > 0) {  // R32: a new request takes what is left (a decode takes one token)
+          p[h].chunk = std::min(uncached, left);
+          left -= uncached > 0 ? p[h].chunk : 1;
+        }
+      }
       admitted++;
     }
     // (d) unschedulable: nothing can ever free memory for the head
@@ -452,10 +484,14 @@ struct Sim {
       for (int i = 0; i < P; ++i) {
         if (p[i].st != RUNNING) continue;
         kvsum += p[i].gblk;
-        if (p[i].first) {  // prefill of the uncached tokens happens in the first iteration
-          pf += unc[i];
-          p[i].first = false;
-        }
+        // R16: without a budget the whole prefill runs in the request's first iteration;
+        // R31: with one, this iteration's chunk.  The iteration that completes the prefill (or
+        // any iteration of a decoding request) emits one token.
+        const int64_t c = budget() > 0 ? p[i].chunk : p[i].prem;
+        p[i].emit = p[i].prem == 0 || c == p[i].prem;
+        pf += c;
+        p[i].prem -= c;
+        p[i].chunk = 0;
       }
       i128 ps = (i128)eng[0] + (i128)eng[1] * pf + (i128)eng[2] * bs * kvsum;
       int64_t dur = ceil_div(ps, 1000000);
@@ -537,7 +573,7 @@ struct Sim {
       if (in_flight && iter_end == now) {
         in_flight = false;
         for (int i = 0; i < P; ++i)
-          if (p[i].st == RUNNING) {
+          if (p[i].st == RUNNING && p[i].emit) {
             p[i].emitted += 1;
             if (p[i].emitted == turn_rec(i, p[i].turn)[1]) finish(i);
           }
@@ -601,7 +637,9 @@ int or_simulate(const void* progs, const int32_t* turns, int64_t n_turns, int S,
     return -1;
   if (r_end > (int64_t)S * n_rate * n_kv * n_pol) return -1;
   if (eng[0] < 1 || eng[4] < 1 || eng[5] < 1) return -1;
-  if (eng[8] < 0 || eng[8] > 1 || eng[9] != 0) return -1;
+  // chunked prefill needs room for every decode (budget >= max_batch), reservation mode only
+  if (eng[8] < 0 || eng[8] > 1 || eng[9] < 0) return -1;
+  if (eng[9] > 0 && (eng[9] < eng[5] || eng[8] != 0)) return -1;
   auto one = [&](int64_t r) {
     int64_t pol_i = r % n_pol, kv_i = (r / n_pol) % n_kv, rate_i = (r / ((int64_t)n_pol * n_kv)) % n_rate;
     int64_t seed = r / ((int64_t)n_pol * n_kv * n_rate);

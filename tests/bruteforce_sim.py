@@ -17,6 +17,10 @@ Semantics followed (C-5/C-6, Alg. 1 and §5.3):
     request tops up, best-ranked first, and when the pool is dry the worst-ranked running
     request is thrown back to the queue (recompute), keeping its output so far; thrown-back
     requests are served first
+  * engine prefill_chunk = B > 0 (NEXT-2, R31-R32): each iteration computes at most
+    B tokens: one per decoding request, then prompt pieces for the requests still prefilling,
+    best-ranked first, then newcomers while any budget is left; a request produces output only
+    in iterations after (or in the one that finishes) its prompt
 """
 from __future__ import annotations
 
@@ -33,7 +37,7 @@ def simulate(trace, gap_us, kv, pol, est, eng, fitted=None, horizon=200000):
     progs = trace.programs
     T = trace.turns
     c0, cpf, ckv, ch2d, bs, maxb, dram_cap, max_it, growth, chunk = [int(x) for x in eng]
-    assert chunk == 0
+    assert chunk == 0 or not growth
     prio, pause, dram, flags, t_pin, t_thresh = [int(x) for x in pol[:6]]
     dram_on = dram != 0 and dram_cap > 0
     victims_any = bool(flags & 1)
@@ -49,7 +53,7 @@ def simulate(trace, gap_us, kv, pol, est, eng, fitted=None, horizon=200000):
     # per-program state as plain dicts
     S = [dict(where="out", turn=0, ctx=0, blk=0, dblk=0, pin=None, waited_since=None,
               tool_back=None, load_at=None, left=0, fresh=0, done_at=None, served=0, out=0,
-              thrown=False, waited=0)
+              thrown=False, waited=0, take=0, speaks=False)
          for _ in range(P)]
     free = kv
     dfree = dram_cap if dram_on else 0
@@ -139,6 +143,8 @@ def simulate(trace, gap_us, kv, pol, est, eng, fitted=None, horizon=200000):
             fired = True
             for i in sorted(batch):
                 s = S[i]
+                if not s["speaks"]:
+                    continue
                 s["left"] -= 1
                 s["out"] += 1
                 if s["left"] == 0:
@@ -193,11 +199,21 @@ def simulate(trace, gap_us, kv, pol, est, eng, fitted=None, horizon=200000):
                 if S[i]["where"] == "loaded":
                     S[i]["where"] = "run"
                     batch.append(i)
+            rest = chunk
+            if chunk:
+                for i in batch:
+                    S[i]["take"] = 0
+                rest -= sum(1 for i in batch if S[i]["fresh"] == 0)
+                for i in sorted((i for i in batch if S[i]["fresh"] > 0), key=rank):
+                    S[i]["take"] = min(S[i]["fresh"], max(rest, 0))
+                    rest -= S[i]["take"]
             admitted = 0
             while True:
                 waiting = [i for i in range(P) if S[i]["where"] == "queue"]
                 busy = len(batch) + sum(1 for i in range(P) if S[i]["where"] == "loading")
                 if not waiting or busy >= maxb:
+                    break
+                if chunk and rest <= 0:
                     break
                 thrown = [i for i in waiting if S[i]["thrown"]]
                 if thrown:
@@ -249,6 +265,9 @@ def simulate(trace, gap_us, kv, pol, est, eng, fitted=None, horizon=200000):
                 s["left"] = dec - s["out"]
                 if s["where"] == "run":
                     batch.append(h)
+                    if chunk:
+                        s["take"] = min(s["fresh"], rest)
+                        rest -= s["take"] if s["fresh"] > 0 else 1
                 admitted += 1
             waiting = [i for i in range(P) if S[i]["where"] == "queue"]
             loading = [i for i in range(P) if S[i]["where"] == "loading"]
@@ -259,8 +278,10 @@ def simulate(trace, gap_us, kv, pol, est, eng, fitted=None, horizon=200000):
                     return "budget", None, None
                 ps = c0 + ckv * bs * sum(S[i]["blk"] for i in batch)
                 for i in batch:
-                    ps += cpf * S[i]["fresh"]
-                    S[i]["fresh"] = 0
+                    take = S[i]["take"] if chunk else S[i]["fresh"]
+                    S[i]["speaks"] = S[i]["fresh"] == 0 or take == S[i]["fresh"]
+                    ps += cpf * take
+                    S[i]["fresh"] -= take
                 dur = -(-ps // 10**6)
                 engine_until = now + dur
                 for i in batch:

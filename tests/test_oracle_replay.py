@@ -195,12 +195,14 @@ def random_policy(rng):
                      t_thresh_us=rng.choice([cf.ALWAYS, cf.ALWAYS, rng.randint(1, 30)]))
 
 
-@pytest.mark.parametrize("seed", range(8))
+@pytest.mark.parametrize("seed", range(10))
 def test_bruteforce_tiny(seed):
     """Seeds 0-5: admission reserves the request (R12); seeds 6-7: KV growth with recompute
-    preemption (NEXT-2, R27-R30) on smaller pools, so preemption is frequent."""
+    preemption (NEXT-2, R27-R30) on smaller pools, so preemption is frequent; seeds 8-9:
+    chunked prefill with small token budgets (R31-R32)."""
     rng = random.Random(100 + seed)
-    growth = seed >= 6
+    growth = seed in (6, 7)
+    chunked = seed >= 8
     agree = thrown = 0
     for _ in range(150):
         tr = random_tiny_growth(rng) if growth else random_tiny(rng)
@@ -210,6 +212,9 @@ def test_bruteforce_tiny(seed):
                         bs=rng.choice([1, 2] if growth else [1, 2, 4]),
                         max_batch=rng.choice([2, 256] if growth else [1, 2, 256]),
                         dram_blocks=rng.randint(0, 12), max_iters=10**6, kv_growth=int(growth))
+        if chunked:
+            eng = cf.Engine(**{**eng.__dict__, "max_batch": rng.choice([1, 2, 3]),
+                               "prefill_chunk": rng.choice([3, 4, 6])})
         est = cf.Estimator(b_us=rng.choice([5, 40]), t_def_us=rng.randint(1, 40), n_min=rng.randint(1, 3),
                            a_num=rng.randint(0, 2), a_den=rng.choice([1, 3]), ttl_max_us=rng.choice([0, 25]))
         kv = rng.randint(8, 16) if growth else rng.randint(6, 18)
@@ -451,3 +456,38 @@ def test_growth_preempted_rank_first():
     res, bj, cnt = BF.simulate(tr, GAP1, 6, cf.VLLM.as_array(), cf.Estimator().as_array(),
                                eng.as_array(), horizon=2000)
     assert res == "ok" and bj == [6, 11, 14] and cnt["thrown"] == 1
+
+
+def test_chunked_prefill_hand_trace():
+    """R31-R32, UNIT costs (1 µs + 1 µs per prompt token), bs 1, budget 4 tokens, batch 2.
+    A@0 (6 + 2), B@0 (3 + 1):
+      0->5   A computes 4 of its 6 prompt tokens; the budget is spent, so B waits
+      5->10  A its last 2 (emits token 1); B admitted with the 2 tokens left (bubble 5)
+      10->12 A decodes (1 token), B its last prompt token (emits): both finish at 12
+    Without a budget: one 0->10 prefill iteration for both, B done at 10, A at 11."""
+    tr = traces.tiny([(0, [(6, 2, -1, 0)]), (0, [(3, 1, -1, 0)])])
+    eng = cf.Engine(**{**UNIT.__dict__, "max_batch": 2, "prefill_chunk": 4})
+    sw = cf.Sweep(1, [GAP1], [100], [cf.PROG_FCFS])
+    s, j, b = O.simulate(tr, sw, eng, want_bubble=True)
+    assert list(j[0]) == [12, 12] and list(b[0]) == [0, 5]
+    assert s[0][8] == 3 and s[0][9] == 12 and s[0][10] == 9
+    s0, j0 = run(tr, cf.PROG_FCFS, 100, eng=cf.Engine(**{**UNIT.__dict__, "max_batch": 2}))
+    assert list(j0) == [11, 10]
+    res, bj, cnt = BF.simulate(tr, GAP1, 100, cf.PROG_FCFS.as_array(), cf.Estimator().as_array(),
+                               eng.as_array(), horizon=2000)
+    assert res == "ok" and bj == [12, 12]
+
+
+def test_chunked_prefill_huge_budget_is_unchunked():
+    """A budget no iteration can exhaust changes nothing: byte-identical to R16."""
+    tr = small_workload(13, P=10, n_seeds=2)
+    e0 = cf.Engine(c0_ps=3 * 10**6, c_pf_ps=10**6, c_kv_ps=10**4, c_h2d_ps=2 * 10**6, bs=16,
+                   dram_blocks=300)
+    e1 = cf.Engine(**{**e0.__dict__, "prefill_chunk": 1 << 40})
+    pols = [cf.PROG_FCFS, cf.CONTINUUM, cf.VLLM, cf.AUTELLIX, cf.INFERCEPT, cf.VLLM_LMCACHE]
+    sw = cf.Sweep(2, [1 << 20], [700, 5000], pols, cf.Estimator(t_def_us=30_000, n_min=2))
+    a = O.simulate(tr, sw, e0, want_bubble=True)
+    b = O.simulate(tr, sw, e1, want_bubble=True)
+    assert np.all((a[0][:, 0] & 0xFFFFFFFF) == 0)
+    for x, y in zip(a, b):
+        assert np.array_equal(x, y)
