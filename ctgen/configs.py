@@ -41,7 +41,7 @@ class Engine:
     dram_blocks: int = 0
     max_iters: int = (1 << 62)
     kv_growth: int = 0      # 0: reserve the request at admission (R12); 1: vLLM growth (R27-R30)
-    prefill_chunk: int = 0  # reserved (chunked prefill), must be 0
+    prefill_chunk: int = 0  # 0: whole prompt in the first iteration; B: token budget (R31-R32)
 
     def as_array(self) -> np.ndarray:
         return np.array([self.c0_ps, self.c_pf_ps, self.c_kv_ps, self.c_h2d_ps, self.bs,

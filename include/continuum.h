@@ -121,7 +121,10 @@ typedef struct {            /* linear engine cost model (R16) */
                                blocks (R12); 1: vLLM-style block-by-block growth with
                                recompute preemption and the preempted rank of PAPER.md:541
                                (NEXT-2, R27-R30) */
-  int64_t prefill_chunk;    /* reserved for chunked prefill; must be 0 */
+  int64_t prefill_chunk;    /* 0: a request's whole prompt runs in its first iteration (R16);
+                               B > 0: chunked prefill, at most B tokens per iteration (one per
+                               decoding request, then prompt chunks by rank, R31-R32).
+                               Needs B >= max_batch and kv_growth = 0 (else CT_EINVAL). */
 } ct_engine_params;
 
 typedef struct {            /* 48 B */

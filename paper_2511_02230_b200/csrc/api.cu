@@ -180,7 +180,10 @@ int ct_simulate_batch_ex(ct_ctx* c, const ct_trace_set* tr, const ct_sweep* sw,
       E.c_h2d_ps >= (1ll << 40) || E.bs >= (1 << 20) || E.dram_blocks >= (1ll << 30))
     return fail(CT_EINVAL, "engine constants exceed the int64 fixed-point bounds");
   if (E.kv_growth != 0 && E.kv_growth != 1) return fail(CT_EINVAL, "kv_growth must be 0 or 1");
-  if (E.prefill_chunk != 0) return fail(CT_EINVAL, "prefill_chunk is reserved and must be 0");
+  if (E.prefill_chunk < 0 || (E.prefill_chunk > 0 && E.prefill_chunk < E.max_batch))
+    return fail(CT_EINVAL, "prefill_chunk must be 0 (off) or >= max_batch (R31)");
+  if (E.prefill_chunk > 0 && E.kv_growth != 0)
+    return fail(CT_EINVAL, "chunked prefill is modelled with reservation (kv_growth = 0) only");
   bool need_est = false, need_fit = false, need_h2d = false;
   for (int i = 0; i < sw->n_policies; ++i) {
     const ct_policy& p = sw->policies[i];
@@ -245,7 +248,7 @@ int ct_simulate_batch_ex(ct_ctx* c, const ct_trace_set* tr, const ct_sweep* sw,
                          : (uint64_t)(((((unsigned __int128)1) << 64) + (uint64_t)E.bs - 1) /
                                       (unsigned __int128)(uint64_t)E.bs);
   const int ns = (P + 31) / 32;  // slots per lane
-  const bool growth = E.kv_growth != 0;
+  const bool growth = E.kv_growth != 0 || E.prefill_chunk > 0;  // the vLLM-engine kernels
   const int wpb = 4;
   a.smem_per_warp = ct::replay_smem_per_warp(ns, F, growth);
   const int smem = a.smem_per_warp * wpb;

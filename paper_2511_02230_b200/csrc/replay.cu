@@ -19,10 +19,10 @@ namespace ct {
 
 enum : int { S_OUT = 0, S_QUEUED = 1, S_RUN = 2, S_LOAD = 3, S_READY = 4, S_TOOL = 5, S_DONE = 6 };
 
-int replay_smem_per_warp(int ns, int F, bool growth) {
-  if (ns == 1 && !growth) return (32 * (F + 1) + 48 + 15) & ~15;  // registers hold the programs; SMEM: estimator + Acc
+int replay_smem_per_warp(int ns, int F, bool vllm) {
+  if (ns == 1 && !vllm) return (32 * (F + 1) + 48 + 15) & ~15;  // registers hold the programs; SMEM: estimator + Acc
   int pm = 32 * ns;
-  int b = (growth ? 72 : 60) * pm;  // KV growth adds grow_at (8 B) and emt (4 B) per program
+  int b = (vllm ? 76 : 60) * pm;  // the vLLM engine adds grow_at (8 B), emt and prem (4 B each)
   b = (b + 15) & ~15;
   b += 32 * (F + 1) + 48;  // estimator rows + Acc
   return (b + 15) & ~15;
@@ -514,7 +514,7 @@ __device__ __forceinline__ void replay_one_w32(const ReplayArgs& a, int64_t r, S
 // programs changes.  The next event, the macro-step bound and the first finish are therefore one
 // REDUX minimum each, and only lanes that own a due program scan their slots.  Same semantics as
 // replay_one_w32 (C-5/C-6), checked byte for byte by the tests.
-template <int NS, bool GROW>
+template <int NS, bool VLLM>
 __device__ __forceinline__ void replay_one_ns(const ReplayArgs& a, int64_t r, unsigned char* wm,
                                               int lane) {
   constexpr int PM = 32 * NS;
@@ -528,12 +528,15 @@ __device__ __forceinline__ void replay_one_ns(const ReplayArgs& a, int64_t r, un
   int32_t* dblk = gblk + PM;           // DRAM copy blocks
   int32_t* unc = dblk + PM;            // uncached tokens of the current request
   int32_t* turn = unc + PM;            // current turn
-  // KV growth (NEXT-2, R27-R30) only: next iteration boundary at which the running request
-  // needs one more block (INF otherwise) and tokens emitted before a preemption
-  constexpr bool grow_on = GROW;  // == (a.eng.kv_growth != 0), fixed per instantiation
+  // vLLM engine (NEXT-2) only.  KV growth (R27-R30): next iteration boundary at which the
+  // running request needs one more block (INF otherwise) and tokens emitted before a
+  // preemption.  Chunked prefill (R31-R32): prompt tokens of the current request not computed.
+  const bool grow_on = VLLM && a.eng.kv_growth != 0;
+  const bool chunk_on = VLLM && a.eng.prefill_chunk > 0;
   int64_t* grow_at = (int64_t*)(turn + PM);
   int32_t* emt = (int32_t*)(grow_at + PM);
-  Stat* stats = (Stat*)(wm + (((grow_on ? 72 : 60) * PM + 15) & ~15));
+  int32_t* prem = emt + PM;
+  Stat* stats = (Stat*)(wm + (((VLLM ? 76 : 60) * PM + 15) & ~15));
   Acc* acc = (Acc*)(stats + a.F + 1);
 
   const int P = a.P, F = a.F;
@@ -574,9 +577,10 @@ __device__ __forceinline__ void replay_one_ns(const ReplayArgs& a, int64_t r, un
     dblk[p] = 0;
     unc[p] = 0;
     turn[p] = 0;
-    if (grow_on) {
+    if (VLLM) {
       grow_at[p] = CT_INF64;
       emt[p] = 0;
+      prem[p] = 0;
     }
   }
   // per-program bubble series (NEXT-3): accumulated in place by the owner lane
@@ -969,10 +973,11 @@ __device__ __forceinline__ void replay_one_ns(const ReplayArgs& a, int64_t r, un
     }
     int admitted = 0;
     bool stable = true;
-    if (__any_sync(FULL_MASK, (qb | yb) != 0)) {
-      // (b) loaded requests join the batch
+    int64_t left = 1;  // token budget left in this iteration (chunked prefill)
+    // (b) loaded requests join the batch
+    auto join_ready = [&]() {
       const uint32_t cnt = __reduce_add_sync(FULL_MASK, (uint32_t)__popc(yb));
-      if (cnt) {
+      {
         int64_t lk = 0, lp = 0;
 #pragma unroll
         for (int s = 0; s < NS; ++s) {
@@ -984,6 +989,9 @@ __device__ __forceinline__ void replay_one_ns(const ReplayArgs& a, int64_t r, un
               fin[p] = n_it + tj.y - e;
               emt[p] = 0;
               set_grow(p, (int64_t)ctx[p] + tj.x + e + 1, fin[p]);
+            } else if (chunk_on) {  // its prompt is computed in chunks from (b2) on
+              prem[p] = unc[p];
+              fin[p] = CT_INF64;
             } else {
               fin[p] = n_it + tj.y;
             }
@@ -995,14 +1003,49 @@ __device__ __forceinline__ void replay_one_ns(const ReplayArgs& a, int64_t r, un
         rb |= yb;
         yb = 0;
         kv_sum += (int64_t)warp_sum_u64((uint64_t)lk);
-        pf += (int64_t)warp_sum_u64((uint64_t)lp);
+        if (!chunk_on) pf += (int64_t)warp_sum_u64((uint64_t)lp);
         n_run += cnt;
         n_load -= cnt;
       }
+    };
+    if (chunk_on) {  // loaded requests join first: (b2) shares the budget among all running
+      if (__any_sync(FULL_MASK, yb != 0)) join_ready();
+      // (b2) chunked prefill (R31/R32): one token per decoding request, then the prefilling
+      // running requests, best-ranked first, take min(remaining prompt, budget left)
+      uint32_t nd = 0, mp = 0;
+#pragma unroll
+      for (int s = 0; s < NS; ++s)
+        if ((rb >> s) & 1u) {
+          if (prem[lane + 32 * s] == 0) ++nd; else mp |= 1u << s;
+        }
+      left = E.prefill_chunk - (int64_t)__reduce_add_sync(FULL_MASK, nd);
+      while (__any_sync(FULL_MASK, mp != 0)) {
+        const int i = pick_best(mp);
+        const int64_t c = min((int64_t)prem[i], max(left, (int64_t)0));
+        left -= c;
+        pf += c;
+        __syncwarp();
+        if (own(i)) {
+          mp &= ~bit(i);
+          prem[i] -= (int32_t)c;
+          if (prem[i] == 0) {  // the prompt completes in this iteration, which emits token 1
+            fin[i] = n_it + turn_rec(i, turn[i]).y;
+            fmin = min(fmin, fin[i]);
+          }
+        }
+        __syncwarp();
+      }
+    }
+    if (__any_sync(FULL_MASK, (qb | yb) != 0)) {
+      if (__any_sync(FULL_MASK, yb != 0)) join_ready();
       // (c) admit loop (victims PAPER.md:645-655)
       for (;;) {
         if (!__any_sync(FULL_MASK, qb != 0)) break;
         if (n_run + n_load >= E.max_batch) break;
+        if (chunk_on && left <= 0) {  // R32: no token budget left in this iteration; the next
+          stable = false;             // boundary has a fresh budget, so it must be a step
+          break;
+        }
         int h = -1;
         // preempted requests rank first (R29); only KV growth preempts
         const bool any_x = grow_on && __any_sync(FULL_MASK, (qb & xb) != 0);
@@ -1093,11 +1136,15 @@ __device__ __forceinline__ void replay_one_ns(const ReplayArgs& a, int64_t r, un
           } else {
             rb |= bit(h);
             fin[h] = n_it + tr.y - he;
-            fmin = min(fmin, fin[h]);
             if (grow_on) {
               emt[h] = 0;
               set_grow(h, hctx + tr.x + he + 1, fin[h]);
             }
+            if (chunk_on) {  // R32: a newcomer takes what is left of the budget
+              prem[h] = (int32_t)(u - min(u, left));
+              if (prem[h] > 0) fin[h] = CT_INF64;
+            }
+            fmin = min(fmin, fin[h]);
           }
         }
         if (loading) {
@@ -1105,7 +1152,13 @@ __device__ __forceinline__ void replay_one_ns(const ReplayArgs& a, int64_t r, un
         } else {
           ++n_run;
           kv_sum += ng;
-          pf += u;
+          if (chunk_on) {
+            const int64_t c = min(u, left);
+            pf += c;
+            left -= u > 0 ? c : 1;  // a fully cached request decodes: one token
+          } else {
+            pf += u;
+          }
         }
         ++admitted;
         __syncwarp();
@@ -1119,6 +1172,12 @@ __device__ __forceinline__ void replay_one_ns(const ReplayArgs& a, int64_t r, un
     }
     // (e) start the next iteration(s) (linear cost model, R16)
     if (n_run > 0) {
+      if (chunk_on && stable) {  // a prompt still in progress makes the next boundary a step
+        bool pending = false;
+#pragma unroll
+        for (int s = 0; s < NS; ++s) pending |= ((rb >> s) & 1u) && prem[lane + 32 * s] > 0;
+        if (__any_sync(FULL_MASK, pending)) stable = false;
+      }
       if (kv_sum != kv_at) {
         kv_at = kv_sum;
         d_cur = ceil_ps_to_us((uint64_t)(E.c0_ps + E.c_kv_ps * bs * kv_sum));
@@ -1230,8 +1289,9 @@ __device__ __forceinline__ void replay_one_ns(const ReplayArgs& a, int64_t r, un
   __syncwarp();
 }
 
-// GROW: KV growth (NEXT-2), always through the shared-memory path (also P <= 32).
-template <int NS, int MINB, bool GROW = false>
+// VLLM: the vLLM engine of NEXT-2 (KV growth, chunked prefill), always through the
+// shared-memory path (also P <= 32).
+template <int NS, int MINB, bool VLLM = false>
 __global__ void __launch_bounds__(128, MINB) replay_kernel(ReplayArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x & 31;
@@ -1242,10 +1302,10 @@ __global__ void __launch_bounds__(128, MINB) replay_kernel(ReplayArgs a) {
     idx = __shfl_sync(FULL_MASK, idx, 0);
     const int64_t r = a.r_begin + (int64_t)idx;
     if (r >= a.r_end) break;
-    if (NS == 1 && !GROW)
+    if (NS == 1 && !VLLM)
       replay_one_w32(a, r, (Stat*)wm, lane);
     else
-      replay_one_ns<NS, GROW>(a, r, wm, lane);
+      replay_one_ns<NS, VLLM>(a, r, wm, lane);
   }
 }
 

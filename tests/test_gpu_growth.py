@@ -105,3 +105,52 @@ def test_bubble_series_reserve_mode(ctx, P):
     s, _, b = check(ctx, tr, sw, eng)
     ok = (s[:, 0] & 0xFFFFFFFF) == 0
     assert np.array_equal(b[ok].sum(axis=1), s[ok, 6])  # per-program series sums to the total
+
+
+# ---- chunked prefill (NEXT-2, R31-R32) ---------------------------------------------------------
+def test_chunked_hand_trace(ctx):
+    tr = traces.tiny([(0, [(6, 2, -1, 0)]), (0, [(3, 1, -1, 0)])])
+    eng = cf.Engine(**{**UNIT.__dict__, "max_batch": 2, "prefill_chunk": 4})
+    s, j, b = check(ctx, tr, cf.Sweep(1, [1 << 20], [100], [cf.PROG_FCFS]), eng)
+    assert list(j[0]) == [12, 12] and list(b[0]) == [0, 5]
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_chunked_random_tiny(ctx, seed):
+    rng = random.Random(3000 + seed)
+    tr = random_growth_set(rng, 300)
+    mb = rng.choice([1, 2, 3])
+    eng = cf.Engine(c0_ps=rng.randint(1, 3 * 10**6), c_pf_ps=rng.choice([0, 5 * 10**5, 10**6]),
+                    c_kv_ps=rng.choice([0, 10**4, 2 * 10**5]), c_h2d_ps=rng.randint(1, 2 * 10**6),
+                    bs=rng.choice([1, 2, 4]), max_batch=mb, dram_blocks=rng.randint(0, 12),
+                    max_iters=rng.choice([10**6, 40]), prefill_chunk=rng.choice([mb, 3, 5]) + mb)
+    est = cf.Estimator(b_us=rng.choice([5, 40]), t_def_us=rng.randint(1, 40), n_min=rng.randint(1, 3))
+    fitted = np.array([[rng.randint(0, 30) for _ in range(3)] for _ in range(2)], np.int64)
+    sw = cf.Sweep(300, [1 << 20, 3 << 19], [12, 20, 40], random_policies(rng, 6), est, fitted)
+    s, _, _ = check(ctx, tr, sw, eng)
+    assert np.mean((s[:, 0] & 0xFFFFFFFF) == 0) > 0.3
+
+
+@pytest.mark.parametrize("P", [1, 7, 32, 33, 100, 200])
+def test_chunked_workloads_all_policies(ctx, P):
+    """Token budgets from tight (prompts span several iterations) to ample."""
+    n_seeds = 4 if P <= 64 else 2
+    tr = traces.generate(n_seeds, P, mix="mix", ctx_cap=8192, stream=300 + P)
+    fitted = np.tile(np.array([[0, 200_000, 3_000_000, 60_000_000]], np.int64), (tr.n_tools, 1))
+    for budget in (512, 2048):
+        eng = cf.Engine(**{**cf.ENGINE_8B.__dict__, "dram_blocks": 40 * P, "prefill_chunk": budget})
+        sw = cf.Sweep(n_seeds, [200_000, 3_000_000], [700, 20 * P + 700], ALL_POLICIES,
+                      fitted=fitted)
+        s, _, _ = check(ctx, tr, sw, eng)
+        assert np.mean((s[:, 0] & 0xFFFFFFFF) == 0) > 0.8
+
+
+def test_chunked_invalid_combinations(ctx):
+    import paper_2511_02230_b200 as ct
+    from paper_2511_02230_b200 import _lib
+    tr = traces.tiny([(0, [(1, 1, -1, 0)])])
+    sw = cf.Sweep(1, [1 << 20], [10], [cf.PROG_FCFS])
+    for bad in ({"prefill_chunk": 4, "max_batch": 8}, {"prefill_chunk": 64, "kv_growth": 1},
+                {"prefill_chunk": -1}):
+        with pytest.raises(_lib.CtError):
+            ct.ct_simulate_batch(ctx, ct.DeviceTrace(tr), sw, cf.Engine(**{**UNIT.__dict__, **bad}))
