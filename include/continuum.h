@@ -261,6 +261,38 @@ int ct_simulate_batch_host(ct_ctx* ctx, const ct_trace_set* host_traces, const c
 int ct_jct_stats(ct_ctx* ctx, const ct_replica_summary* summaries, int64_t n_replicas,
                  int32_t n_cells, ct_cell_stats* out, void* stream);
 
+/* On-device trace synthesis (NEXT-4).  Writes the trace set that
+ * ctgen/synth.py defines (an integer-only generator: SplitMix64 counters, quantile tables with
+ * 16-bit interpolation) for seeds [seed0, seed0 + n_seeds), P programs
+ * each, straight into HBM: no host generation and no host-to-device copy of the traces.
+ * Tables are int64[1025] quantiles at p = i/1024, monotone, values < 2^46. */
+#define CT_SYNTH_TABLE 1025
+typedef struct {
+  int64_t stream;           /* generator stream (key part 0) */
+  int64_t ctx_cap;          /* R24: a program keeps the leading turns whose cumulative
+                               new + decode <= ctx_cap; >= 8192 */
+  int32_t max_turns;        /* 2..1024 */
+  int32_t n_bfcl;           /* BFCL programs per seed (rank of the mix key < n_bfcl) */
+  int32_t n_tools;          /* F, 1..CT_MAX_TOOLS */
+  int32_t reserved;
+  const int64_t* turns_swe; /* [host] [1025] SWE turn-count quantiles */
+  const int64_t* obs;       /* [host] [2][1025] observation tokens (SWE, BFCL) */
+  const int64_t* dec;       /* [host] [2][1025] decode tokens (SWE, BFCL) */
+  const int64_t* dur;       /* [host] [F][1025] tool durations, µs */
+  const int64_t* exp_q20;   /* [host] [1025] unit-rate arrival gaps in Q20 */
+  const uint32_t* tool_cdf; /* [host] [F] cumulative u32 threshold within the tool's class */
+  const int32_t* tool_class;/* [host] [F] 0 = SWE, 1 = BFCL (each class has >= 1 tool) */
+} ct_synth_params;
+
+/* programs [dev] n_seeds * P records (turn0 relative to `turns`); turns [dev] turns_cap records;
+ * *n_turns [host] receives the number written.  Synchronises `stream` (the turn count is
+ * needed on the host).  Errors: CT_EINVAL (bad parameters, P not in [1, CT_MAX_PROGRAMS],
+ * turns_cap too small: *n_turns still receives the count needed, nothing is written to
+ * turns), CT_ENOMEM, CT_ECUDA. */
+int ct_synthesize_traces(ct_ctx* ctx, const ct_synth_params* sp, int64_t seed0, int32_t n_seeds,
+                         int32_t n_programs, ct_program* programs, ct_turn* turns,
+                         int64_t turns_cap, int64_t* n_turns, void* stream);
+
 /* Launch statistics of the last ct_simulate_batch / ct_fit_ttl on this context (bench
  * accounting).  With timing enabled (ct_ctx_set_timing), the library records CUDA events on the
  * caller's stream around the dominant kernel of each call (replay_kernel, fit_hist_kernel);

@@ -3,8 +3,10 @@
 Product path only: C ABI in include/continuum.h, CUDA kernels in csrc/, ctypes binding
 in api.py.  No CPU fallback.
 """
-from .api import (Context, DeviceTrace, ct_fit_ttl, ct_jct_stats, ct_simulate_batch,  # noqa: F401
+from .api import (Context, DeviceTrace, SynthesizedTrace, ct_synthesize_traces,  # noqa: F401
+                  ct_fit_ttl, ct_jct_stats, ct_simulate_batch,  # noqa: F401
                   ct_simulate_batch_host, cost_params, status, SUMMARY_FIELDS)
 
-__all__ = ["Context", "DeviceTrace", "ct_fit_ttl", "ct_jct_stats", "ct_simulate_batch",
+__all__ = ["Context", "DeviceTrace", "SynthesizedTrace", "ct_synthesize_traces", "ct_fit_ttl",
+           "ct_jct_stats", "ct_simulate_batch",
            "ct_simulate_batch_host", "cost_params", "status", "SUMMARY_FIELDS"]

@@ -19,7 +19,13 @@ MAX_J = 64
 # every symbol include/continuum.h declares (checked by tests/test_abi.py)
 EXPORTS = ["ct_version", "ct_last_error", "ct_ctx_create", "ct_ctx_destroy", "ct_fit_ttl",
            "ct_simulate_batch", "ct_simulate_batch_ex", "ct_simulate_batch_host", "ct_jct_stats",
-           "ct_last_launch", "ct_ctx_set_timing"]
+           "ct_last_launch", "ct_ctx_set_timing", "ct_synthesize_traces"]
+
+
+class SynthParams(C.Structure):
+    _fields_ = [("stream", i64), ("ctx_cap", i64), ("max_turns", i32), ("n_bfcl", i32),
+                ("n_tools", i32), ("reserved", i32), ("turns_swe", vp), ("obs", vp), ("dec", vp),
+                ("dur", vp), ("exp_q20", vp), ("tool_cdf", vp), ("tool_class", vp)]
 
 
 class ReplayOutputs(C.Structure):
@@ -99,10 +105,12 @@ def lib() -> C.CDLL:
         L.ct_simulate_batch_host.argtypes = [vp, C.POINTER(TraceSet), C.POINTER(Sweep),
                                              C.POINTER(EngineParams), i64, i64, vp, vp, vp]
         L.ct_jct_stats.argtypes = [vp, vp, i64, i32, vp, vp]
+        L.ct_synthesize_traces.argtypes = [vp, C.POINTER(SynthParams), i64, i32, i32, vp, vp, i64,
+                                           C.POINTER(i64), vp]
         L.ct_last_launch.argtypes = [vp, C.POINTER(LaunchInfo)]
         L.ct_ctx_set_timing.argtypes = [vp, C.c_int]
         for f in ("ct_ctx_create", "ct_ctx_destroy", "ct_fit_ttl", "ct_simulate_batch",
-                  "ct_simulate_batch_ex", "ct_simulate_batch_host", "ct_jct_stats", "ct_last_launch", "ct_ctx_set_timing"):
+                  "ct_simulate_batch_ex", "ct_simulate_batch_host", "ct_synthesize_traces", "ct_jct_stats", "ct_last_launch", "ct_ctx_set_timing"):
             getattr(L, f).restype = C.c_int
         _lib = L
     return _lib

@@ -88,6 +88,38 @@ class DeviceTrace:
                           self.n_seeds, self.n_programs, self.n_tools, 0)
 
 
+class SynthesizedTrace(DeviceTrace):
+    """A trace set written straight into HBM by ct_synthesize_traces (no host copy)."""
+
+    def __init__(self, programs: torch.Tensor, turns: torch.Tensor, n_seeds: int, n_programs: int,
+                 n_tools: int):
+        self.trace = None
+        self.programs, self.turns = programs, turns
+        self.n_seeds, self.n_programs, self.n_tools = n_seeds, n_programs, n_tools
+
+
+def ct_synthesize_traces(ctx: Context, sp, seed0: int, n_seeds: int, n_programs: int,
+                         turns_cap: int | None = None, stream=None) -> SynthesizedTrace:
+    """On-device trace synthesis (NEXT-4) of ctgen.synth's generator; `sp` is a
+    ctgen.synth.SynthParams.  turns_cap defaults to n_seeds * P * max_turns."""
+    dev = torch.device("cuda", ctx.device)
+    tabs = [np.ascontiguousarray(x, dtype=np.int64) for x in (sp.turns_swe, sp.obs, sp.dec, sp.dur, sp.exp)]
+    cdf = np.ascontiguousarray(sp.tool_cdf, dtype=np.uint32)
+    cls = np.ascontiguousarray(sp.tool_class, dtype=np.int32)
+    p = L.SynthParams(int(sp.stream), int(sp.ctx_cap), int(sp.max_turns), int(sp.n_bfcl), len(cdf), 0,
+                      *[t.ctypes.data for t in tabs], cdf.ctypes.data, cls.ctypes.data)
+    if turns_cap is None:
+        turns_cap = n_seeds * n_programs * int(sp.max_turns)
+    progs = torch.empty(16 * n_seeds * n_programs, dtype=torch.uint8, device=dev)
+    turns = torch.empty((max(turns_cap, 1), 4), dtype=torch.int32, device=dev)
+    nt = C.c_int64(0)
+    rc = L.lib().ct_synthesize_traces(ctx.handle, C.byref(p), int(seed0), int(n_seeds),
+                                      int(n_programs), progs.data_ptr(), turns.data_ptr(),
+                                      int(turns_cap), C.byref(nt), _stream_ptr(stream))
+    L.check(rc, "ct_synthesize_traces")
+    return SynthesizedTrace(progs, turns[: nt.value], n_seeds, n_programs, len(cdf))
+
+
 class _SweepStruct:
     """Keeps the host axis arrays alive for the duration of a call."""
 

@@ -31,6 +31,8 @@ struct ct_ctx {
   size_t h_out_cap = 0;
   void* h_jct = nullptr;
   size_t h_jct_cap = 0;
+  void* syn = nullptr;  // synthesis: tables | cdf | class | per-program class | seed totals | blocks
+  size_t syn_cap = 0;
   ct_launch_info last{};
   int fit_occ = 0, fit_occ_smem = -1, fit_occ_v = -1;
   bool timing = false;
@@ -114,7 +116,7 @@ int ct_ctx_create(int device, ct_ctx** out) {
 
 int ct_ctx_destroy(ct_ctx* c) {
   if (!c) return CT_OK;
-  void* ps[] = {c->counter, c->axes, c->fit, c->chunks, c->h_progs, c->h_turns, c->h_out, c->h_jct};
+  void* ps[] = {c->counter, c->axes, c->fit, c->chunks, c->h_progs, c->h_turns, c->h_out, c->h_jct, c->syn};
   for (void* p : ps)
     if (p) cudaFree(p);
   for (auto e : c->ev)
@@ -464,4 +466,74 @@ int ct_jct_stats(ct_ctx* c, const ct_replica_summary* sum, int64_t n, int32_t n_
   return CT_OK;
 }
 
+
+// ---------------------------------------------------------------------------------------------
+int ct_synthesize_traces(ct_ctx* c, const ct_synth_params* sp, int64_t seed0, int32_t n_seeds,
+                         int32_t P, ct_program* programs, ct_turn* turns, int64_t turns_cap,
+                         int64_t* n_turns, void* stream) {
+  if (!c || !sp || !n_turns) return fail(CT_EINVAL, "NULL argument");
+  *n_turns = 0;
+  if (P < 1 || P > CT_MAX_PROGRAMS) return fail(CT_EINVAL, "n_programs %d not in [1, %d]", P, CT_MAX_PROGRAMS);
+  if (n_seeds < 0 || seed0 < 0) return fail(CT_EINVAL, "seed range");
+  const int F = sp->n_tools;
+  if (F < 1 || F > CT_MAX_TOOLS) return fail(CT_EINVAL, "n_tools %d", F);
+  if (sp->ctx_cap < 8192 || sp->ctx_cap >= (1ll << 31)) return fail(CT_EINVAL, "ctx_cap not in [8192, 2^31)");
+  if (sp->max_turns < 2 || sp->max_turns > 1024) return fail(CT_EINVAL, "max_turns not in [2, 1024]");
+  if (sp->n_bfcl < 0 || sp->n_bfcl > P) return fail(CT_EINVAL, "n_bfcl not in [0, P]");
+  if (!sp->turns_swe || !sp->obs || !sp->dec || !sp->dur || !sp->exp_q20 || !sp->tool_cdf || !sp->tool_class)
+    return fail(CT_EINVAL, "NULL table");
+  if (turns_cap < 0 || turns_cap >= (1ll << 31)) return fail(CT_EINVAL, "turns_cap not in [0, 2^31)");
+  const int nt = 6 + F;
+  const int64_t* rows[6] = {sp->turns_swe, sp->obs, sp->obs + CT_SYNTH_TABLE, sp->dec,
+                            sp->dec + CT_SYNTH_TABLE, sp->exp_q20};
+  std::vector<int64_t> tab((size_t)nt * CT_SYNTH_TABLE);
+  for (int r = 0; r < nt; ++r) {
+    const int64_t* src = r < 6 ? rows[r] : sp->dur + (size_t)(r - 6) * CT_SYNTH_TABLE;
+    for (int i = 0; i < CT_SYNTH_TABLE; ++i) {
+      if (src[i] < 0 || src[i] >= (1ll << 46) || (i && src[i] < src[i - 1]))
+        return fail(CT_EINVAL, "table %d is not monotone in [0, 2^46)", r);
+      tab[(size_t)r * CT_SYNTH_TABLE + i] = src[i];
+    }
+  }
+  bool has[2] = {false, false};
+  for (int f = 0; f < F; ++f) {
+    if (sp->tool_class[f] != 0 && sp->tool_class[f] != 1) return fail(CT_EINVAL, "tool_class[%d]", f);
+    has[sp->tool_class[f]] = true;
+  }
+  if (!has[0] || !has[1]) return fail(CT_EINVAL, "each class needs at least one tool");
+  if (n_seeds == 0) return CT_OK;
+  if (!programs || (turns_cap > 0 && !turns)) return fail(CT_EINVAL, "NULL output");
+  const int64_t S = n_seeds, nb = (S + 1023) / 1024;
+  const size_t o_tab = 0, o_cdf = o_tab + 8 * tab.size(), o_cls = o_cdf + 4 * (size_t)F,
+               o_pcls = (o_cls + 4 * (size_t)F + 15) & ~(size_t)15, o_tot = (o_pcls + (size_t)S * P + 15) & ~(size_t)15,
+               o_blk = o_tot + 8 * (size_t)S, bytes = o_blk + 8 * (size_t)(nb + 1);
+  int rc = ensure(&c->syn, &c->syn_cap, bytes);
+  if (rc) return rc;
+  cudaStream_t s = (cudaStream_t)stream;
+  unsigned char* base = (unsigned char*)c->syn;
+  CT_CUDA(cudaMemcpyAsync(base + o_tab, tab.data(), 8 * tab.size(), cudaMemcpyHostToDevice, s));
+  CT_CUDA(cudaMemcpyAsync(base + o_cdf, sp->tool_cdf, 4 * (size_t)F, cudaMemcpyHostToDevice, s));
+  CT_CUDA(cudaMemcpyAsync(base + o_cls, sp->tool_class, 4 * (size_t)F, cudaMemcpyHostToDevice, s));
+  ct::SynthLaunch L;
+  L.sp = sp;
+  L.seed0 = seed0;
+  L.n_seeds = S;
+  L.P = P;
+  L.tab = (const int64_t*)(base + o_tab);
+  L.cdf = (const uint32_t*)(base + o_cdf);
+  L.cls = (const int32_t*)(base + o_cls);
+  L.progs = programs;
+  L.turns = turns;
+  L.turns_cap = turns_cap;
+  L.pcls = base + o_pcls;
+  L.seed_tot = (int64_t*)(base + o_tot);
+  L.blk = (int64_t*)(base + o_blk);
+  int64_t total = 0;
+  cudaError_t e = ct::launch_synth(L, c->sm_count, s, &total);
+  if (e != cudaSuccess) return cuda_fail(e, "synthesis");
+  *n_turns = total;
+  if (total > turns_cap)
+    return fail(CT_EINVAL, "turns_cap %lld < %lld turn records", (long long)turns_cap, (long long)total);
+  return CT_OK;
+}
 }  // extern "C"

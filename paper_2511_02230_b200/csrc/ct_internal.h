@@ -78,6 +78,26 @@ int fit_hist_occupancy(const FitPlan& p);  // resident CTAs per SM
 cudaError_t launch_fit_hist(const FitArgs& a, const FitPlan& p, int grid, cudaStream_t s);
 cudaError_t launch_fit_scan(const ScanArgs& a, cudaStream_t s);
 
+// On-device trace synthesis (synth.cu).  Device scratch is owned by the context.
+struct SynthLaunch {
+  const ct_synth_params* sp;
+  int64_t seed0;
+  int64_t n_seeds;
+  int P;
+  const int64_t* tab;   // [dev] (6 + F) x 1025 quantile tables
+  const uint32_t* cdf;  // [dev] F
+  const int32_t* cls;   // [dev] F
+  ct_program* progs;
+  ct_turn* turns;
+  int64_t turns_cap;
+  uint8_t* pcls;        // [dev] S * P
+  int64_t* seed_tot;    // [dev] S
+  int64_t* blk;         // [dev] ceil(S / 1024) + 1
+};
+// Runs the three passes; synchronises `st` after the count pass and skips the write pass when
+// the total (returned in *total_host) exceeds turns_cap.
+cudaError_t launch_synth(const SynthLaunch& L, int sm_count, cudaStream_t st, int64_t* total_host);
+
 cudaError_t launch_jct_stats(const ct_replica_summary* s, int64_t n, int32_t n_cells,
                              ct_cell_stats* out, cudaStream_t st);
 
