@@ -175,6 +175,7 @@ def cpu_baseline(w, budget_s, n_threads):
             turns += x
     dt = time.time() - t0
     return {"value": turns / dt, "unit": UNIT, "cores": n_threads, "kind": "oracle",
+            "est_turns_per_step": turns / len(reps) * R,
             "sample": "%d of %d replicas (every %d-th), %d replica-turns, %.1f s wall on %d threads"
                       % (len(reps), R, stride, turns, dt, n_threads)}
 
@@ -195,8 +196,11 @@ def run_reference(args):
             last = cb
     v = float(np.mean(vals))
     last["value"] = v
+    # one full step (the whole workload) at the sampled rate: the sample's turns per replica x R
+    ms_full = last.pop("est_turns_per_step") / v * 1e3
     line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True, "scaling": "strong",
+            "warmup": args.warmup, "ms_per_step": ms_full, "higher_is_better": True, "scaling": "strong",
+            "ms_per_step_basis": "whole workload at the sampled rate (each step times a bounded sample)",
             "vs_baseline": None, "dtype": "int64", "data": "synthetic", "impl": "reference",
             "config": {"workload": w.name, "replicas": w.sweep.n_replicas,
                        "programs_per_replica": w.trace.n_programs, "description": w.description},
@@ -392,6 +396,7 @@ def main():
     cb = None
     if world == 1 and not args.no_cpu_baseline:
         cb = cpu_baseline(w, args.cpu_seconds, os.cpu_count() or 1)
+        cb.pop("est_turns_per_step")
 
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t / args.steps * 1e3, "higher_is_better": True,
