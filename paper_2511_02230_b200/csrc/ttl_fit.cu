@@ -54,12 +54,14 @@ static const FitVariant kVariants[] = {{16, false, 16}, {16, true, 16}, {8, fals
                                        {32, false, 0},                    // 17: 15, TMA-staged
                                        {32, false, 0},                    // 18: 16, TMA-staged
                                        {32, false, 0},                    // 19: 15, per-warp TMA
-                                       {32, false, 0}};                   // 20: 16, per-warp TMA
+                                       {32, false, 0},                    // 20: 16, per-warp TMA
+                                       {32, false, 0},                    // 21: cp.async 16 w x 4 x 1 KB
+                                       {32, false, 0}};                   // 22: 21, no 32-bit sums
 constexpr int N_VARIANTS = sizeof kVariants / sizeof kVariants[0];
 static int g_variant = -1;  // default 15: measured best on B200 (DESIGN.md §8 variant table)
 
 static int variant() {
-  static_assert(N_VARIANTS == 21, "variant table / hist_fn mismatch");
+  static_assert(N_VARIANTS == 23, "variant table / hist_fn mismatch");
   if (g_variant < 0) {
     const char* e = getenv("CT_FIT_VARIANT");
     int v = e ? atoi(e) : 15;
@@ -82,11 +84,15 @@ FitPlan fit_plan(int K, int64_t b_us) {
     if (v == 15) v = 16;
     if (v == 17) v = 18;
     if (v == 19) v = 20;
+    if (v == 21) v = 22;
   }
   FitPlan p;
   p.stages = 0;
   const int hist = (K + 1) * 64 * 4;
-  if (v >= 19) {
+  const int aw = 16;  // cp.async variants: warps per CTA, 4 x 1 KB ring per warp
+  if (v >= 21) {
+    if (hist + aw * 4096 > SMEM_LIMIT) v = 8;
+  } else if (v >= 19) {
     if (hist + WTMA_W * WTMA_S * (WTMA_B + 8) > SMEM_LIMIT) v = 8;
   } else if (v >= 17) {
     p.stages = std::min(TMA_MAX_STAGES, (SMEM_LIMIT - hist) / (TMA_STAGE + 16));
@@ -98,8 +104,9 @@ FitPlan fit_plan(int K, int64_t b_us) {
   p.cta = v >= 10;
   p.ranges = v >= 15;
   p.repl = kVariants[v].repl;
-  p.threads = v >= 19 ? 32 * WTMA_W : v >= 17 ? TMA_THREADS : v >= 10 ? 256 : FIT_THREADS;
-  p.smem = v >= 19   ? hist + WTMA_W * WTMA_S * (WTMA_B + 8)
+  p.threads = v >= 21 ? 32 * aw : v >= 19 ? 32 * WTMA_W : v >= 17 ? TMA_THREADS : v >= 10 ? 256 : FIT_THREADS;
+  p.smem = v >= 21   ? hist + aw * 4096
+           : v >= 19 ? hist + WTMA_W * WTMA_S * (WTMA_B + 8)
            : v >= 17 ? hist + p.stages * (TMA_STAGE + 16)
                      : v >= 10 ? hist : FIT_WARPS * 4 * smem_words(K, kVariants[v]);
   return p;
@@ -772,6 +779,134 @@ __global__ void __launch_bounds__(32 * WW, 1) fit_hist_wtma_kernel(FitArgs a) {
   }
 }
 
+// cp.async variant: the Ampere-style multistage pipeline.  Each lane copies its own 16-B pieces
+// of the warp's chunks global -> shared with cp.async.cg (no register staging, so 32 warps fit
+// in 64 registers), AD stages deep, and later reads back only what it copied itself: no warp
+// or CTA synchronisation in the stream, only per-thread cp.async.wait_group.  Chunks of
+// 32 AU int4 are dealt round-robin to the AW warps; histogram and pieces as fit_hist_seg_kernel.
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+template <bool IDENT, bool FAST32, int AW, int AD, int AU>
+__global__ void __launch_bounds__(32 * AW, 1) fit_hist_async_kernel(FitArgs a) {
+  extern __shared__ __align__(128) uint32_t hsm[];
+  __shared__ unsigned long long red[AW][3];
+  const int K = a.K;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int words = (K + 1) * 64;
+  const uint32_t ring = (uint32_t)__cvta_generic_to_shared(hsm + words) + warp * (AD * AU * 512) + 16 * lane;
+  const Lane L = cta_lane(a, hsm);
+  const int64_t s0 = a.tool_off[0], s1e = a.tool_off[a.F];
+  const int64_t per = (s1e - s0 + gridDim.x - 1) / gridDim.x;
+  auto bnd = [&](int64_t b) -> int64_t {
+    if (b == 0) return s0;
+    if (b >= (int64_t)gridDim.x) return s1e;
+    return min(s1e, max(s0, (s0 + b * per) & ~(int64_t)3));
+  };
+  int64_t lo = bnd(blockIdx.x);
+  const int64_t hi = bnd((int64_t)blockIdx.x + 1);
+  int tool = 0;
+  const uint32_t base = L.cnt_base;
+  while (lo < hi) {
+    while (a.tool_off[tool + 1] <= lo) ++tool;
+    const int64_t beg = lo;
+    const int64_t end = min(min(hi, a.tool_off[tool + 1]), lo + a.ch);
+    lo = end;
+    int64_t va = (beg + 3) & ~(int64_t)3;
+    if (va > end) va = end;
+    const int64_t vb = va + ((end - va) & ~(int64_t)3);
+    const int4* v = (const int4*)(a.dur + va);
+    const int64_t n4 = (vb - va) >> 2;
+    const int64_t nch = (n4 + 32 * AU - 1) / (32 * AU);
+    auto issue = [&](int64_t c, int slot) {
+      if (c < nch) {
+#pragma unroll
+        for (int u = 0; u < AU; ++u) {
+          const int64_t idx = c * (32 * AU) + 32 * u + lane;
+          if (idx < n4) cp_async16(ring + slot * (AU * 512) + u * 512, v + idx);
+        }
+      }
+      cp_commit();  // one group per stage, empty or not: the wait counts stay uniform
+    };
+#pragma unroll
+    for (int st = 0; st < AD; ++st) issue(warp + (int64_t)AW * st, st);
+    for (int i = tid; i < words; i += 32 * AW) hsm[i] = 0;
+    __syncthreads();
+    uint64_t s1 = 0, s2 = 0, q1 = 0, q2 = 0, q3 = 0;
+    if (tid < 32) {  // scalar head and tail (< 4 samples each)
+      if (beg + lane < va) sample<IDENT, 64, false>(L, __ldg(&a.dur[beg + lane]), s1, s2);
+      if (vb + lane < end) sample<IDENT, 64, false>(L, __ldg(&a.dur[vb + lane]), s1, s2);
+    }
+    int slot = 0;
+    for (int64_t c = warp; c < nch; c += AW) {
+      cp_wait<AD - 1>();
+      uint32_t s1w = 0;
+#pragma unroll
+      for (int u = 0; u < AU; ++u) {
+        const int64_t idx = c * (32 * AU) + 32 * u + lane;
+        if (idx < n4) {
+          int4 x;
+          asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];"
+                       : "=r"(x.x), "=r"(x.y), "=r"(x.z), "=r"(x.w)
+                       : "r"(ring + slot * (AU * 512) + u * 512));
+          if (FAST32) {
+            sample_cta<IDENT>(L, base, x.x, s1w, s2);
+            sample_cta<IDENT>(L, base, x.y, s1w, q1);
+            sample_cta<IDENT>(L, base, x.z, s1w, q2);
+            sample_cta<IDENT>(L, base, x.w, s1w, q3);
+          } else {
+            sample_cta<IDENT>(L, base, x.x, s1, s2);
+            sample_cta<IDENT>(L, base, x.y, s1, q1);
+            sample_cta<IDENT>(L, base, x.z, s1, q2);
+            sample_cta<IDENT>(L, base, x.w, s1, q3);
+          }
+        }
+      }
+      if (FAST32) s1 += s1w;  // 4 AU samples per lane per chunk: < 2^29 when b < 2^26
+      issue(c + (int64_t)AW * AD, slot);  // this lane's slot is free again: it read it itself
+      if (++slot == AD) slot = 0;
+    }
+    cp_wait<0>();
+    s2 += q1 + q2 + q3;
+    const uint64_t w1 = warp_sum_u64(s1), w2 = warp_sum_u64(s2 & 0xffffffffull),
+                   w3 = warp_sum_u64(s2 >> 32);
+    if (lane == 0) { red[warp][0] = w1; red[warp][1] = w2; red[warp][2] = w3; }
+    __syncthreads();
+    if (tid < 6) {  // tid 0-2: the tool's row, 3-5: the pooled row F
+      const int q = tid % 3;
+      uint64_t sum = 0;
+      for (int w = 0; w < AW; ++w) sum += red[w][q];
+      unsigned long long* st = a.stat + (tid < 3 ? tool : a.F) * 6;
+      if (q == 0) atomicAdd(st, (unsigned long long)(end - beg));
+      if (sum) atomicAdd(st + 1 + q, (unsigned long long)sum);
+    }
+    for (int b = tid; b <= K; b += 32 * AW) {  // merge the 32 lane replicas of every bucket
+      const uint4* pc = (const uint4*)(hsm + b * 64);
+      uint64_t cn = 0, rr = 0;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const uint4 x = pc[q], y = pc[8 + q];
+        cn += (uint64_t)x.x + x.y + x.z + x.w;
+        rr += (uint64_t)y.x + y.y + y.z + y.w;
+      }
+      if (cn) {
+        const uint64_t sm = b < K ? (uint64_t)b * L.step * cn - rr : 0;
+#pragma unroll
+        for (int row2 = 0; row2 < 2; ++row2) {
+          const int64_t o = (int64_t)(row2 ? a.F : tool) * (K + 1) + b;
+          atomicAdd(&a.hcnt[o], (unsigned long long)cn);
+          if (sm) atomicAdd(&a.hsum[o], (unsigned long long)sm);
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
 template <bool IDENT>
 static void* hist_fn(int v) {
   switch (v) {
@@ -795,7 +930,9 @@ static void* hist_fn(int v) {
     case 17: return (void*)fit_hist_tma_kernel<IDENT, true>;      // TMA-staged ranges
     case 18: return (void*)fit_hist_tma_kernel<IDENT, false>;
     case 19: return (void*)fit_hist_wtma_kernel<IDENT, true, WTMA_W, WTMA_B, WTMA_S>;  // per-warp TMA
-    default: return (void*)fit_hist_wtma_kernel<IDENT, false, WTMA_W, WTMA_B, WTMA_S>;
+    case 20: return (void*)fit_hist_wtma_kernel<IDENT, false, WTMA_W, WTMA_B, WTMA_S>;
+    case 21: return (void*)fit_hist_async_kernel<IDENT, true, 16, 4, 2>;  // cp.async pipeline
+    default: return (void*)fit_hist_async_kernel<IDENT, false, 16, 4, 2>;
   }
 }
 
