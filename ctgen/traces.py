@@ -315,3 +315,47 @@ def turn_scaling(tr: TraceSet, k: int) -> TraceSet:
                 rows.append((new, dec, tool, dur))
     turns = np.array(rows, dtype=np.int32).reshape(-1, 4)
     return TraceSet(progs, turns, tr.n_seeds, tr.n_programs, tr.n_tools, tr.pclass)
+
+
+def to_jsonl(tr: TraceSet, path: str, seed: int = 0, messages: bool = False) -> None:
+    """Write seed `seed` of a trace set as a JSONL trace (one program per line, SPEC.md:144-152
+    field names) for the host ingest (NEXT-4).  Times are written as exact decimal seconds of
+    the integer µs (arrival = arr_q µs, i.e. the trace's arrivals at gap_us = 2^20).  With
+    `messages`, non-final turns carry a synthetic raw model output instead of tool_name, in
+    the App. A formats, rotating over the turns."""
+    import json
+
+    def sec(us: int) -> str:
+        return "%d.%06d" % divmod(int(us), 1_000_000)
+
+    P = tr.n_programs
+    with open(path, "w") as fh:
+        for i in range(seed * P, (seed + 1) * P):
+            t0, nt = int(tr.programs["turn0"][i]), int(tr.programs["nturns"][i])
+            turns = []
+            for j in range(nt):
+                new, dec, tool, dur = (int(x) for x in tr.turns[t0 + j])
+                t = {"new_prompt_tokens": new, "decode_tokens": dec}
+                if j < nt - 1:
+                    name = TOOLS[tool][0]
+                    if messages:
+                        t["message"] = _message(name, i + j)
+                    else:
+                        t["tool_name"] = name
+                    t["tool_duration_s"] = "@" + sec(dur) + "@"
+                turns.append(t)
+            rec = {"program_id": "p%d" % i, "arrival_time_s": "@" + sec(tr.programs["arr_q"][i]) + "@",
+                   "turns": turns}
+            # numbers as exact decimal text (json.dumps would print a float)
+            fh.write(json.dumps(rec).replace('"@', "").replace('@"', "") + "\n")
+
+
+def _message(name: str, k: int) -> str:
+    forms = [
+        "```bash\n%s -la . && echo done\n```" % name,
+        '{"id": "fc_%d", "call_id": "call_%d", "type": "function_call", "name": "%s", '
+        '"arguments": {"q": "x"}}' % (k, k, name),
+        '{"name": "%s", "arguments": {"q": "x"}}' % name,
+        "%s(query=\"x\", n=3)" % name,
+    ]
+    return forms[k % len(forms)]

@@ -293,6 +293,59 @@ int ct_synthesize_traces(ct_ctx* ctx, const ct_synth_params* sp, int64_t seed0, 
                          int32_t n_programs, ct_program* programs, ct_turn* turns,
                          int64_t turns_cap, int64_t* n_turns, void* stream);
 
+/* ---- host-side trace ingest (NEXT-4) ----------------------------------
+ * These two calls run on the host only (no CUDA call, no context): they turn recorded agent
+ * traces into the ct_program / ct_turn records the replay reads.  DESIGN.md R33-R35. */
+
+/* tool-call formats of ct_parse_tool_name (§5.2 and App. A) */
+#define CT_TOOLFMT_AUTO 0       /* detect: JSON (OPENAI / NAME / TERMINAL by its keys), a ```bash
+                                   fence, a <tool_call> wrapper, a pythonic call; else no call */
+#define CT_TOOLFMT_OPENAI 1     /* JSON block or array of blocks; the first block whose "type"
+                                   names a function/tool call gives "name" (or "function"."name")
+                                    */
+#define CT_TOOLFMT_NAME 2       /* Qwen-3 style {"name": f, "arguments": {...}} (App. A) */
+#define CT_TOOLFMT_PYTHONIC 3   /* Llama-3 style f(p1=v1, ...) or [f(...), ...] (App. A) */
+#define CT_TOOLFMT_BASH 4       /* bash command (the ```bash block if one is present, else the
+                                   whole message): split on && and ||, first whitespace token
+                                   of the first sub-command (App. A) */
+#define CT_TOOLFMT_TERMINAL 5   /* Terminal-Bench {"commands": [{"keystrokes": ...}, ...]}: the
+                                   first command's keystrokes parsed as BASH (App. A) */
+
+/* Extract the tool name of one model output message.  msg [host] is `len` bytes of UTF-8 (need
+ * not be NUL-terminated).  On CT_OK, *name_len = length of the name written to name [host]
+ * (NUL-terminated, at most name_cap - 1 bytes) or 0 when the message holds no tool call, and
+ * *malformed = 1 when a structured block (JSON) could not be parsed or lacks its name (the name
+ * is then absent; SPEC.md:164 counts these as parse warnings), else 0.
+ * Errors: CT_EINVAL (NULL pointers, len < 0, unknown format, name longer than name_cap - 1). */
+int ct_parse_tool_name(const char* msg, int64_t len, int32_t format, char* name, int32_t name_cap,
+                       int32_t* name_len, int32_t* malformed);
+
+/* Load a JSONL trace: one program per line,
+ *   {"program_id": str|int, "arrival_time_s": num, "turns": [turn, ...]}
+ *   turn = {"new_prompt_tokens": int >= 0, "decode_tokens": int >= 1,
+ *           "tool_name": str, "tool_duration_s": num >= 0}   (tool fields on non-final turns)
+ * where a non-final turn may give "message" (the raw model output, parsed with
+ * ct_parse_tool_name(format)) instead of "tool_name".  Blank lines are skipped; unknown keys are
+ * ignored.  Validation: turns non-empty; decode >= 1; tool fields present on
+ * every non-final turn and absent on the final one; cumulative new + decode <= ctx_window when
+ * ctx_window > 0.  Times are parsed from their decimal text exactly and rounded half away from
+ * zero to integer µs; tool durations below 1 µs become 1 µs (R25).  Programs are sorted by
+ * arrival (stable; file order on ties) and written as one seed with arr_q = arrival µs, so a
+ * sweep with gap_us = 2^20 replays the recorded arrivals and any other gap scales them (R34).
+ * Tool ids: the first n_known names of `tool_names` keep their ids; other names are appended
+ * in order of first use (after sorting).  tool_names [host] is a table of 64-byte NUL-padded
+ * entries with room for CT_MAX_TOOLS; names must be 1..63 bytes.
+ * Two-call use: with programs == NULL or turns == NULL nothing but the counts is written.
+ * Outputs: counts[0] = programs, counts[1] = turns, counts[2] = tools (known + new),
+ *          counts[3] = malformed tool-call messages (warnings), counts[4] = failing line (1-based,
+ *          0 on success).
+ * Errors: CT_EINVAL (unreadable file, JSON or schema violation, named with its line and field in
+ * ct_last_error; more than CT_MAX_TOOLS tools; capacity too small: counts still filled),
+ * CT_ENOMEM. */
+int ct_load_trace_jsonl(const char* path, int32_t format, int64_t ctx_window, char* tool_names,
+                        int32_t n_known, ct_program* programs, int64_t programs_cap,
+                        ct_turn* turns, int64_t turns_cap, int64_t* counts);
+
 /* Launch statistics of the last ct_simulate_batch / ct_fit_ttl on this context (bench
  * accounting).  With timing enabled (ct_ctx_set_timing), the library records CUDA events on the
  * caller's stream around the dominant kernel of each call (replay_kernel, fit_hist_kernel);

@@ -19,7 +19,8 @@ MAX_J = 64
 # every symbol include/continuum.h declares (checked by tests/test_abi.py)
 EXPORTS = ["ct_version", "ct_last_error", "ct_ctx_create", "ct_ctx_destroy", "ct_fit_ttl",
            "ct_simulate_batch", "ct_simulate_batch_ex", "ct_simulate_batch_host", "ct_jct_stats",
-           "ct_last_launch", "ct_ctx_set_timing", "ct_synthesize_traces"]
+           "ct_last_launch", "ct_ctx_set_timing", "ct_synthesize_traces", "ct_parse_tool_name",
+           "ct_load_trace_jsonl"]
 
 
 class SynthParams(C.Structure):
@@ -109,8 +110,13 @@ def lib() -> C.CDLL:
                                            C.POINTER(i64), vp]
         L.ct_last_launch.argtypes = [vp, C.POINTER(LaunchInfo)]
         L.ct_ctx_set_timing.argtypes = [vp, C.c_int]
+        L.ct_parse_tool_name.argtypes = [C.c_char_p, i64, i32, C.c_char_p, i32, C.POINTER(i32),
+                                         C.POINTER(i32)]
+        L.ct_load_trace_jsonl.argtypes = [C.c_char_p, i32, i64, vp, i32, vp, i64, vp, i64,
+                                          C.POINTER(i64)]
         for f in ("ct_ctx_create", "ct_ctx_destroy", "ct_fit_ttl", "ct_simulate_batch",
-                  "ct_simulate_batch_ex", "ct_simulate_batch_host", "ct_synthesize_traces", "ct_jct_stats", "ct_last_launch", "ct_ctx_set_timing"):
+                  "ct_simulate_batch_ex", "ct_simulate_batch_host", "ct_synthesize_traces", "ct_jct_stats", "ct_last_launch", "ct_ctx_set_timing",
+                  "ct_parse_tool_name", "ct_load_trace_jsonl"):
             getattr(L, f).restype = C.c_int
         _lib = L
     return _lib

@@ -273,3 +273,51 @@ def ct_jct_stats(ctx: Context, summary: torch.Tensor, n_cells: int, out: torch.T
 
 def status(summary: torch.Tensor | np.ndarray):
     return summary[:, 0] & 0xFFFFFFFF
+
+
+# ---- host-side trace ingest (NEXT-4; csrc/ingest.cpp) -------------------------------------------
+TOOLFMT = {"auto": 0, "openai": 1, "name": 2, "pythonic": 3, "bash": 4, "terminal": 5}
+
+
+def ct_parse_tool_name(msg, fmt: str | int = "auto") -> tuple[str | None, bool]:
+    """Tool name of one model output message (App. A): (name or None,
+    malformed)."""
+    b = msg.encode() if isinstance(msg, str) else bytes(msg)
+    f = TOOLFMT[fmt] if isinstance(fmt, str) else int(fmt)
+    cap = len(b) + 1
+    buf = C.create_string_buffer(cap)
+    n, bad = C.c_int32(0), C.c_int32(0)
+    L.check(L.lib().ct_parse_tool_name(b, len(b), f, buf, cap, C.byref(n), C.byref(bad)),
+            "ct_parse_tool_name")
+    return (buf.raw[: n.value].decode("utf-8", "surrogateescape") if n.value else None,
+            bool(bad.value))
+
+
+def ct_load_trace_jsonl(path: str, fmt: str | int = "auto", ctx_window: int = 0,
+                        known_tools=()):
+    """Load a JSONL agent trace (one program per line) into one seed of replay records.
+
+    Returns (ctgen TraceSet with n_seeds = 1, tool names by id, malformed-message count).
+    arr_q holds the recorded arrival in µs: replay it with gap_us = 2^20 for the recorded
+    arrival process (any other gap rescales it)."""
+    from ctgen.traces import PROG_DTYPE, TraceSet
+    f = TOOLFMT[fmt] if isinstance(fmt, str) else int(fmt)
+    names = C.create_string_buffer(64 * 64)
+    for i, nm in enumerate(known_tools):
+        e = nm.encode()
+        names[64 * i: 64 * i + len(e)] = e
+    counts = (C.c_int64 * 5)()
+    p = path.encode()
+    lib = L.lib()
+    L.check(lib.ct_load_trace_jsonl(p, f, int(ctx_window), names, len(known_tools), None, 0, None,
+                                    0, counts), "ct_load_trace_jsonl")
+    n_p, n_t = int(counts[0]), int(counts[1])
+    progs = np.zeros(n_p, dtype=PROG_DTYPE)
+    turns = np.zeros((n_t, 4), dtype=np.int32)
+    L.check(lib.ct_load_trace_jsonl(p, f, int(ctx_window), names, len(known_tools),
+                                    progs.ctypes.data, n_p, turns.ctypes.data, n_t, counts),
+            "ct_load_trace_jsonl")
+    n_f = int(counts[2])
+    tools = [names.raw[64 * i: 64 * (i + 1)].split(b"\0", 1)[0].decode() for i in range(n_f)]
+    tr = TraceSet(progs, turns, 1, n_p, max(n_f, 1), np.zeros(n_p, np.uint8))
+    return tr, tools, int(counts[3])

@@ -87,6 +87,8 @@ typedef __int128 i128;
 
 }  // namespace
 
+void ct::set_last_error(const char* msg) { g_err = msg; }
+
 extern "C" {
 
 int ct_version(void) { return CT_ABI_VERSION; }

@@ -98,6 +98,9 @@ struct SynthLaunch {
 // the total (returned in *total_host) exceeds turns_cap.
 cudaError_t launch_synth(const SynthLaunch& L, int sm_count, cudaStream_t st, int64_t* total_host);
 
+// Sets the thread-local message ct_last_error() returns (api.cu); host code in other files.
+void set_last_error(const char* msg);
+
 cudaError_t launch_jct_stats(const ct_replica_summary* s, int64_t n, int32_t n_cells,
                              ct_cell_stats* out, cudaStream_t st);
 
