@@ -253,15 +253,18 @@ int ct_simulate_batch_ex(ct_ctx* c, const ct_trace_set* tr, const ct_sweep* sw,
                                       (unsigned __int128)(uint64_t)E.bs);
   const int ns = (P + 31) / 32;  // slots per lane
   const bool growth = E.kv_growth != 0 || E.prefill_chunk > 0;  // the vLLM-engine kernels
+  int n_fast = 0;
+  for (size_t i = 0; i < n_pol; ++i) n_fast += ct::fast_policy(sw->policies[i], E) ? 1 : 0;
+  const int mode = (ns != 1 || growth || n_fast == 0) ? 0 : (n_fast == (int)n_pol ? 1 : 2);
   const int wpb = 4;
   a.smem_per_warp = ct::replay_smem_per_warp(ns, F, growth);
   const int smem = a.smem_per_warp * wpb;
-  int occ = ct::replay_occupancy(ns, growth, wpb, smem);
+  int occ = ct::replay_occupancy(ns, growth, mode, wpb, smem);
   if (occ < 1) return fail(CT_ECUDA, "replay kernel cannot be resident (smem %d)", smem);
   const int64_t need_blocks = (re - rb + wpb - 1) / wpb;
   const int grid = (int)std::min<int64_t>((int64_t)c->sm_count * occ, need_blocks);
   if (c->timing) CT_CUDA(cudaEventRecord(c->ev[0], s));
-  cudaError_t e = ct::launch_replay(a, ns, growth, wpb, grid, s);
+  cudaError_t e = ct::launch_replay(a, ns, growth, mode, wpb, grid, s);
   if (e != cudaSuccess) return cuda_fail(e, "replay launch");
   if (c->timing) CT_CUDA(cudaEventRecord(c->ev[1], s));
   c->replay_timed = c->timing;

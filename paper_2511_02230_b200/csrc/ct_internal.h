@@ -28,14 +28,23 @@ struct ReplayArgs {
   uint64_t bs_magic;  // ceil(2^64 / bs) (0 when bs == 1)
 };
 
+// The TTL-grid policy class, for which the P <= 32 replay has a specialised path: program
+// FCFS; EVICT, or FIXED with T_thresh = CT_ALWAYS (pin for t_pin); no DRAM tier; eager expiry
+// and the paper's victim rule (flags 0).
+inline __host__ __device__ bool fast_policy(const ct_policy& p, const ct_engine_params& E) {
+  return p.priority == CT_PRIO_PROG_FCFS && p.flags == 0 && (p.dram == 0 || E.dram_blocks <= 0) &&
+         (p.pause == CT_PAUSE_EVICT || (p.pause == CT_PAUSE_FIXED && p.t_thresh_us == CT_ALWAYS));
+}
+
 // Bytes of shared memory one replica (one warp) needs for `ns` slots per lane and F tools.
 // KV growth (NEXT-2) always runs the shared-memory path, also for P <= 32.
 int replay_smem_per_warp(int ns, int F, bool growth);
 // Launch the persistent replay kernel; returns the cudaError of the launch.
-cudaError_t launch_replay(const ReplayArgs& a, int ns, bool growth, int warps_per_block, int grid,
-                          cudaStream_t s);
+// mode (ns == 1, default engine): 0 generic, 1 all policies fast_policy(), 2 mixed.
+cudaError_t launch_replay(const ReplayArgs& a, int ns, bool growth, int mode, int warps_per_block,
+                          int grid, cudaStream_t s);
 // Max resident blocks per SM for the given configuration.
-int replay_occupancy(int ns, bool growth, int warps_per_block, int smem_per_block);
+int replay_occupancy(int ns, bool growth, int mode, int warps_per_block, int smem_per_block);
 
 struct FitArgs {
   const int32_t* dur;

@@ -61,6 +61,9 @@ __device__ __forceinline__ int64_t shfl64(int64_t v, int src) {
   return (int64_t)__shfl_sync(FULL_MASK, (unsigned long long)v, src);
 }
 
+// FAST: the policy is in the TTL-grid class (fast_policy(), ct_internal.h), so the estimator,
+// DRAM, request-FCFS / PLAS and the other pause actions compile away.
+template <bool FAST>
 __device__ __forceinline__ void replay_one_w32(const ReplayArgs& a, int64_t r, Stat* stats,
                                                int lane) {
   const int P = a.P, F = a.F;
@@ -70,7 +73,9 @@ __device__ __forceinline__ void replay_one_w32(const ReplayArgs& a, int64_t r, S
   const int rate_i = (int)((r / (npol * nkv)) % nrate);
   const int64_t seed = r / (npol * nkv * nrate);
   const ct_policy* polp = a.pols + pol_i;  // t_pin / t_thresh re-read from L1 when needed
-  const int prio = polp->priority, pause = polp->pause, pflags = polp->flags;
+  const int prio = FAST ? CT_PRIO_PROG_FCFS : polp->priority;
+  const int pause = FAST ? CT_PAUSE_FIXED : polp->pause;
+  const int pflags = FAST ? 0 : polp->flags;
   const int64_t gap = a.gap[rate_i];
   const ct_engine_params& E = a.eng;
   const ct_estimator_params& est = a.est;
@@ -82,10 +87,10 @@ __device__ __forceinline__ void replay_one_w32(const ReplayArgs& a, int64_t r, S
   bsm.ident = bs == 1 ? 1u : 0u;
   const bool eager = (pflags & CT_FLAG_STEP_EXPIRY) == 0;
   const bool vany = (pflags & CT_FLAG_VICTIMS_ANY) != 0;
-  const bool dram_on = polp->dram != 0 && E.dram_blocks > 0;
-  const bool need_stats = pause == CT_PAUSE_PAPER || pause == CT_PAUSE_INFERCEPT ||
-                          (pause == CT_PAUSE_FIXED && polp->t_thresh_us != CT_ALWAYS);
-  const bool plas = prio == CT_PRIO_PLAS;
+  const bool dram_on = !FAST && polp->dram != 0 && E.dram_blocks > 0;
+  const bool need_stats = !FAST && (pause == CT_PAUSE_PAPER || pause == CT_PAUSE_INFERCEPT ||
+                                    (pause == CT_PAUSE_FIXED && polp->t_thresh_us != CT_ALWAYS));
+  const bool plas = !FAST && prio == CT_PRIO_PLAS;
   if (need_stats) {
     for (int i = lane; i < 4 * (F + 1); i += 32) ((int64_t*)stats)[i] = 0;
     __syncwarp();
@@ -263,6 +268,10 @@ __device__ __forceinline__ void replay_one_w32(const ReplayArgs& a, int64_t r, S
           switch (pause) {
             case CT_PAUSE_FIXED:
             case CT_PAUSE_PAPER: {
+              if (FAST) {  // FIXED with CT_ALWAYS pins for t_pin; EVICT never pins
+                ttl = polp->pause == CT_PAUSE_FIXED ? polp->t_pin_us : 0;
+                break;
+              }
               const Stat sg = stats[F], sf = stats[ptool];
               ttl = pause == CT_PAUSE_PAPER
                         ? calc_ttl(sg, sf, est, D, turns_done)
@@ -1291,7 +1300,9 @@ __device__ __forceinline__ void replay_one_ns(const ReplayArgs& a, int64_t r, un
 
 // VLLM: the vLLM engine of NEXT-2 (KV growth, chunked prefill), always through the
 // shared-memory path (also P <= 32).
-template <int NS, int MINB, bool VLLM = false>
+// MODE (P <= 32 default engine): 0 every policy generic, 1 every policy in the TTL-grid class
+// (the specialised replay only: 3x smaller code, no register spills), 2 mixed (per replica).
+template <int NS, int MINB, bool VLLM = false, int MODE = 0>
 __global__ void __launch_bounds__(128, MINB) replay_kernel(ReplayArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x & 31;
@@ -1302,9 +1313,12 @@ __global__ void __launch_bounds__(128, MINB) replay_kernel(ReplayArgs a) {
     idx = __shfl_sync(FULL_MASK, idx, 0);
     const int64_t r = a.r_begin + (int64_t)idx;
     if (r >= a.r_end) break;
-    if (NS == 1 && !VLLM)
-      replay_one_w32(a, r, (Stat*)wm, lane);
-    else
+    if (NS == 1 && !VLLM) {
+      if (MODE == 1 || (MODE == 2 && fast_policy(a.pols[(int)(r % a.n_pol)], a.eng)))
+        replay_one_w32<true>(a, r, (Stat*)wm, lane);
+      else
+        replay_one_w32<false>(a, r, (Stat*)wm, lane);
+    } else
       replay_one_ns<NS, VLLM>(a, r, wm, lane);
   }
 }
@@ -1320,7 +1334,7 @@ static int minb() {
   return g_minb;
 }
 
-static void* pick(int ns, bool growth) {
+static void* pick(int ns, bool growth, int mode) {
   if (growth) {
     switch (ns) {
       case 1: return (void*)replay_kernel<1, 1, true>;
@@ -1336,6 +1350,14 @@ static void* pick(int ns, bool growth) {
   }
   switch (ns) {
     case 1:
+      if (mode == 1) {
+        switch (minb()) {
+          case 10: return (void*)replay_kernel<1, 10, false, 1>;
+          case 12: return (void*)replay_kernel<1, 12, false, 1>;
+          default: return (void*)replay_kernel<1, 8, false, 1>;
+        }
+      }
+      if (mode == 2) return (void*)replay_kernel<1, 8, false, 2>;
       switch (minb()) {
         case 6: return (void*)replay_kernel<1, 6>;
         case 10: return (void*)replay_kernel<1, 10>;
@@ -1353,8 +1375,8 @@ static void* pick(int ns, bool growth) {
   return nullptr;
 }
 
-int replay_occupancy(int ns, bool growth, int warps_per_block, int smem_per_block) {
-  void* k = pick(ns, growth);
+int replay_occupancy(int ns, bool growth, int mode, int warps_per_block, int smem_per_block) {
+  void* k = pick(ns, growth, mode);
   if (!k) return 0;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_per_block);
   int nb = 0;
@@ -1362,9 +1384,9 @@ int replay_occupancy(int ns, bool growth, int warps_per_block, int smem_per_bloc
   return nb;
 }
 
-cudaError_t launch_replay(const ReplayArgs& a, int ns, bool growth, int warps_per_block, int grid,
-                          cudaStream_t s) {
-  void* k = pick(ns, growth);
+cudaError_t launch_replay(const ReplayArgs& a, int ns, bool growth, int mode, int warps_per_block,
+                          int grid, cudaStream_t s) {
+  void* k = pick(ns, growth, mode);
   if (!k) return cudaErrorInvalidValue;
   int smem = a.smem_per_warp * warps_per_block;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
