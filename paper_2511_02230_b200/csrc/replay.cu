@@ -52,6 +52,24 @@ __device__ __forceinline__ int64_t macro_iters(int64_t m, int64_t gap, int64_t d
   return 1 + c;
 }
 
+// 32-bit variant for d < 2^31 µs (host-checked for the FAST kernels): m - 1 < 2^31 (m is at
+// most a request's decode tokens), so every product is one 32 x 32 -> 64-bit multiply.
+__device__ __forceinline__ int64_t macro_iters32(int64_t m, int64_t gap, int64_t dur1, uint32_t d,
+                                                 float rd) {
+  if (gap >= CT_INF64 / 2) return m;
+  const int64_t g = gap - dur1;
+  if (g <= 0) return 1;
+  if ((uint64_t)g > (uint64_t)(uint32_t)(m - 1) * d) return m;
+  uint32_t c = (uint32_t)((float)g * rd);
+  while ((uint64_t)c * d < (uint64_t)g) ++c;
+  while (c > 0 && (uint64_t)(c - 1) * d >= (uint64_t)g) --c;
+  return 1 + (int64_t)c;
+}
+
+enum : int {  // summary counter index (FAST path: the lane that holds it)
+  ACC_BUBBLE = 0, ACC_PREFILL, ACC_RECOMP, ACC_BUSY, ACC_HITS, ACC_EXP, ACC_VICT, ACC_RELOAD
+};
+
 struct Acc {  // per-replica summary counters (P <= 32 path)
   int64_t bubble, prefill, recomp, busy;
   int32_t hits, exp, vict, reload;
@@ -131,13 +149,23 @@ __device__ __forceinline__ void replay_one_w32(const ReplayArgs& a, int64_t r, S
   int32_t kv_sum = 0;
   int64_t pf = 0;
   int status = CT_R_OK;
-  // summary counters live in shared memory (lane 0 updates them) to keep registers for occupancy
+  // summary counters: generic path in shared memory (lane 0 updates them) to keep registers for
+  // occupancy; FAST path one counter per lane in a register (lane k holds counter k of ACC_*)
   Acc* acc = (Acc*)(stats + F + 1);
-  if (lane == 0) *acc = Acc{0, 0, 0, 0, 0, 0, 0, 0};
+  if (!FAST && lane == 0) *acc = Acc{0, 0, 0, 0, 0, 0, 0, 0};
+  int64_t accv = 0;
+#define ACC_ADD(field, k, v)                     \
+  do {                                           \
+    if (FAST) {                                  \
+      if (lane == (k)) accv += (int64_t)(v);     \
+    } else if (lane == 0) {                      \
+      acc->field += (v);                         \
+    }                                            \
+  } while (0)
   // duration of a no-prefill iteration for the current batch (depends on kv_sum only) and its
   // reciprocal for the macro-step division, recomputed only when kv_sum changes
   int32_t kv_at = -1;
-  int64_t d_cur = 0;
+  int64_t d_cur = 0, base_ps = 0;  // base_ps = c0 + c_kv bs kv_sum (ps), d_cur = ceil(base_ps / 1e6)
   float rd_cur = 0.0f;
 
   // evict(v): free its GPU blocks; DRAM write-through when the tier is on (R18).  Uniform.
@@ -183,7 +211,7 @@ __device__ __forceinline__ void replay_one_w32(const ReplayArgs& a, int64_t r, S
         const bool xd = texp <= now && texp <= tev;
         uint32_t m = __ballot_sync(FULL_MASK, xd);
         if (m) {
-          if (lane == 0) acc->exp += __popc(m);
+          ACC_ADD(exp, ACC_EXP, __popc(m));
           if (dram_on) {  // write-through order matters: (time, index) order
             while (m) {
               const int64_t tm = warp_min64_redux((m >> lane) & 1u ? texp : CT_INF64);
@@ -313,7 +341,7 @@ __device__ __forceinline__ void replay_one_w32(const ReplayArgs& a, int64_t r, S
     // (a) STEP reading: release expired pins of programs not waiting
     if (!eager) {
       uint32_t m = __ballot_sync(FULL_MASK, pin && st == S_TOOL && texp <= now);
-      if (lane == 0) acc->exp += __popc(m);
+      ACC_ADD(exp, ACC_EXP, __popc(m));
       while (m) {
         const int p = __ffs(m) - 1;
         m &= m - 1;
@@ -362,7 +390,7 @@ __device__ __forceinline__ void replay_one_w32(const ReplayArgs& a, int64_t r, S
           const uint32_t mv = __ballot_sync(FULL_MASK, pin && lane != h);
           if (!mv) break;
           evict(31 - __clz(mv));
-          if (lane == 0) acc->vict += 1;
+          ACC_ADD(vict, ACC_VICT, 1);
         }
       }
       if (need > free_blk) {  // HOL break
@@ -373,7 +401,7 @@ __device__ __forceinline__ void replay_one_w32(const ReplayArgs& a, int64_t r, S
       free_blk -= (int32_t)need;
       const int32_t ng = hg + (int32_t)need;
       const int64_t hreq = shfl64(req, h);
-      if (lane == 0) acc->bubble += now - hreq;
+      ACC_ADD(bubble, ACC_BUBBLE, now - hreq);
       const bool hp = __shfl_sync(FULL_MASK, pin ? 1 : 0, h) != 0;
       const int32_t hd = __shfl_sync(FULL_MASK, dblk, h);
       int64_t cached;
@@ -381,19 +409,19 @@ __device__ __forceinline__ void replay_one_w32(const ReplayArgs& a, int64_t r, S
       int64_t ld = 0;
       if (hp) {
         cached = hctx;
-        if (lane == 0) acc->hits += 1;
+        ACC_ADD(hits, ACC_HITS, 1);
       } else if (dram_on && hd > 0 && hd == (int32_t)ceil_div_magic((uint32_t)hctx, bsm)) {
         cached = hctx;
         loading = true;
         ld = max(now, chan) + ceil_ps_to_us((uint64_t)((int64_t)hd * E.c_h2d_ps));
         chan = ld;
-        if (lane == 0) acc->reload += 1;
+        ACC_ADD(reload, ACC_RELOAD, 1);
       } else {
         cached = 0;
-        if (lane == 0) acc->recomp += hctx;
+        ACC_ADD(recomp, ACC_RECOMP, hctx);
       }
       const int64_t u = hctx + hnew - cached;
-      if (lane == 0) acc->prefill += u;
+      ACC_ADD(prefill, ACC_PREFILL, u);
       if (lane == h) {
         if (a.bubble) a.bubble[(r - a.r_begin) * P + lane] += now - req;
         pin = false;
@@ -428,13 +456,13 @@ __device__ __forceinline__ void replay_one_w32(const ReplayArgs& a, int64_t r, S
     if (n_run > 0) {
       if (kv_sum != kv_at) {
         kv_at = kv_sum;
-        d_cur = ceil_ps_to_us((uint64_t)(E.c0_ps + E.c_kv_ps * bs * kv_sum));
+        base_ps = E.c0_ps + E.c_kv_ps * bs * kv_sum;
+        d_cur = ceil_ps_to_us((uint64_t)base_ps);
         rd_cur = __frcp_rn((float)d_cur);
       }
       const int64_t d = d_cur;
       // the first iteration carries the prefill of newly admitted requests (R16)
-      const int64_t dur1 =
-          pf > 0 ? ceil_ps_to_us((uint64_t)(E.c0_ps + E.c_kv_ps * bs * kv_sum + E.c_pf_ps * pf)) : d;
+      const int64_t dur1 = pf > 0 ? ceil_ps_to_us((uint64_t)(base_ps + E.c_pf_ps * pf)) : d;
       pf = 0;
       int64_t k = 1;
       if (stable) {
@@ -442,7 +470,8 @@ __device__ __forceinline__ void replay_one_w32(const ReplayArgs& a, int64_t r, S
         // finish or the first boundary at or after the next external event
         const int64_t mfin = warp_min64_redux(st == S_RUN ? fin : CT_INF64);
         const int64_t te = warp_min64_redux(min(tev, texp));
-        k = macro_iters(mfin - n_it, te - now, dur1, d, rd_cur);
+        k = FAST ? macro_iters32(mfin - n_it, te - now, dur1, (uint32_t)d, rd_cur)
+                 : macro_iters(mfin - n_it, te - now, dur1, d, rd_cur);
 #ifdef CT_DEBUG_LOOPS
         ++dbg_macro;
 #endif
@@ -451,7 +480,7 @@ __device__ __forceinline__ void replay_one_w32(const ReplayArgs& a, int64_t r, S
       if (n_it + k > E.max_iters) { status = CT_R_EVENT_BUDGET; break; }
       n_it += k;
       iter_end = now + dur;
-      if (lane == 0) acc->busy += dur;  // cold: kept in shared memory, not a register
+      ACC_ADD(busy, ACC_BUSY, dur);
       if (plas && st == S_RUN) svc += dur;  // every running request accrues the iterations
       in_flight = true;
     }
@@ -476,7 +505,23 @@ __device__ __forceinline__ void replay_one_w32(const ReplayArgs& a, int64_t r, S
     p50 = shfl64(req, __ffs(__ballot_sync(FULL_MASK, c5)) - 1);
     p99 = shfl64(req, __ffs(__ballot_sync(FULL_MASK, c9)) - 1);
   }
+  int64_t av[8];
+  if (FAST) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) av[k] = shfl64(accv, k);
+  }
+#undef ACC_ADD
   if (lane == 0) {
+    if (!FAST) {
+      av[ACC_BUBBLE] = acc->bubble;
+      av[ACC_PREFILL] = acc->prefill;
+      av[ACC_RECOMP] = acc->recomp;
+      av[ACC_BUSY] = acc->busy;
+      av[ACC_HITS] = acc->hits;
+      av[ACC_EXP] = acc->exp;
+      av[ACC_VICT] = acc->vict;
+      av[ACC_RELOAD] = acc->reload;
+    }
     ct_replica_summary o;
     if (status == CT_R_OK) {
       o.status = status;
@@ -486,16 +531,16 @@ __device__ __forceinline__ void replay_one_w32(const ReplayArgs& a, int64_t r, S
       o.max_jct_us = jmax;
       o.p50_jct_us = p50;
       o.p99_jct_us = p99;
-      o.sum_bubble_us = acc->bubble;
+      o.sum_bubble_us = av[ACC_BUBBLE];
       o.makespan_us = now - arr0;  // the last event processed is the last completion
       o.iterations = n_it;
-      o.busy_us = acc->busy;
-      o.prefill_tokens = acc->prefill;
-      o.recompute_tokens = acc->recomp;
-      o.pin_hits = acc->hits;
-      o.pin_expiries = acc->exp;
-      o.victims = acc->vict;
-      o.reloads = acc->reload;
+      o.busy_us = av[ACC_BUSY];
+      o.prefill_tokens = av[ACC_PREFILL];
+      o.recompute_tokens = av[ACC_RECOMP];
+      o.pin_hits = av[ACC_HITS];
+      o.pin_expiries = av[ACC_EXP];
+      o.victims = av[ACC_VICT];
+      o.reloads = av[ACC_RELOAD];
 #ifdef CT_DEBUG_LOOPS
       o.reloads = dbg_loops;
       o.victims = dbg_sched;
