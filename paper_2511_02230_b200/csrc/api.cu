@@ -257,8 +257,9 @@ int ct_simulate_batch_ex(ct_ctx* c, const ct_trace_set* tr, const ct_sweep* sw,
   int64_t kv_max = 0;
   for (size_t i = 0; i < n_kv; ++i) kv_max = std::max<int64_t>(kv_max, sw->kv_blocks[i]);
   const i128 d_max = ((i128)E.c0_ps + (i128)E.c_kv_ps * E.bs * kv_max + 999999) / 1000000;
+  a.d32 = d_max < ((i128)1 << 31) ? 1 : 0;
   int n_fast = 0;
-  if (d_max < ((i128)1 << 31))
+  if (a.d32)
     for (size_t i = 0; i < n_pol; ++i) n_fast += ct::fast_policy(sw->policies[i], E) ? 1 : 0;
   const int mode = (ns != 1 || growth || n_fast == 0) ? 0 : (n_fast == (int)n_pol ? 1 : 2);
   const int wpb = 4;

@@ -26,6 +26,7 @@ struct ReplayArgs {
   unsigned long long* counter;
   int smem_per_warp;
   uint64_t bs_magic;  // ceil(2^64 / bs) (0 when bs == 1)
+  int d32;            // every no-prefill iteration is below 2^31 µs (32-bit macro-step division)
 };
 
 // The TTL-grid policy class, for which the P <= 32 replay has a specialised path: program

@@ -750,7 +750,7 @@ __device__ __forceinline__ void replay_one_ns(const ReplayArgs& a, int64_t r, un
   int n_run = 0, n_load = 0;  // n_load counts LOADING and READY
   int64_t kv_sum = 0, pf = 0;
   int status = CT_R_OK;
-  int64_t kv_at = -1, d_cur = 0;
+  int64_t kv_at = -1, d_cur = 0, base_ps = 0;  // base_ps = c0 + c_kv bs kv_sum (ps)
   float rd_cur = 0.0f;
 
   // evict(v): free its GPU blocks, DRAM write-through when the tier is on (R18); unpin.  Uniform.
@@ -1234,13 +1234,13 @@ __device__ __forceinline__ void replay_one_ns(const ReplayArgs& a, int64_t r, un
       }
       if (kv_sum != kv_at) {
         kv_at = kv_sum;
-        d_cur = ceil_ps_to_us((uint64_t)(E.c0_ps + E.c_kv_ps * bs * kv_sum));
+        base_ps = E.c0_ps + E.c_kv_ps * bs * kv_sum;
+        d_cur = ceil_ps_to_us((uint64_t)base_ps);
         rd_cur = __frcp_rn((float)d_cur);
       }
       const int64_t d = d_cur;
       // the first iteration carries the prefill of newly admitted requests (R16)
-      const int64_t dur1 =
-          pf > 0 ? ceil_ps_to_us((uint64_t)(E.c0_ps + E.c_kv_ps * bs * kv_sum + E.c_pf_ps * pf)) : d;
+      const int64_t dur1 = pf > 0 ? ceil_ps_to_us((uint64_t)(base_ps + E.c_pf_ps * pf)) : d;
       pf = 0;
       int64_t k = 1;
       if (stable) {
@@ -1248,7 +1248,8 @@ __device__ __forceinline__ void replay_one_ns(const ReplayArgs& a, int64_t r, un
         // finish or the first boundary at or after the next external event
         const int64_t mfin = warp_min64_redux(grow_on ? min(fmin, gmin) : fmin);
         const int64_t te = min(warp_min64_redux(min(lev, lexp)), t_arr);
-        k = macro_iters(mfin - n_it, te - now, dur1, d, rd_cur);
+        k = a.d32 ? macro_iters32(mfin - n_it, te - now, dur1, (uint32_t)d, rd_cur)
+                  : macro_iters(mfin - n_it, te - now, dur1, d, rd_cur);
       }
       const int64_t dur = dur1 + (k - 1) * d;
       if (n_it + k > E.max_iters) { status = CT_R_EVENT_BUDGET; break; }
