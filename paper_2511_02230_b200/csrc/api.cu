@@ -261,9 +261,13 @@ int ct_simulate_batch_ex(ct_ctx* c, const ct_trace_set* tr, const ct_sweep* sw,
   int n_fast = 0;
   if (a.d32)
     for (size_t i = 0; i < n_pol; ++i) n_fast += ct::fast_policy(sw->policies[i], E) ? 1 : 0;
-  const int mode = (ns != 1 || growth || n_fast == 0) ? 0 : (n_fast == (int)n_pol ? 1 : 2);
+  int n_prog = 0;
+  for (size_t i = 0; i < n_pol; ++i) n_prog += ct::prog_policy(sw->policies[i], E) ? 1 : 0;
+  const int mode = growth ? 0
+                   : ns == 1 ? (n_fast == 0 ? 0 : (n_fast == (int)n_pol ? 1 : 2))
+                             : (n_prog == (int)n_pol ? 1 : 0);
   const int wpb = 4;
-  a.smem_per_warp = ct::replay_smem_per_warp(ns, F, growth);
+  a.smem_per_warp = ct::replay_smem_per_warp(ns, F, growth, mode);
   const int smem = a.smem_per_warp * wpb;
   int occ = ct::replay_occupancy(ns, growth, mode, wpb, smem);
   if (occ < 1) return fail(CT_ECUDA, "replay kernel cannot be resident (smem %d)", smem);

@@ -37,9 +37,16 @@ inline __host__ __device__ bool fast_policy(const ct_policy& p, const ct_engine_
          (p.pause == CT_PAUSE_EVICT || (p.pause == CT_PAUSE_FIXED && p.t_thresh_us == CT_ALWAYS));
 }
 
+// The program-FCFS class, for which the P > 32 replay has a specialised path: program FCFS; any
+// pause action but InferCept; no DRAM tier; eager expiry and the paper's victim rule.
+inline __host__ __device__ bool prog_policy(const ct_policy& p, const ct_engine_params& E) {
+  return p.priority == CT_PRIO_PROG_FCFS && p.flags == 0 && (p.dram == 0 || E.dram_blocks <= 0) &&
+         p.pause != CT_PAUSE_INFERCEPT;
+}
+
 // Bytes of shared memory one replica (one warp) needs for `ns` slots per lane and F tools.
 // KV growth (NEXT-2) always runs the shared-memory path, also for P <= 32.
-int replay_smem_per_warp(int ns, int F, bool growth);
+int replay_smem_per_warp(int ns, int F, bool growth, int mode);
 // Launch the persistent replay kernel; returns the cudaError of the launch.
 // mode (ns == 1, default engine): 0 generic, 1 all policies fast_policy(), 2 mixed.
 cudaError_t launch_replay(const ReplayArgs& a, int ns, bool growth, int mode, int warps_per_block,

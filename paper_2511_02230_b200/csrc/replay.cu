@@ -19,10 +19,12 @@ namespace ct {
 
 enum : int { S_OUT = 0, S_QUEUED = 1, S_RUN = 2, S_LOAD = 3, S_READY = 4, S_TOOL = 5, S_DONE = 6 };
 
-int replay_smem_per_warp(int ns, int F, bool vllm) {
+int replay_smem_per_warp(int ns, int F, bool vllm, int mode) {
   if (ns == 1 && !vllm) return (32 * (F + 1) + 48 + 15) & ~15;  // registers hold the programs; SMEM: estimator + Acc
   int pm = 32 * ns;
-  int b = (vllm ? 76 : 60) * pm;  // the vLLM engine adds grow_at (8 B), emt and prem (4 B each)
+  // the vLLM engine adds grow_at (8 B), emt and prem (4 B each); the program-FCFS class (mode 1)
+  // drops svc (8 B) and dblk (4 B)
+  int b = (vllm ? 76 : mode == 1 ? 48 : 60) * pm;
   b = (b + 15) & ~15;
   b += 32 * (F + 1) + 48;  // estimator rows + Acc
   return (b + 15) & ~15;
@@ -568,7 +570,9 @@ __device__ __forceinline__ void replay_one_w32(const ReplayArgs& a, int64_t r, S
 // programs changes.  The next event, the macro-step bound and the first finish are therefore one
 // REDUX minimum each, and only lanes that own a due program scan their slots.  Same semantics as
 // replay_one_w32 (C-5/C-6), checked byte for byte by the tests.
-template <int NS, bool VLLM>
+// PROG: the policy is in the program-FCFS class (prog_policy(), ct_internal.h): request FCFS,
+// PLAS, the DRAM tier, InferCept and the alternative readings compile away.
+template <int NS, bool VLLM, bool PROG>
 __device__ __forceinline__ void replay_one_ns(const ReplayArgs& a, int64_t r, unsigned char* wm,
                                               int lane) {
   constexpr int PM = 32 * NS;
@@ -576,11 +580,12 @@ __device__ __forceinline__ void replay_one_ns(const ReplayArgs& a, int64_t r, un
   int64_t* texp = tev + PM;            // expiry + 1 while pinned in a tool call, INF otherwise
   int64_t* req = texp + PM;            // request arrival; JCT once done
   int64_t* fin = req + PM;             // finishing iteration while running, INF otherwise
+  // PROG keeps no svc / dblk arrays (never read): 48 instead of 60 B per program
   int64_t* svc = fin + PM;             // attained engine time (PLAS)
-  int32_t* ctx = (int32_t*)(svc + PM); // context tokens
+  int32_t* ctx = (int32_t*)(svc + (PROG ? 0 : PM)); // context tokens
   int32_t* gblk = ctx + PM;            // GPU blocks held
   int32_t* dblk = gblk + PM;           // DRAM copy blocks
-  int32_t* unc = dblk + PM;            // uncached tokens of the current request
+  int32_t* unc = dblk + (PROG ? 0 : PM);  // uncached tokens of the current request
   int32_t* turn = unc + PM;            // current turn
   // vLLM engine (NEXT-2) only.  KV growth (R27-R30): next iteration boundary at which the
   // running request needs one more block (INF otherwise) and tokens emitted before a
@@ -590,7 +595,7 @@ __device__ __forceinline__ void replay_one_ns(const ReplayArgs& a, int64_t r, un
   int64_t* grow_at = (int64_t*)(turn + PM);
   int32_t* emt = (int32_t*)(grow_at + PM);
   int32_t* prem = emt + PM;
-  Stat* stats = (Stat*)(wm + (((VLLM ? 76 : 60) * PM + 15) & ~15));
+  Stat* stats = (Stat*)(wm + (((VLLM ? 76 : PROG ? 48 : 60) * PM + 15) & ~15));
   Acc* acc = (Acc*)(stats + a.F + 1);
 
   const int P = a.P, F = a.F;
@@ -600,7 +605,9 @@ __device__ __forceinline__ void replay_one_ns(const ReplayArgs& a, int64_t r, un
   const int rate_i = (int)((r / (npol * nkv)) % nrate);
   const int64_t seed = r / (npol * nkv * nrate);
   const ct_policy* polp = a.pols + pol_i;
-  const int prio = polp->priority, pause = polp->pause, pflags = polp->flags;
+  const int prio = PROG ? CT_PRIO_PROG_FCFS : polp->priority;
+  const int pause = polp->pause;
+  const int pflags = PROG ? 0 : polp->flags;
   const int64_t gap = a.gap[rate_i];
   const ct_program* prog = a.progs + seed * P;
   const ct_engine_params& E = a.eng;
@@ -613,10 +620,10 @@ __device__ __forceinline__ void replay_one_ns(const ReplayArgs& a, int64_t r, un
   bsm.ident = bs == 1 ? 1u : 0u;
   const bool eager = (pflags & CT_FLAG_STEP_EXPIRY) == 0;
   const bool vany = (pflags & CT_FLAG_VICTIMS_ANY) != 0;
-  const bool dram_on = polp->dram != 0 && E.dram_blocks > 0;
-  const bool need_stats = pause == CT_PAUSE_PAPER || pause == CT_PAUSE_INFERCEPT ||
+  const bool dram_on = !PROG && polp->dram != 0 && E.dram_blocks > 0;
+  const bool need_stats = pause == CT_PAUSE_PAPER || (!PROG && pause == CT_PAUSE_INFERCEPT) ||
                           (pause == CT_PAUSE_FIXED && polp->t_thresh_us != CT_ALWAYS);
-  const bool plas = prio == CT_PRIO_PLAS;
+  const bool plas = !PROG && prio == CT_PRIO_PLAS;
 
 #pragma unroll
   for (int s = 0; s < NS; ++s) {
@@ -625,10 +632,10 @@ __device__ __forceinline__ void replay_one_ns(const ReplayArgs& a, int64_t r, un
     texp[p] = CT_INF64;
     req[p] = 0;
     fin[p] = CT_INF64;
-    svc[p] = 0;
+    if (!PROG) svc[p] = 0;
     ctx[p] = 0;
     gblk[p] = 0;
-    dblk[p] = 0;
+    if (!PROG) dblk[p] = 0;
     unc[p] = 0;
     turn[p] = 0;
     if (VLLM) {
@@ -932,9 +939,13 @@ __device__ __forceinline__ void replay_one_ns(const ReplayArgs& a, int64_t r, un
           const int nt = prog[p].nturns;
           if (tp == nt - 1) {  // last request: free its KV, the program completes
             free_blk += g;
-            dfree += dblk[p];
+            if (!PROG) dfree += dblk[p];
             __syncwarp();
-            if (own(p)) { gblk[p] = 0; dblk[p] = 0; req[p] = now - arrival(p); }
+            if (own(p)) {
+              gblk[p] = 0;
+              if (!PROG) dblk[p] = 0;
+              req[p] = now - arrival(p);
+            }
             ++D;
             turns_done += nt;
             __syncwarp();
@@ -1156,7 +1167,7 @@ __device__ __forceinline__ void replay_one_ns(const ReplayArgs& a, int64_t r, un
         if (lane == 0) acc->bubble += now - req[h];
         if (bub && own(h)) bub[h] += now - req[h];
         const bool hp = (__shfl_sync(FULL_MASK, pb, h & 31) >> (h >> 5)) & 1u;
-        const int64_t hd = dblk[h];
+        const int64_t hd = PROG ? 0 : dblk[h];
         int64_t cached;
         bool loading = false;
         int64_t ld = 0;
@@ -1346,8 +1357,9 @@ __device__ __forceinline__ void replay_one_ns(const ReplayArgs& a, int64_t r, un
 
 // VLLM: the vLLM engine of NEXT-2 (KV growth, chunked prefill), always through the
 // shared-memory path (also P <= 32).
-// MODE (P <= 32 default engine): 0 every policy generic, 1 every policy in the TTL-grid class
-// (the specialised replay only: 3x smaller code, no register spills), 2 mixed (per replica).
+// MODE (default engine): P <= 32: 0 every policy generic, 1 every policy in the TTL-grid class
+// (the specialised replay only: 3x smaller code, no register spills), 2 mixed (per replica);
+// P > 32: 0 generic, 1 every policy in the program-FCFS class.
 template <int NS, int MINB, bool VLLM = false, int MODE = 0>
 __global__ void __launch_bounds__(128, MINB) replay_kernel(ReplayArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -1365,7 +1377,7 @@ __global__ void __launch_bounds__(128, MINB) replay_kernel(ReplayArgs a) {
       else
         replay_one_w32<false>(a, r, (Stat*)wm, lane);
     } else
-      replay_one_ns<NS, VLLM>(a, r, wm, lane);
+      replay_one_ns<NS, VLLM, (MODE == 1)>(a, r, wm, lane);
   }
 }
 
@@ -1380,6 +1392,9 @@ static int minb() {
   return g_minb;
 }
 
+#ifndef NS_PROG_MINB
+#define NS_PROG_MINB 5  // 5 CTAs of 4 warps per SM: <= 102 registers, 48 B SMEM per program
+#endif
 static void* pick(int ns, bool growth, int mode) {
   if (growth) {
     switch (ns) {
@@ -1410,13 +1425,13 @@ static void* pick(int ns, bool growth, int mode) {
         case 12: return (void*)replay_kernel<1, 12>;
         default: return (void*)replay_kernel<1, 8>;
       }
-    case 2: return (void*)replay_kernel<2, 1>;
-    case 3: return (void*)replay_kernel<3, 1>;
-    case 4: return (void*)replay_kernel<4, 1>;
-    case 5: return (void*)replay_kernel<5, 1>;
-    case 6: return (void*)replay_kernel<6, 1>;
-    case 7: return (void*)replay_kernel<7, 1>;
-    case 8: return (void*)replay_kernel<8, 1>;
+    case 2: return mode == 1 ? (void*)replay_kernel<2, NS_PROG_MINB, false, 1> : (void*)replay_kernel<2, 1>;
+    case 3: return mode == 1 ? (void*)replay_kernel<3, NS_PROG_MINB, false, 1> : (void*)replay_kernel<3, 1>;
+    case 4: return mode == 1 ? (void*)replay_kernel<4, NS_PROG_MINB, false, 1> : (void*)replay_kernel<4, 1>;
+    case 5: return mode == 1 ? (void*)replay_kernel<5, NS_PROG_MINB, false, 1> : (void*)replay_kernel<5, 1>;
+    case 6: return mode == 1 ? (void*)replay_kernel<6, NS_PROG_MINB, false, 1> : (void*)replay_kernel<6, 1>;
+    case 7: return mode == 1 ? (void*)replay_kernel<7, NS_PROG_MINB, false, 1> : (void*)replay_kernel<7, 1>;
+    case 8: return mode == 1 ? (void*)replay_kernel<8, NS_PROG_MINB, false, 1> : (void*)replay_kernel<8, 1>;
   }
   return nullptr;
 }
