@@ -74,6 +74,23 @@ __device__ __forceinline__ uint64_t isqrt_u64(uint64_t x) {
   return r;
 }
 
+// floor(num / den) for 0 < den < 2^64, exact.  Fast path when the quotient is below 2^50: the
+// double estimate has relative error < 2^-50.5 (three roundings), so it is within one of the
+// quotient and a single integer correction against num - q den makes it exact.  Larger
+// quotients take the generic 128-bit division.
+__device__ __forceinline__ u128_t div_u128_u64(u128_t num, uint64_t den) {
+  const double dn = (double)(uint64_t)(num >> 64) * 18446744073709551616.0 + (double)(uint64_t)num;
+  const double est = dn / (double)den;
+  if (est < 1125899906842624.0) {  // 2^50
+    uint64_t q = (uint64_t)est;
+    const u128_t prod = (u128_t)q * den;
+    if (prod > num) q -= 1;
+    else if (num - prod >= den) q += 1;
+    return q;
+  }
+  return num / den;
+}
+
 struct Stat {  // one estimator row: n, sum t~, sum t~^2 (128-bit as lo/hi)
   int64_t n, s1;
   uint64_t s2lo, s2hi;
@@ -90,12 +107,12 @@ __device__ __forceinline__ int64_t bernstein(const Stat& s, uint64_t lq, int64_t
     u128_t s2 = ((u128_t)s.s2hi << 64) | s.s2lo;
     u128_t num = (u128_t)(uint64_t)n * s2 - (u128_t)(uint64_t)s.s1 * (uint64_t)s.s1;
     uint64_t den = (uint64_t)n * (uint64_t)(n - 1);  // n < 2^31 (validated)
-    v = num / den;
+    v = div_u128_u64(num, den);
   }
   uint64_t nsh = (uint64_t)n << 32;
-  u128_t a2 = ((u128_t)2 * v * lq) / nsh;
+  u128_t a2 = div_u128_u64((u128_t)2 * v * lq, nsh);
   uint64_t t2 = isqrt_u64((uint64_t)a2);
-  u128_t t3 = ((u128_t)3 * (uint64_t)b_us * lq) / nsh;
+  u128_t t3 = div_u128_u64((u128_t)3 * (uint64_t)b_us * lq, nsh);
   return mu + (int64_t)t2 + (int64_t)t3;
 }
 
@@ -108,15 +125,15 @@ __device__ __forceinline__ int64_t calc_ttl(const Stat& g, const Stat& f,
   else if (f.n >= e.n_min) B = bernstein(f, e.lq, e.b_us);
   else B = bernstein(g, e.lq, e.b_us);
   if (B < 1) B = 1;
-  const uint64_t T2 = (uint64_t)e.t_default_us * (uint64_t)e.t_default_us;
+  const u128_t T2 = (u128_t)(uint64_t)e.t_default_us * (uint64_t)e.t_default_us;  // < 2^80
   u128_t ttl;
   if (n_done > 0) {
-    u128_t num = (u128_t)T2 * ((u128_t)(uint64_t)n_done * (uint64_t)e.a_den +
-                               (u128_t)(uint64_t)e.a_num * (uint64_t)turns_done);
+    u128_t num = T2 * ((u128_t)(uint64_t)n_done * (uint64_t)e.a_den +
+                       (u128_t)(uint64_t)e.a_num * (uint64_t)turns_done);
     u128_t den = (u128_t)(uint64_t)B * (uint64_t)n_done * (uint64_t)e.a_den;
-    ttl = num / den;
+    ttl = (den >> 64) == 0 ? div_u128_u64(num, (uint64_t)den) : num / den;
   } else {
-    ttl = (u128_t)T2 / (uint64_t)B;
+    ttl = div_u128_u64(T2, (uint64_t)B);
   }
   if (e.ttl_max_us > 0 && ttl > (u128_t)(uint64_t)e.ttl_max_us) ttl = (uint64_t)e.ttl_max_us;
   return (int64_t)(uint64_t)ttl;

@@ -235,3 +235,29 @@ def test_fit_large_grids(ctx, K):
     g, o = fit_both(ctx, dur, off, K, 50_000, 3, 13_400_000, 40, cf.Estimator())
     for x, y in zip(g, o):
         assert np.array_equal(x, y)
+
+
+@pytest.mark.parametrize("case", range(6))
+def test_fit_estimator_extremes(ctx, case):
+    """Bernstein / CalcTTL at the validated extremes (b, T_default up to 2^40 - 1, delta down to
+    1e-9, tiny and large n, large alpha and AvgTurns): the 128-bit divisions take both the
+    double-estimate fast path and the generic path, and must stay exact."""
+    rng = np.random.default_rng(100 + case)
+    F = 6
+    sizes = [1, 2, 3, int(rng.integers(5, 50)), int(rng.integers(1000, 5000)), 20_000]
+    off = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+    n = int(off[-1])
+    hi = [2**31 - 1, 2**28, 5_000_000][case % 3]
+    dur = rng.integers(0, hi, n).astype(np.int32)
+    dur[: 3] = 2**31 - 1
+    big, b31 = 2**40 - 1, 2**31 - 1  # validated maxima: T_default, ttl_max < 2^40; b < 2^31 (fit)
+    est = [cf.Estimator(delta=1e-9, b_us=b31, t_def_us=big, n_min=1, a_num=1000, a_den=1, ttl_max_us=big),
+           cf.Estimator(delta=0.999, b_us=b31, t_def_us=7, n_min=2, a_num=0, a_den=3, ttl_max_us=0),
+           cf.Estimator(delta=1e-6, b_us=2**30, t_def_us=10**12, n_min=1, a_num=7, a_den=9, ttl_max_us=big),
+           cf.Estimator(delta=0.05, b_us=60_000_000, t_def_us=10_000_000, n_min=5, ttl_max_us=0),
+           cf.Estimator(delta=1e-9, b_us=1, t_def_us=big, n_min=3, a_num=5, a_den=1, ttl_max_us=big),
+           cf.Estimator(delta=0.3, b_us=b31, t_def_us=2**39, n_min=1, a_num=1, a_den=10**6, ttl_max_us=big)][case]
+    avg = [(10**6, 3), (0, 0), (2**31, 1), (500, 40), (7, 7), (1, 2**20)][case]
+    g, o = fit_both(ctx, dur, off, 64, 250_000, 2, 13_400_000, 40, est, avg=avg)
+    for name, x, y in zip(("ttl_argmax", "ttl_paper", "stats"), g, o):
+        assert np.array_equal(x, y), (name, case, x, y)
