@@ -563,6 +563,286 @@ __device__ __forceinline__ void replay_one_w32(const ReplayArgs& a, int64_t r, S
 }
 
 // -----------------------------------------------------------------------------------------------
+// TTL-grid class with 32-bit replica-relative times.  Every time is µs since the replica's first
+// arrival (program 0), saturated at T32_LIM; every iteration lasts >= 1 µs, so iteration indices
+// stay below the time and fit too.  The moment the next event (or an iteration end) lies at or
+// beyond T32_LIM the function returns false and the caller replays the replica on the 64-bit
+// path (replay_one_w32<true>): the saturated values are only ever compared, never applied.
+// Otherwise identical to replay_one_w32<true> step for step (C-5/C-6); the parity
+// tests cover both, including horizons beyond 2^32 µs.
+constexpr uint32_t T32_INF = 0xFFFFFFFFu;
+constexpr uint32_t T32_LIM = 0xFFFFFFF0u;
+
+__device__ __forceinline__ uint32_t sat32(int64_t v) {  // v >= 0
+  return v >= (int64_t)T32_LIM ? T32_LIM : (uint32_t)v;
+}
+
+__device__ __forceinline__ bool replay_one_t32(const ReplayArgs& a, int64_t r, int lane) {
+  const int P = a.P;
+  const int64_t npol = a.n_pol, nkv = a.n_kv, nrate = a.n_rate;
+  const int pol_i = (int)(r % npol);
+  const int kv_i = (int)((r / npol) % nkv);
+  const int rate_i = (int)((r / (npol * nkv)) % nrate);
+  const int64_t seed = r / (npol * nkv * nrate);
+  const ct_policy* polp = a.pols + pol_i;
+  // FIXED with CT_ALWAYS pins for t_pin; EVICT never pins (fast_policy)
+  const int64_t ttl = polp->pause == CT_PAUSE_FIXED ? polp->t_pin_us : 0;
+  const int64_t gap = a.gap[rate_i];
+  const ct_engine_params& E = a.eng;
+  DivMagic bsm;
+  bsm.mhi = (uint32_t)(a.bs_magic >> 32);
+  bsm.mlo = (uint32_t)a.bs_magic;
+  bsm.dm1 = (uint32_t)(E.bs - 1);
+  bsm.ident = E.bs == 1 ? 1u : 0u;
+
+  const bool live = lane < P;
+  int32_t turn0 = 0, nturns = 1;
+  int64_t arr64 = CT_INF64;
+  if (live) {
+    const ct_program pr = a.progs[seed * P + lane];
+    turn0 = pr.turn0;
+    nturns = pr.nturns;
+    arr64 = (pr.arr_q * gap) >> 20;
+  }
+  const int64_t arr0 = shfl64(arr64, 0);  // programs arrive in index order: the time origin
+  const uint32_t arr = live ? sat32(arr64 - arr0) : T32_INF;
+  if (a.bubble && live) a.bubble[(r - a.r_begin) * P + lane] = 0;
+  int st = S_OUT;
+  uint32_t tev = arr;      // arrival (OUT), tool return (TOOL); INF otherwise
+  uint32_t texp = T32_INF; // expiry + 1 while pinned in a tool call
+  uint32_t req = 0;        // request arrival; JCT once done
+  uint32_t fin = 0;        // iteration index at whose end the running request finishes
+  int32_t ctx = 0, gblk = 0, turn = 0;
+  bool pin = false;
+  int4 rec = make_int4(0, 0, -1, 0);
+
+  uint32_t now = 0, iter_end = 0, n_it = 0;
+  bool in_flight = false;
+  int32_t free_blk = (int32_t)a.kv[kv_i];
+  int32_t D = 0, turns_done = 0;
+  int n_run = 0;
+  int32_t kv_sum = 0;
+  int64_t pf = 0;
+  int status = CT_R_OK;
+  int64_t accv = 0;  // lane k holds summary counter k (ACC_*)
+  auto acc_add = [&](int k, int64_t v) {
+    if (lane == k) accv += v;
+  };
+  int32_t kv_at = -1;
+  int64_t base_ps = 0;
+  uint32_t d_cur = 0;
+  float rd_cur = 0.0f;
+
+  for (;;) {
+    uint32_t t;
+    if (in_flight) {
+      t = iter_end;
+    } else {
+      t = __reduce_min_sync(FULL_MASK, min(tev, texp));
+      if (t == T32_INF) break;
+    }
+    if (t >= T32_LIM) return false;  // beyond the 32-bit horizon: replay on the 64-bit path
+    now = t;
+
+    if (__any_sync(FULL_MASK, min(tev, texp) <= now)) {
+      // PinExpiry (EAGER, R4/R15) precedes the program's own tool return at the same µs (R1)
+      const bool xd = texp <= now && texp <= tev;
+      const uint32_t m = __ballot_sync(FULL_MASK, xd);
+      if (m) {
+        acc_add(ACC_EXP, __popc(m));
+        free_blk += (int32_t)__reduce_add_sync(FULL_MASK, xd ? (uint32_t)gblk : 0u);
+        if (xd) { gblk = 0; pin = false; texp = T32_INF; }
+      }
+      const bool due = tev <= now;
+      if (due && st == S_TOOL) {  // ToolReturn == OnRequestArrive
+        ++turn;
+        rec = __ldg((const int4*)a.turns + turn0 + turn);
+        st = S_QUEUED;
+        req = tev;
+        tev = T32_INF;
+        texp = T32_INF;  // a retained pin has no expiry event while waiting
+      } else if (due && st == S_OUT) {  // ProgramArrival
+        st = S_QUEUED;
+        req = tev;
+        tev = T32_INF;
+        rec = __ldg((const int4*)a.turns + turn0);
+      }
+    }
+
+    // IterationEnd: members whose last token was emitted finish, in index order (C-6)
+    if (in_flight && iter_end == now) {
+      in_flight = false;
+      uint32_t m = __ballot_sync(FULL_MASK, st == S_RUN && fin == n_it);
+      while (m) {
+        const int p = __ffs(m) - 1;
+        m &= m - 1;
+        const int pt = __shfl_sync(FULL_MASK, turn, p);
+        const int pn = __shfl_sync(FULL_MASK, nturns, p);
+        const int pg = __shfl_sync(FULL_MASK, gblk, p);
+        --n_run;
+        kv_sum -= pg;
+        if (lane == p) ctx += rec.x + rec.y;
+        if (pt == pn - 1) {  // last request: free its KV, the program completes
+          free_blk += pg;
+          if (lane == p) { gblk = 0; st = S_DONE; req = now - arr; }
+          ++D;
+          turns_done += pn;
+        } else {
+          if (ttl > 0) {  // pin_request only if TTL != 0
+            if (lane == p) { pin = true; texp = sat32((int64_t)now + ttl + 1); }
+          } else {  // evict
+            free_blk += pg;
+            if (lane == p) { gblk = 0; pin = false; texp = T32_INF; }
+          }
+          if (lane == p) { tev = sat32((int64_t)now + rec.w); st = S_TOOL; }
+        }
+      }
+    }
+    if (in_flight) continue;  // mid-iteration: events only mutate Q / pins (R2)
+
+    // ---- scheduling point (R3) --------------------------------------------------------------
+    int admitted = 0;
+    bool stable = true;
+    if (__any_sync(FULL_MASK, st == S_QUEUED)) {
+      for (;;) {  // admit loop (victims PAPER.md:645-655)
+        const uint32_t mq = __ballot_sync(FULL_MASK, st == S_QUEUED);
+        if (!mq) break;
+        if (n_run >= E.max_batch) break;
+        const uint32_t mp = __ballot_sync(FULL_MASK, st == S_QUEUED && pin);
+        const int h = __ffs(mp ? mp : mq) - 1;
+        const int32_t hctx = __shfl_sync(FULL_MASK, ctx, h);
+        const int32_t hg = __shfl_sync(FULL_MASK, gblk, h);
+        const int32_t hnew = __shfl_sync(FULL_MASK, rec.x, h);
+        const int32_t hdec = __shfl_sync(FULL_MASK, rec.y, h);
+        const int64_t need = (int64_t)ceil_div_magic((uint32_t)(hctx + hnew + hdec), bsm) - hg;
+        if (need > free_blk && admitted == 0) {
+          while (need > free_blk) {  // victims: latest program arrival first, never the head
+            const uint32_t mv = __ballot_sync(FULL_MASK, pin && lane != h);
+            if (!mv) break;
+            const int v = 31 - __clz(mv);
+            free_blk += __shfl_sync(FULL_MASK, gblk, v);
+            if (lane == v) { gblk = 0; pin = false; texp = T32_INF; }
+            acc_add(ACC_VICT, 1);
+          }
+        }
+        if (need > free_blk) {  // HOL break
+          if (admitted > 0 && __ballot_sync(FULL_MASK, pin && lane != h)) stable = false;
+          break;
+        }
+        free_blk -= (int32_t)need;
+        const int32_t ng = hg + (int32_t)need;
+        acc_add(ACC_BUBBLE, (int64_t)(now - __shfl_sync(FULL_MASK, req, h)));
+        const bool hp = __shfl_sync(FULL_MASK, pin ? 1 : 0, h) != 0;
+        const int64_t cached = hp ? hctx : 0;
+        if (hp) acc_add(ACC_HITS, 1);
+        else acc_add(ACC_RECOMP, hctx);
+        const int64_t u = hctx + hnew - cached;
+        acc_add(ACC_PREFILL, u);
+        if (lane == h) {
+          if (a.bubble) a.bubble[(r - a.r_begin) * P + lane] += now - req;
+          pin = false;
+          texp = T32_INF;
+          gblk = ng;
+          st = S_RUN;
+          fin = sat32((int64_t)n_it + rec.y);
+        }
+        ++n_run;
+        kv_sum += ng;
+        pf += u;
+        ++admitted;
+      }
+      // unschedulable: the head missed with nothing running (C-5 5c)
+      if (admitted == 0 && n_run == 0 && __any_sync(FULL_MASK, st == S_QUEUED)) {
+        status = CT_R_UNSCHEDULABLE;
+        break;
+      }
+    }
+    // start the next iteration(s) (linear cost model, R16)
+    if (n_run > 0) {
+      if (kv_sum != kv_at) {
+        kv_at = kv_sum;
+        base_ps = E.c0_ps + E.c_kv_ps * E.bs * kv_sum;
+        d_cur = (uint32_t)ceil_ps_to_us((uint64_t)base_ps);  // < 2^31 (host-checked)
+        rd_cur = __frcp_rn((float)d_cur);
+      }
+      const int64_t dur1 = pf > 0 ? ceil_ps_to_us((uint64_t)(base_ps + E.c_pf_ps * pf)) : d_cur;
+      pf = 0;
+      int64_t k = 1;
+      if (stable) {
+        const uint32_t mfin = __reduce_min_sync(FULL_MASK, st == S_RUN ? fin : T32_INF);
+        const uint32_t te = __reduce_min_sync(FULL_MASK, min(tev, texp));
+        k = macro_iters32((int64_t)(mfin - n_it), te == T32_INF ? CT_INF64 : (int64_t)te - now,
+                          dur1, d_cur, rd_cur);
+      }
+      const int64_t dur = dur1 + (k - 1) * (int64_t)d_cur;
+      if ((int64_t)n_it + k > E.max_iters) { status = CT_R_EVENT_BUDGET; break; }
+      const int64_t end = (int64_t)now + dur;
+      if (end >= (int64_t)T32_LIM) return false;  // beyond the 32-bit horizon
+      n_it += (uint32_t)k;
+      iter_end = (uint32_t)end;
+      acc_add(ACC_BUSY, dur);
+      in_flight = true;
+    }
+  }
+  if (status == CT_R_OK && D != P) status = CT_R_UNSCHEDULABLE;
+
+  // ---- per-replica summary (A-8) --------------------------------------------------------------
+  const int64_t ri = r - a.r_begin;
+  int64_t jsum = 0, jmax = 0, p50 = 0, p99 = 0;
+  if (status == CT_R_OK) {
+    const uint32_t jv = live ? req : 0;
+    jsum = (int64_t)__reduce_add_sync(FULL_MASK, jv >> 16) * 65536 +
+           (int64_t)__reduce_add_sync(FULL_MASK, jv & 0xFFFFu);
+    jmax = __reduce_max_sync(FULL_MASK, jv);
+    const int r50 = (50 * P + 99) / 100, r99 = (99 * P + 99) / 100;
+    int lt = 0, le = 0;
+    for (int q = 0; q < P; ++q) {
+      const uint32_t x = __shfl_sync(FULL_MASK, req, q);
+      lt += x < req;
+      le += x <= req;
+    }
+    const bool c5 = live && lt < r50 && r50 <= le, c9 = live && lt < r99 && r99 <= le;
+    p50 = __shfl_sync(FULL_MASK, req, __ffs(__ballot_sync(FULL_MASK, c5)) - 1);
+    p99 = __shfl_sync(FULL_MASK, req, __ffs(__ballot_sync(FULL_MASK, c9)) - 1);
+  }
+  int64_t av[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) av[k] = shfl64(accv, k);
+  if (lane == 0) {
+    ct_replica_summary o;
+    if (status == CT_R_OK) {
+      o.status = status;
+      o.n_done = D;
+      o.turns_done = turns_done;
+      o.sum_jct_us = jsum;
+      o.max_jct_us = jmax;
+      o.p50_jct_us = p50;
+      o.p99_jct_us = p99;
+      o.sum_bubble_us = av[ACC_BUBBLE];
+      o.makespan_us = now;  // the last event processed is the last completion; origin = arr0
+      o.iterations = n_it;
+      o.busy_us = av[ACC_BUSY];
+      o.prefill_tokens = av[ACC_PREFILL];
+      o.recompute_tokens = av[ACC_RECOMP];
+      o.pin_hits = av[ACC_HITS];
+      o.pin_expiries = av[ACC_EXP];
+      o.victims = av[ACC_VICT];
+      o.reloads = av[ACC_RELOAD];
+    } else {
+      int64_t* w = (int64_t*)&o;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) w[i] = 0;
+      o.status = status;
+    }
+    a.out[ri] = o;
+  }
+  if (a.jct && live) a.jct[ri * P + lane] = status == CT_R_OK ? (int64_t)req : -1;
+  if (a.bubble && live && status != CT_R_OK) a.bubble[ri * P + lane] = -1;
+  __syncwarp();
+  return true;
+}
+
+// -----------------------------------------------------------------------------------------------
 // 32 < P <= 256: program p lives on lane p % 32, slot p / 32.  Per-program scalars are SoA in
 // shared memory (written only by the owner lane); lifecycle sets are per-lane bit registers
 // (bit s = slot s); every lane caches the minimum of its own programs' event times (tool return /
@@ -1372,10 +1652,11 @@ __global__ void __launch_bounds__(128, MINB) replay_kernel(ReplayArgs a) {
     const int64_t r = a.r_begin + (int64_t)idx;
     if (r >= a.r_end) break;
     if (NS == 1 && !VLLM) {
-      if (MODE == 1 || (MODE == 2 && fast_policy(a.pols[(int)(r % a.n_pol)], a.eng)))
-        replay_one_w32<true>(a, r, (Stat*)wm, lane);
-      else
+      if (MODE == 1 || (MODE == 2 && fast_policy(a.pols[(int)(r % a.n_pol)], a.eng))) {
+        if (!replay_one_t32(a, r, lane)) replay_one_w32<true>(a, r, (Stat*)wm, lane);
+      } else {
         replay_one_w32<false>(a, r, (Stat*)wm, lane);
+      }
     } else
       replay_one_ns<NS, VLLM, (MODE == 1)>(a, r, wm, lane);
   }

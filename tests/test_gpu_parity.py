@@ -261,3 +261,28 @@ def test_fit_estimator_extremes(ctx, case):
     g, o = fit_both(ctx, dur, off, 64, 250_000, 2, 13_400_000, 40, est, avg=avg)
     for name, x, y in zip(("ttl_argmax", "ttl_paper", "stats"), g, o):
         assert np.array_equal(x, y), (name, case, x, y)
+
+
+@pytest.mark.parametrize("P", [1, 17, 32])
+def test_ttl_grid_32bit_horizon(ctx, P):
+    """TTL-grid-only sweeps run the 32-bit-time kernel.  Long inter-arrival gaps (up to 2^30 µs),
+    TTLs up to 2^40 µs and slow engines push replica horizons past 2^32 µs, where the replica
+    must fall back to the 64-bit path: both must agree with the oracle byte for byte, including
+    the per-program bubble output (reset on fallback) and EVENT_BUDGET replicas."""
+    import paper_2511_02230_b200 as ct
+    n_seeds = 4
+    tr = traces.generate(n_seeds, P, n_bfcl=P // 2, mix="mix", ctx_cap=1500 * 16, stream=40 + P)
+    gaps = [1 << 20, 300_000_000, (1 << 30) - 1]
+    pols = [cf.ttl_grid(t) for t in (0, 1, 2_000_000, 600_000_000, 1 << 40)] + [cf.PROG_FCFS]
+    span, budget = 0, False
+    for eng in (cf.ENGINE_8B, cf.Engine(**{**cf.ENGINE_8B.__dict__, "c0_ps": 4 * 10**11}),
+                cf.Engine(**{**cf.ENGINE_8B.__dict__, "max_iters": 2000 if P == 1 else 20000})):
+        sw = cf.Sweep(n_seeds, gaps, [4096, 1600], pols)
+        s, j, b = ct.ct_simulate_batch(ctx, ct.DeviceTrace(tr), sw, eng, jct=True, bubble=True)
+        torch.cuda.synchronize()
+        os_, oj, ob = O.simulate(tr, sw, eng, n_threads=8, want_bubble=True)
+        assert_same(s.cpu().numpy(), j.cpu().numpy(), os_, oj)
+        assert np.array_equal(b.cpu().numpy(), ob)
+        span = max(span, int(np.max(os_[:, 7])))
+        budget |= bool(np.any(os_[:, 0] == 2))
+    assert budget and (P == 1 or span > 2**32)  # both the fallback and EVENT_BUDGET were exercised
