@@ -14,6 +14,13 @@ for P, mix in ((16, "mix"), (70, "mix")):
     sw = cf.Sweep(2, [300_000], [600, 3000], pols, fitted=fitted)
     s, j = ct.ct_simulate_batch(ctx, ct.DeviceTrace(tr), sw, eng, jct=True)
     c = ct.ct_jct_stats(ctx, s, sw.n_cells)
+# specialised kernels: TTL-grid class (32-bit times, with a horizon fallback at the long gap)
+# and the program-FCFS class for P > 32
+for P, pols in ((16, [cf.ttl_grid(0), cf.ttl_grid(2_000_000), cf.PROG_FCFS]),
+                (70, [cf.CONTINUUM, cf.ttl_grid(500_000), cf.PROG_FCFS])):
+    tr = traces.generate(2, P, mix="mix", ctx_cap=8192, stream=P + 1)
+    sw = cf.Sweep(2, [300_000, (1 << 30) - 1], [3000], pols)
+    s, j = ct.ct_simulate_batch(ctx, ct.DeviceTrace(tr), sw, cf.ENGINE_8B, jct=True)
 dur, off = traces.tool_samples(tr)
 cp = ct.cost_params(13_400_000, 200, 16, 1, 10, 50_000, 256, [2000, 8000], [1, 2])
 ct.ct_fit_ttl(ctx, torch.from_numpy(dur).cuda(), off, cp, cf.Estimator())
