@@ -595,6 +595,7 @@ __device__ __forceinline__ bool replay_one_t32(const ReplayArgs& a, int64_t r, i
   bsm.dm1 = (uint32_t)(E.bs - 1);
   bsm.ident = E.bs == 1 ? 1u : 0u;
 
+  if (a.bubble) return false;  // the per-program bubble output runs on the 64-bit path
   const bool live = lane < P;
   int32_t turn0 = 0, nturns = 1;
   int64_t arr64 = CT_INF64;
@@ -606,7 +607,6 @@ __device__ __forceinline__ bool replay_one_t32(const ReplayArgs& a, int64_t r, i
   }
   const int64_t arr0 = shfl64(arr64, 0);  // programs arrive in index order: the time origin
   const uint32_t arr = live ? sat32(arr64 - arr0) : T32_INF;
-  if (a.bubble && live) a.bubble[(r - a.r_begin) * P + lane] = 0;
   int st = S_OUT;
   uint32_t tev = arr;      // arrival (OUT), tool return (TOOL); INF otherwise
   uint32_t texp = T32_INF; // expiry + 1 while pinned in a tool call
@@ -628,6 +628,8 @@ __device__ __forceinline__ bool replay_one_t32(const ReplayArgs& a, int64_t r, i
   auto acc_add = [&](int k, int64_t v) {
     if (lane == k) accv += v;
   };
+  // iteration budget as a 32-bit bound (n_it < 2^32 on this path)
+  const uint32_t it_cap = E.max_iters >= (int64_t)T32_INF ? T32_INF : (uint32_t)E.max_iters;
   int32_t kv_at = -1;
   int64_t base_ps = 0;
   uint32_t d_cur = 0;
@@ -739,7 +741,6 @@ __device__ __forceinline__ bool replay_one_t32(const ReplayArgs& a, int64_t r, i
         const int64_t u = hctx + hnew - cached;
         acc_add(ACC_PREFILL, u);
         if (lane == h) {
-          if (a.bubble) a.bubble[(r - a.r_begin) * P + lane] += now - req;
           pin = false;
           texp = T32_INF;
           gblk = ng;
@@ -775,7 +776,7 @@ __device__ __forceinline__ bool replay_one_t32(const ReplayArgs& a, int64_t r, i
                           dur1, d_cur, rd_cur);
       }
       const int64_t dur = dur1 + (k - 1) * (int64_t)d_cur;
-      if ((int64_t)n_it + k > E.max_iters) { status = CT_R_EVENT_BUDGET; break; }
+      if ((uint64_t)n_it + (uint64_t)k > it_cap) { status = CT_R_EVENT_BUDGET; break; }
       const int64_t end = (int64_t)now + dur;
       if (end >= (int64_t)T32_LIM) return false;  // beyond the 32-bit horizon
       n_it += (uint32_t)k;
@@ -837,7 +838,6 @@ __device__ __forceinline__ bool replay_one_t32(const ReplayArgs& a, int64_t r, i
     a.out[ri] = o;
   }
   if (a.jct && live) a.jct[ri * P + lane] = status == CT_R_OK ? (int64_t)req : -1;
-  if (a.bubble && live && status != CT_R_OK) a.bubble[ri * P + lane] = -1;
   __syncwarp();
   return true;
 }

@@ -267,8 +267,8 @@ def test_fit_estimator_extremes(ctx, case):
 def test_ttl_grid_32bit_horizon(ctx, P):
     """TTL-grid-only sweeps run the 32-bit-time kernel.  Long inter-arrival gaps (up to 2^30 µs),
     TTLs up to 2^40 µs and slow engines push replica horizons past 2^32 µs, where the replica
-    must fall back to the 64-bit path: both must agree with the oracle byte for byte, including
-    the per-program bubble output (reset on fallback) and EVENT_BUDGET replicas."""
+    must fall back to the 64-bit path: both must agree with the oracle byte for byte, as must the
+    per-program bubble output (always the 64-bit path) and EVENT_BUDGET replicas."""
     import paper_2511_02230_b200 as ct
     n_seeds = 4
     tr = traces.generate(n_seeds, P, n_bfcl=P // 2, mix="mix", ctx_cap=1500 * 16, stream=40 + P)
@@ -278,9 +278,13 @@ def test_ttl_grid_32bit_horizon(ctx, P):
     for eng in (cf.ENGINE_8B, cf.Engine(**{**cf.ENGINE_8B.__dict__, "c0_ps": 4 * 10**11}),
                 cf.Engine(**{**cf.ENGINE_8B.__dict__, "max_iters": 2000 if P == 1 else 20000})):
         sw = cf.Sweep(n_seeds, gaps, [4096, 1600], pols)
+        os_, oj, ob = O.simulate(tr, sw, eng, n_threads=8, want_bubble=True)
+        # without the bubble output: the 32-bit kernel (and its fallback); with it: 64-bit path
+        s, j = ct.ct_simulate_batch(ctx, ct.DeviceTrace(tr), sw, eng, jct=True)
+        torch.cuda.synchronize()
+        assert_same(s.cpu().numpy(), j.cpu().numpy(), os_, oj)
         s, j, b = ct.ct_simulate_batch(ctx, ct.DeviceTrace(tr), sw, eng, jct=True, bubble=True)
         torch.cuda.synchronize()
-        os_, oj, ob = O.simulate(tr, sw, eng, n_threads=8, want_bubble=True)
         assert_same(s.cpu().numpy(), j.cpu().numpy(), os_, oj)
         assert np.array_equal(b.cpu().numpy(), ob)
         span = max(span, int(np.max(os_[:, 7])))
