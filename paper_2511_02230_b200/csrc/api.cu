@@ -263,8 +263,13 @@ int ct_simulate_batch_ex(ct_ctx* c, const ct_trace_set* tr, const ct_sweep* sw,
     for (size_t i = 0; i < n_pol; ++i) n_fast += ct::fast_policy(sw->policies[i], E) ? 1 : 0;
   int n_prog = 0;
   for (size_t i = 0; i < n_pol; ++i) n_prog += ct::prog_policy(sw->policies[i], E) ? 1 : 0;
-  const int mode = growth ? 0
-                   : ns == 1 ? (n_fast == 0 ? 0 : (n_fast == (int)n_pol ? 1 : 2))
+  // P <= 32 32-bit-time kernels need d < 2^31 µs (a.d32); see replay.cu MODE
+  const int n_prog32 = a.d32 ? n_prog : 0;
+  const int mode = growth    ? 0
+                   : ns == 1 ? (n_fast == (int)n_pol     ? 1
+                                : n_prog32 == (int)n_pol ? 3
+                                : n_prog32 > 0           ? 2
+                                                         : 0)
                              : (n_prog == (int)n_pol ? 1 : 0);
   const int wpb = 4;
   a.smem_per_warp = ct::replay_smem_per_warp(ns, F, growth, mode);

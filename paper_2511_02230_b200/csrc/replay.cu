@@ -577,7 +577,12 @@ __device__ __forceinline__ uint32_t sat32(int64_t v) {  // v >= 0
   return v >= (int64_t)T32_LIM ? T32_LIM : (uint32_t)v;
 }
 
-__device__ __forceinline__ bool replay_one_t32(const ReplayArgs& a, int64_t r, int lane) {
+// STATS = false: the TTL-grid class (fast_policy); STATS = true: the program-FCFS class with
+// the estimator (prog32_policy: EVICT, FIXED with a threshold, PAPER CalcTTL, FITTED), whose
+// statistic rows live in shared memory as on the 64-bit path.
+template <bool STATS>
+__device__ __forceinline__ bool replay_one_t32(const ReplayArgs& a, int64_t r, Stat* stats,
+                                               int lane) {
   const int P = a.P;
   const int64_t npol = a.n_pol, nkv = a.n_kv, nrate = a.n_rate;
   const int pol_i = (int)(r % npol);
@@ -585,8 +590,17 @@ __device__ __forceinline__ bool replay_one_t32(const ReplayArgs& a, int64_t r, i
   const int rate_i = (int)((r / (npol * nkv)) % nrate);
   const int64_t seed = r / (npol * nkv * nrate);
   const ct_policy* polp = a.pols + pol_i;
-  // FIXED with CT_ALWAYS pins for t_pin; EVICT never pins (fast_policy)
-  const int64_t ttl = polp->pause == CT_PAUSE_FIXED ? polp->t_pin_us : 0;
+  // TTL-grid class: FIXED with CT_ALWAYS pins for t_pin; EVICT never pins (fast_policy)
+  const int pause = polp->pause;
+  const int64_t ttl_fixed = pause == CT_PAUSE_FIXED ? polp->t_pin_us : 0;
+  const int F = a.F;
+  const ct_estimator_params& est = a.est;
+  const bool need_stats =
+      STATS && (pause == CT_PAUSE_PAPER || (pause == CT_PAUSE_FIXED && polp->t_thresh_us != CT_ALWAYS));
+  if (need_stats) {
+    for (int i = lane; i < 4 * (F + 1); i += 32) ((int64_t*)stats)[i] = 0;
+    __syncwarp();
+  }
   const int64_t gap = a.gap[rate_i];
   const ct_engine_params& E = a.eng;
   DivMagic bsm;
@@ -656,6 +670,29 @@ __device__ __forceinline__ bool replay_one_t32(const ReplayArgs& a, int64_t r, i
         if (xd) { gblk = 0; pin = false; texp = T32_INF; }
       }
       const bool due = tev <= now;
+      if (need_stats) {  // estimator rows: Δ_obs = dur of the finished turn's tool, clamped (R5)
+        uint32_t mr = __ballot_sync(FULL_MASK, due && st == S_TOOL);
+        while (mr) {
+          const int p = __ffs(mr) - 1;
+          mr &= mr - 1;
+          const int f = __shfl_sync(FULL_MASK, rec.z, p);
+          const int64_t x = min((int64_t)__shfl_sync(FULL_MASK, rec.w, p), est.b_us);
+          const uint64_t x2 = (uint64_t)x * (uint64_t)x;
+          if (lane == 0) {
+            Stat* rows[2] = {&stats[F], &stats[f]};
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+              Stat* q = rows[k];
+              q->n += 1;
+              q->s1 += x;
+              const uint64_t lo = q->s2lo + x2;
+              q->s2hi += (lo < x2);
+              q->s2lo = lo;
+            }
+          }
+          __syncwarp();
+        }
+      }
       if (due && st == S_TOOL) {  // ToolReturn == OnRequestArrive
         ++turn;
         rec = __ldg((const int4*)a.turns + turn0 + turn);
@@ -690,8 +727,22 @@ __device__ __forceinline__ bool replay_one_t32(const ReplayArgs& a, int64_t r, i
           ++D;
           turns_done += pn;
         } else {
+          int64_t ttl = ttl_fixed;
+          if (STATS) {
+            const int ptool = __shfl_sync(FULL_MASK, rec.z, p);
+            if (pause == CT_PAUSE_FIXED) {
+              ttl = simplified_ttl(stats[F], stats[ptool], est, polp->t_pin_us, polp->t_thresh_us);
+            } else if (pause == CT_PAUSE_PAPER) {
+              ttl = calc_ttl(stats[F], stats[ptool], est, D, turns_done);
+            } else if (pause == CT_PAUSE_FITTED) {
+              ttl = __ldg(&a.fitted[(int64_t)ptool * a.J + min(pt, a.J - 1)]);
+            }
+          }
           if (ttl > 0) {  // pin_request only if TTL != 0
-            if (lane == p) { pin = true; texp = sat32((int64_t)now + ttl + 1); }
+            if (lane == p) {
+              pin = true;
+              texp = ttl >= (int64_t)T32_LIM ? T32_LIM : sat32((int64_t)now + ttl + 1);
+            }
           } else {  // evict
             free_blk += pg;
             if (lane == p) { gblk = 0; pin = false; texp = T32_INF; }
@@ -1637,9 +1688,11 @@ __device__ __forceinline__ void replay_one_ns(const ReplayArgs& a, int64_t r, un
 
 // VLLM: the vLLM engine of NEXT-2 (KV growth, chunked prefill), always through the
 // shared-memory path (also P <= 32).
-// MODE (default engine): P <= 32: 0 every policy generic, 1 every policy in the TTL-grid class
-// (the specialised replay only: 3x smaller code, no register spills), 2 mixed (per replica);
-// P > 32: 0 generic, 1 every policy in the program-FCFS class.
+// MODE (default engine): P <= 32: 0 every policy generic; 1 every policy in the TTL-grid class
+// (32-bit times, fallback to the 64-bit TTL-grid path); 3 every policy in the program-FCFS class
+// (32-bit times with the estimator, fallback to the generic path); 2 mixed: program-FCFS-class
+// replicas as in 3, the others generic.  P > 32: 0 generic, 1 every policy in the program-FCFS
+// class.
 template <int NS, int MINB, bool VLLM = false, int MODE = 0>
 __global__ void __launch_bounds__(128, MINB) replay_kernel(ReplayArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -1652,8 +1705,10 @@ __global__ void __launch_bounds__(128, MINB) replay_kernel(ReplayArgs a) {
     const int64_t r = a.r_begin + (int64_t)idx;
     if (r >= a.r_end) break;
     if (NS == 1 && !VLLM) {
-      if (MODE == 1 || (MODE == 2 && fast_policy(a.pols[(int)(r % a.n_pol)], a.eng))) {
-        if (!replay_one_t32(a, r, lane)) replay_one_w32<true>(a, r, (Stat*)wm, lane);
+      if (MODE == 1) {
+        if (!replay_one_t32<false>(a, r, (Stat*)wm, lane)) replay_one_w32<true>(a, r, (Stat*)wm, lane);
+      } else if (MODE == 3 || (MODE == 2 && prog_policy(a.pols[(int)(r % a.n_pol)], a.eng))) {
+        if (!replay_one_t32<true>(a, r, (Stat*)wm, lane)) replay_one_w32<false>(a, r, (Stat*)wm, lane);
       } else {
         replay_one_w32<false>(a, r, (Stat*)wm, lane);
       }
@@ -1701,6 +1756,7 @@ static void* pick(int ns, bool growth, int mode) {
         }
       }
       if (mode == 2) return (void*)replay_kernel<1, 8, false, 2>;
+      if (mode == 3) return (void*)replay_kernel<1, 8, false, 3>;
       switch (minb()) {
         case 6: return (void*)replay_kernel<1, 6>;
         case 10: return (void*)replay_kernel<1, 10>;

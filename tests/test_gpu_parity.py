@@ -263,8 +263,9 @@ def test_fit_estimator_extremes(ctx, case):
         assert np.array_equal(x, y), (name, case, x, y)
 
 
+@pytest.mark.parametrize("kind", ["grid", "prog"])
 @pytest.mark.parametrize("P", [1, 17, 32])
-def test_ttl_grid_32bit_horizon(ctx, P):
+def test_ttl_grid_32bit_horizon(ctx, P, kind):
     """TTL-grid-only sweeps run the 32-bit-time kernel.  Long inter-arrival gaps (up to 2^30 µs),
     TTLs up to 2^40 µs and slow engines push replica horizons past 2^32 µs, where the replica
     must fall back to the 64-bit path: both must agree with the oracle byte for byte, as must the
@@ -274,10 +275,15 @@ def test_ttl_grid_32bit_horizon(ctx, P):
     tr = traces.generate(n_seeds, P, n_bfcl=P // 2, mix="mix", ctx_cap=1500 * 16, stream=40 + P)
     gaps = [1 << 20, 300_000_000, (1 << 30) - 1]
     pols = [cf.ttl_grid(t) for t in (0, 1, 2_000_000, 600_000_000, 1 << 40)] + [cf.PROG_FCFS]
+    fitted = None
+    if kind == "prog":  # program-FCFS class with the estimator (32-bit kernel MODE 3)
+        fitted = np.tile(np.array([[0, 200_000, 3_000_000, 1 << 40]], np.int64), (tr.n_tools, 1))
+        pols = [cf.CONTINUUM, cf.simplified(5_000_000, 2_000_000), cf.simplified(1 << 40, 10**9),
+                cf.CONTINUUM_FITTED, cf.ttl_grid(2_000_000), cf.PROG_FCFS]
     span, budget = 0, False
     for eng in (cf.ENGINE_8B, cf.Engine(**{**cf.ENGINE_8B.__dict__, "c0_ps": 4 * 10**11}),
                 cf.Engine(**{**cf.ENGINE_8B.__dict__, "max_iters": 2000 if P == 1 else 20000})):
-        sw = cf.Sweep(n_seeds, gaps, [4096, 1600], pols)
+        sw = cf.Sweep(n_seeds, gaps, [4096, 1600], pols, fitted=fitted)
         os_, oj, ob = O.simulate(tr, sw, eng, n_threads=8, want_bubble=True)
         # without the bubble output: the 32-bit kernel (and its fallback); with it: 64-bit path
         s, j = ct.ct_simulate_batch(ctx, ct.DeviceTrace(tr), sw, eng, jct=True)

@@ -1,3 +1,4 @@
 #!/bin/bash
-# A/B of library variants built in tools/var_*.so (CT_LIB_PATH override), cfg3 slice, 2 rounds.
-for i in 1 2; do for v in "$@"; do echo -n "$v "; CT_LIB_PATH=tools/var_$v.so python tools/prof_kernels.py replay cfg3 64 | tail -1 | cut -c1-90; done; done
+# A/B of library variants built in tools/var_*.so (CT_LIB_PATH override); args: workload seeds variants...
+W=$1; S=$2; shift 2
+for i in 1 2; do for v in "$@"; do echo -n "$v "; CT_LIB_PATH=tools/var_$v.so python tools/prof_kernels.py replay $W $S | tail -1 | cut -c1-90; done; done

@@ -36,7 +36,14 @@ def main():
     else:
         name = sys.argv[2] if len(sys.argv) > 2 else "cfg3"
         seeds = int(sys.argv[3]) if len(sys.argv) > 3 else 16
-        w = {"cfg2": cf.config2, "cfg3": cf.config3, "cfg5": cf.config5}[name](n_seeds=seeds)
+        if name == "cont":  # cfg3's workload under program-FCFS-class policies with the estimator
+            w = cf.config3(n_seeds=seeds)
+            pols = [cf.CONTINUUM, cf.simplified(5_000_000, 2_000_000), cf.PROG_FCFS] + \
+                [cf.ttl_grid(t) for t in cf.ttl_axis(13, 100_000, 60_000_000)[1:]]
+            w = cf.Workload("cont", w.trace, cf.Sweep(seeds, cf.rate_axis(16), [8192], pols),
+                            w.engine, "cfg3 trace, 16 program-FCFS policies")
+        else:
+            w = {"cfg2": cf.config2, "cfg3": cf.config3, "cfg5": cf.config5}[name](n_seeds=seeds)
         dt = ct.DeviceTrace(w.trace)
         for i in range(2):
             e0.record()
