@@ -31,6 +31,8 @@ struct ct_ctx {
   size_t h_out_cap = 0;
   void* h_jct = nullptr;
   size_t h_jct_cap = 0;
+  void* fb = nullptr;  // MODE 4 fallback replica list
+  size_t fb_cap = 0;
   void* syn = nullptr;  // synthesis: tables | cdf | class | per-program class | seed totals | blocks
   size_t syn_cap = 0;
   ct_launch_info last{};
@@ -118,7 +120,8 @@ int ct_ctx_create(int device, ct_ctx** out) {
 
 int ct_ctx_destroy(ct_ctx* c) {
   if (!c) return CT_OK;
-  void* ps[] = {c->counter, c->axes, c->fit, c->chunks, c->h_progs, c->h_turns, c->h_out, c->h_jct, c->syn};
+  void* ps[] = {c->counter, c->axes, c->fit, c->chunks, c->h_progs, c->h_turns, c->h_out, c->h_jct, c->syn,
+                c->fb};
   for (void* p : ps)
     if (p) cudaFree(p);
   for (auto e : c->ev)
@@ -272,15 +275,41 @@ int ct_simulate_batch_ex(ct_ctx* c, const ct_trace_set* tr, const ct_sweep* sw,
                                                          : 0)
                              : (n_prog == (int)n_pol ? 1 : 0);
   const int wpb = 4;
-  a.smem_per_warp = ct::replay_smem_per_warp(ns, F, growth, mode);
+  a.from_list = 0;
+  a.fb_list = nullptr;
+  a.fb_count = c->counter + 1;
+  // P > 32, program-FCFS class: the 32-bit kernel (MODE 4) first, then MODE 1 over the replicas
+  // it handed back (horizon reached, or the bubble output requested)
+  const bool ns32 = ns > 1 && mode == 1 && a.d32 && !a.bubble;
+  if (ns32) {
+    rc = ensure(&c->fb, &c->fb_cap, 8 * (size_t)(re - rb));
+    if (rc) return rc;
+    a.fb_list = (int64_t*)c->fb;
+    CT_CUDA(cudaMemsetAsync(c->counter + 1, 0, 16, s));
+  }
+  const int mode1 = ns32 ? 4 : mode;
+  a.smem_per_warp = ns32 ? ct::replay_ns32_smem_per_warp(ns, F)
+                         : ct::replay_smem_per_warp(ns, F, growth, mode);
   const int smem = a.smem_per_warp * wpb;
-  int occ = ct::replay_occupancy(ns, growth, mode, wpb, smem);
+  int occ = ct::replay_occupancy(ns, growth, mode1, wpb, smem);
   if (occ < 1) return fail(CT_ECUDA, "replay kernel cannot be resident (smem %d)", smem);
   const int64_t need_blocks = (re - rb + wpb - 1) / wpb;
   const int grid = (int)std::min<int64_t>((int64_t)c->sm_count * occ, need_blocks);
   if (c->timing) CT_CUDA(cudaEventRecord(c->ev[0], s));
-  cudaError_t e = ct::launch_replay(a, ns, growth, mode, wpb, grid, s);
+  cudaError_t e = ct::launch_replay(a, ns, growth, mode1, wpb, grid, s);
   if (e != cudaSuccess) return cuda_fail(e, "replay launch");
+  if (ns32) {
+    ct::ReplayArgs b = a;
+    b.from_list = 1;
+    b.counter = c->counter + 2;
+    b.smem_per_warp = ct::replay_smem_per_warp(ns, F, growth, mode);
+    const int smem2 = b.smem_per_warp * wpb;
+    const int occ2 = ct::replay_occupancy(ns, growth, mode, wpb, smem2);
+    if (occ2 < 1) return fail(CT_ECUDA, "replay kernel cannot be resident (smem %d)", smem2);
+    const int grid2 = (int)std::min<int64_t>((int64_t)c->sm_count * occ2, need_blocks);
+    e = ct::launch_replay(b, ns, growth, mode, wpb, grid2, s);
+    if (e != cudaSuccess) return cuda_fail(e, "replay fallback launch");
+  }
   if (c->timing) CT_CUDA(cudaEventRecord(c->ev[1], s));
   c->replay_timed = c->timing;
   c->last.grid = grid;
@@ -288,7 +317,7 @@ int ct_simulate_batch_ex(ct_ctx* c, const ct_trace_set* tr, const ct_sweep* sw,
   c->last.warps_per_block = wpb;
   c->last.slots_per_lane = ns;
   c->last.smem_per_block = smem;
-  c->last.launches = 1;
+  c->last.launches = ns32 ? 2 : 1;
   return CT_OK;
 }
 

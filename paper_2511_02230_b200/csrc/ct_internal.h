@@ -27,6 +27,9 @@ struct ReplayArgs {
   int smem_per_warp;
   uint64_t bs_magic;  // ceil(2^64 / bs) (0 when bs == 1)
   int d32;            // every no-prefill iteration is below 2^31 µs (32-bit macro-step division)
+  int from_list;      // replay the replicas fb_list[0 .. *fb_count) instead of [r_begin, r_end)
+  int64_t* fb_list;   // MODE 4: replicas handed to the 64-bit kernel (horizon, bubble output)
+  unsigned long long* fb_count;
 };
 
 // The TTL-grid policy class, for which the P <= 32 replay has a specialised path: program
@@ -47,6 +50,8 @@ inline __host__ __device__ bool prog_policy(const ct_policy& p, const ct_engine_
 // Bytes of shared memory one replica (one warp) needs for `ns` slots per lane and F tools.
 // KV growth (NEXT-2) always runs the shared-memory path, also for P <= 32.
 int replay_smem_per_warp(int ns, int F, bool growth, int mode);
+// Same for the 32-bit program-FCFS kernel (MODE 4, ns >= 2).
+int replay_ns32_smem_per_warp(int ns, int F);
 // Launch the persistent replay kernel; returns the cudaError of the launch.
 // mode (ns == 1, default engine): 0 generic, 1 all policies fast_policy(), 2 mixed.
 cudaError_t launch_replay(const ReplayArgs& a, int ns, bool growth, int mode, int warps_per_block,

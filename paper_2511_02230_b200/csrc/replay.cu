@@ -1686,13 +1686,452 @@ __device__ __forceinline__ void replay_one_ns(const ReplayArgs& a, int64_t r, un
   __syncwarp();
 }
 
+// -----------------------------------------------------------------------------------------------
+// 32 < P <= 256, program-FCFS class (prog_policy), default engine, with 32-bit replica-relative
+// times (as replay_one_t32: µs since the first arrival, saturated at T32_LIM; iteration indices
+// stay below the time).  28 B of shared memory per program (tev, texp, req/JCT, fin as u32;
+// ctx, gblk, turn), so 28 warps (all 4,096 replicas of cfg2) fit on the GPU at once.  Returns
+// false, before writing any output, when the replica reaches the horizon or asks for the
+// bubble output; the caller queues it for the 64-bit kernel (replay_one_ns<NS, false, true>),
+// which replays it from scratch.  Otherwise identical to that path step for step.
+int replay_ns32_smem_per_warp(int ns, int F) {
+  return ((28 * 32 * ns + 15) & ~15) + ((32 * (F + 1) + 48 + 15) & ~15);
+}
+
+template <int NS>
+__device__ __forceinline__ bool replay_one_ns32(const ReplayArgs& a, int64_t r,
+                                                unsigned char* wm, int lane) {
+  constexpr int PM = 32 * NS;
+  if (a.bubble) return false;  // the per-program bubble output runs on the 64-bit path
+  uint32_t* tev = (uint32_t*)wm;   // tool return, INF otherwise
+  uint32_t* texp = tev + PM;       // expiry + 1 while pinned in a tool call, INF otherwise
+  uint32_t* req = texp + PM;       // request arrival; JCT once done
+  uint32_t* fin = req + PM;        // finishing iteration while running, INF otherwise
+  int32_t* ctx = (int32_t*)(fin + PM);
+  int32_t* gblk = ctx + PM;
+  int32_t* turn = gblk + PM;
+  Stat* stats = (Stat*)(wm + ((28 * PM + 15) & ~15));
+
+  const int P = a.P, F = a.F;
+  const int64_t npol = a.n_pol, nkv = a.n_kv, nrate = a.n_rate;
+  const int pol_i = (int)(r % npol);
+  const int kv_i = (int)((r / npol) % nkv);
+  const int rate_i = (int)((r / (npol * nkv)) % nrate);
+  const int64_t seed = r / (npol * nkv * nrate);
+  const ct_policy* polp = a.pols + pol_i;
+  const int pause = polp->pause;
+  const int64_t gap = a.gap[rate_i];
+  const ct_program* prog = a.progs + seed * P;
+  const ct_engine_params& E = a.eng;
+  const ct_estimator_params& est = a.est;
+  const int64_t bs = E.bs;
+  DivMagic bsm;
+  bsm.mhi = (uint32_t)(a.bs_magic >> 32);
+  bsm.mlo = (uint32_t)a.bs_magic;
+  bsm.dm1 = (uint32_t)(bs - 1);
+  bsm.ident = bs == 1 ? 1u : 0u;
+  const bool need_stats = pause == CT_PAUSE_PAPER ||
+                          (pause == CT_PAUSE_FIXED && polp->t_thresh_us != CT_ALWAYS);
+
+#pragma unroll
+  for (int s = 0; s < NS; ++s) {
+    const int p = lane + 32 * s;
+    tev[p] = T32_INF;
+    texp[p] = T32_INF;
+    req[p] = 0;
+    fin[p] = T32_INF;
+    ctx[p] = 0;
+    gblk[p] = 0;
+    turn[p] = 0;
+  }
+  if (need_stats)
+    for (int i = lane; i < 4 * (F + 1); i += 32) ((int64_t*)stats)[i] = 0;
+  __syncwarp();
+
+  uint32_t qb = 0, pb = 0, rb = 0, tb = 0;  // per-lane sets over this lane's slots
+  uint32_t lev = T32_INF, lexp = T32_INF, fmin = T32_INF;  // cached minima over this lane's slots
+  auto own = [&](int p) { return lane == (p & 31); };
+  auto bit = [&](int p) { return 1u << (p >> 5); };
+  auto turn_rec = [&](int p, int t) -> int4 { return __ldg(&a.turns[prog[p].turn0 + t]); };
+  const int64_t arr0 = (prog[0].arr_q * gap) >> 20;  // programs arrive in index order: origin
+  auto arrival = [&](int i) -> uint32_t { return sat32(((prog[i].arr_q * gap) >> 20) - arr0); };
+  auto for_each_set = [&](uint32_t m, auto&& fn) {
+    uint32_t slots = __reduce_or_sync(FULL_MASK, m);
+    while (slots) {
+      const int s = __ffs(slots) - 1;
+      slots &= slots - 1;
+      uint32_t b = __ballot_sync(FULL_MASK, (m >> s) & 1u);
+      while (b) {
+        const int p = 32 * s + __ffs(b) - 1;
+        b &= b - 1;
+        fn(p);
+      }
+    }
+  };
+  auto rescan_lev = [&]() {
+    uint32_t m = T32_INF;
+#pragma unroll
+    for (int s = 0; s < NS; ++s) m = min(m, tev[lane + 32 * s]);
+    lev = m;
+  };
+  auto rescan_lexp = [&]() {
+    uint32_t m = T32_INF;
+#pragma unroll
+    for (int s = 0; s < NS; ++s) m = min(m, texp[lane + 32 * s]);
+    lexp = m;
+  };
+  auto rescan_fmin = [&]() {
+    uint32_t m = T32_INF;
+#pragma unroll
+    for (int s = 0; s < NS; ++s) m = min(m, fin[lane + 32 * s]);
+    fmin = m;
+  };
+
+  uint32_t now = 0, iter_end = 0, n_it = 0;
+  const uint32_t it_cap = E.max_iters >= (int64_t)T32_INF ? T32_INF : (uint32_t)E.max_iters;
+  bool in_flight = false;
+  int64_t free_blk = a.kv[kv_i];
+  int next_arr = 0;
+  uint32_t t_arr = 0;  // program 0 arrives at the origin
+  int32_t D = 0, turns_done = 0;
+  int n_run = 0;
+  int64_t kv_sum = 0, pf = 0;
+  int status = CT_R_OK;
+  int64_t kv_at = -1, base_ps = 0;
+  uint32_t d_cur = 0;
+  float rd_cur = 0.0f;
+  int64_t accv = 0;  // lane k holds summary counter k (ACC_*)
+  auto acc_add = [&](int k, int64_t v) {
+    if (lane == k) accv += v;
+  };
+
+  // evict(v): free its GPU blocks; unpin.  Uniform.
+  auto evict_unpin = [&](int v) {
+    free_blk += gblk[v];
+    __syncwarp();  // every lane has read v's fields before the owner rewrites them
+    if (own(v)) {
+      gblk[v] = 0;
+      if (pb & bit(v)) {
+        pb &= ~bit(v);
+        if (texp[v] != T32_INF) { texp[v] = T32_INF; rescan_lexp(); }
+      }
+    }
+    __syncwarp();
+  };
+
+  for (;;) {
+    uint32_t t;
+    if (in_flight) {
+      t = iter_end;
+    } else {
+      t = min(__reduce_min_sync(FULL_MASK, min(lev, lexp)), t_arr);
+      if (t == T32_INF) break;
+    }
+    if (t >= T32_LIM) return false;  // beyond the 32-bit horizon: 64-bit kernel
+    now = t;
+
+    // PinExpiry (EAGER): first µs with now > expiry while not in Q (R4/R15); it
+    // precedes the program's own tool return at the same µs (R1)
+    if (__any_sync(FULL_MASK, lexp <= now)) {
+      uint32_t me = 0;
+      if (lexp <= now) {
+#pragma unroll
+        for (int s = 0; s < NS; ++s) {
+          const int p = lane + 32 * s;
+          me |= (texp[p] <= now && texp[p] <= tev[p] ? 1u : 0u) << s;
+        }
+      }
+      acc_add(ACC_EXP, __reduce_add_sync(FULL_MASK, (uint32_t)__popc(me)));
+      for_each_set(me, [&](int p) { evict_unpin(p); });
+    }
+    // ToolReturn (OnRequestArrive of a seen program)
+    if (__any_sync(FULL_MASK, lev <= now)) {
+      uint32_t md = 0;
+      if (lev <= now) {
+#pragma unroll
+        for (int s = 0; s < NS; ++s) md |= (tev[lane + 32 * s] <= now ? 1u : 0u) << s;
+      }
+      const uint32_t mret = md & tb;
+      if (need_stats) {
+        for_each_set(mret, [&](int p) {  // estimator rows: Δ_obs = dur of the finished turn (R5)
+          const int4 tr = turn_rec(p, turn[p]);
+          const int64_t x = min((int64_t)tr.w, est.b_us);
+          const uint64_t x2 = (uint64_t)x * (uint64_t)x;
+          if (lane == 0) {
+            Stat* rows[2] = {&stats[F], &stats[tr.z]};
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+              Stat* q = rows[k];
+              q->n += 1;
+              q->s1 += x;
+              const uint64_t lo = q->s2lo + x2;
+              q->s2hi += (lo < x2);
+              q->s2lo = lo;
+            }
+          }
+          __syncwarp();
+        });
+      }
+      if (md) {
+        bool rescan_e = false;
+#pragma unroll
+        for (int s = 0; s < NS; ++s) {
+          const int p = lane + 32 * s;
+          if ((mret >> s) & 1u) {
+            turn[p] += 1;
+            req[p] = tev[p];  // the event's own instant
+            tev[p] = T32_INF;
+            if (texp[p] != T32_INF) { texp[p] = T32_INF; rescan_e = true; }  // retained pin
+          }
+        }
+        qb |= mret;
+        tb &= ~mret;
+        rescan_lev();
+        if (rescan_e) rescan_lexp();
+      }
+      __syncwarp();
+    }
+    // ProgramArrival (programs arrive in index order)
+    while (t_arr <= now) {
+      const int p = next_arr;
+      if (own(p)) { qb |= bit(p); req[p] = t_arr; }
+      ++next_arr;
+      t_arr = next_arr < P ? arrival(next_arr) : T32_INF;
+    }
+    __syncwarp();
+
+    // IterationEnd: requests whose last token was emitted finish, in index order (C-6)
+    if (in_flight && iter_end == now) {
+      in_flight = false;
+      uint32_t mf = 0;
+      if (fmin == n_it) {
+#pragma unroll
+        for (int s = 0; s < NS; ++s) mf |= (fin[lane + 32 * s] == n_it ? 1u : 0u) << s;
+      }
+      for_each_set(mf, [&](int p) {
+        // OnRequestFinish
+        const int tp = turn[p];
+        const int4 tr = turn_rec(p, tp);
+        const int nctx = ctx[p] + tr.x + tr.y;
+        const int64_t g = gblk[p];
+        --n_run;
+        kv_sum -= g;
+        __syncwarp();
+        if (own(p)) { rb &= ~bit(p); fin[p] = T32_INF; ctx[p] = nctx; }
+        __syncwarp();
+        const int nt = prog[p].nturns;
+        if (tp == nt - 1) {  // last request: free its KV, the program completes
+          free_blk += g;
+          __syncwarp();
+          if (own(p)) { gblk[p] = 0; req[p] = now - arrival(p); }
+          ++D;
+          turns_done += nt;
+          __syncwarp();
+        } else {
+          const int f = tr.z;
+          int64_t ttl = 0;
+          if (pause == CT_PAUSE_FIXED) {
+            ttl = simplified_ttl(stats[F], stats[f], est, polp->t_pin_us, polp->t_thresh_us);
+          } else if (pause == CT_PAUSE_PAPER) {
+            ttl = calc_ttl(stats[F], stats[f], est, D, turns_done);
+          } else if (pause == CT_PAUSE_FITTED) {
+            ttl = __ldg(&a.fitted[(int64_t)f * a.J + min(tp, a.J - 1)]);
+          }
+          if (ttl > 0) {  // pin_request only if TTL != 0
+            if (own(p)) {
+              pb |= bit(p);
+              texp[p] = ttl >= (int64_t)T32_LIM ? T32_LIM : sat32((int64_t)now + ttl + 1);
+              lexp = min(lexp, texp[p]);
+            }
+          } else {
+            evict_unpin(p);
+          }
+          if (own(p)) { tev[p] = sat32((int64_t)now + tr.w); lev = min(lev, tev[p]); tb |= bit(p); }
+          __syncwarp();
+        }
+      });
+      if (mf) rescan_fmin();
+    }
+    if (in_flight) continue;  // mid-iteration: events only mutate Q / stats / pins (R2)
+
+    // ---- scheduling point (R3): admit loop (victims PAPER.md:645-655) -----
+    int admitted = 0;
+    bool stable = true;
+    if (__any_sync(FULL_MASK, qb != 0)) {
+      for (;;) {
+        if (!__any_sync(FULL_MASK, qb != 0)) break;
+        if (n_run >= E.max_batch) break;
+        // lowest index among pinned-queued, else queued
+        uint32_t sel = qb & pb;
+        uint32_t slots = __reduce_or_sync(FULL_MASK, sel);
+        if (!slots) { sel = qb; slots = __reduce_or_sync(FULL_MASK, sel); }
+        const int s0 = __ffs(slots) - 1;
+        const int h = 32 * s0 + __ffs(__ballot_sync(FULL_MASK, (sel >> s0) & 1u)) - 1;
+        const int4 tr = turn_rec(h, turn[h]);
+        const int64_t hctx = ctx[h];
+        const int64_t hg = gblk[h];
+        const int64_t need = (int64_t)ceil_div_magic((uint32_t)(hctx + tr.x + tr.y), bsm) - hg;
+        if (need > free_blk && admitted == 0) {
+          while (need > free_blk) {  // victims: latest program arrival first, never the head
+            const uint32_t cand = pb & ~(own(h) ? bit(h) : 0u);
+            const uint32_t vs = __reduce_or_sync(FULL_MASK, cand);
+            if (!vs) break;
+            const int s1 = 31 - __clz(vs);
+            const int v = 32 * s1 + 31 - __clz(__ballot_sync(FULL_MASK, (cand >> s1) & 1u));
+            evict_unpin(v);
+            acc_add(ACC_VICT, 1);
+          }
+        }
+        if (need > free_blk) {  // HOL break
+          if (admitted > 0 && __reduce_or_sync(FULL_MASK, pb & ~(own(h) ? bit(h) : 0u)))
+            stable = false;
+          break;
+        }
+        // issue h
+        free_blk -= need;
+        const int32_t ng = (int32_t)(hg + need);
+        acc_add(ACC_BUBBLE, (int64_t)(now - req[h]));
+        const bool hp = (__shfl_sync(FULL_MASK, pb, h & 31) >> (h >> 5)) & 1u;
+        const int64_t cached = hp ? hctx : 0;
+        if (hp) acc_add(ACC_HITS, 1);
+        acc_add(ACC_RECOMP, hctx - cached);
+        const int64_t u = hctx + tr.x - cached;
+        acc_add(ACC_PREFILL, u);
+        __syncwarp();  // every lane has read h's fields before the owner rewrites them
+        if (own(h)) {
+          qb &= ~bit(h);
+          pb &= ~bit(h);  // a queued pin has no pending expiry (cleared at its return)
+          gblk[h] = ng;
+          rb |= bit(h);
+          fin[h] = sat32((int64_t)n_it + tr.y);
+          fmin = min(fmin, fin[h]);
+        }
+        ++n_run;
+        kv_sum += ng;
+        pf += u;
+        ++admitted;
+        __syncwarp();
+      }
+      // unschedulable: the head missed with nothing running (C-5 5c)
+      if (admitted == 0 && n_run == 0 && __any_sync(FULL_MASK, qb != 0)) {
+        status = CT_R_UNSCHEDULABLE;
+        break;
+      }
+    }
+    // start the next iteration(s) (linear cost model, R16)
+    if (n_run > 0) {
+      if (kv_sum != kv_at) {
+        kv_at = kv_sum;
+        base_ps = E.c0_ps + E.c_kv_ps * bs * kv_sum;
+        d_cur = (uint32_t)ceil_ps_to_us((uint64_t)base_ps);  // < 2^31 (host-checked)
+        rd_cur = __frcp_rn((float)d_cur);
+      }
+      const int64_t dur1 = pf > 0 ? ceil_ps_to_us((uint64_t)(base_ps + E.c_pf_ps * pf)) : d_cur;
+      pf = 0;
+      int64_t k = 1;
+      if (stable) {
+        const uint32_t mfin = __reduce_min_sync(FULL_MASK, fmin);
+        const uint32_t te = min(__reduce_min_sync(FULL_MASK, min(lev, lexp)), t_arr);
+        k = macro_iters32((int64_t)(mfin - n_it), te == T32_INF ? CT_INF64 : (int64_t)te - now,
+                          dur1, d_cur, rd_cur);
+      }
+      const int64_t dur = dur1 + (k - 1) * (int64_t)d_cur;
+      if ((uint64_t)n_it + (uint64_t)k > it_cap) { status = CT_R_EVENT_BUDGET; break; }
+      const int64_t end = (int64_t)now + dur;
+      if (end >= (int64_t)T32_LIM) return false;  // beyond the 32-bit horizon
+      n_it += (uint32_t)k;
+      iter_end = (uint32_t)end;
+      acc_add(ACC_BUSY, dur);
+      in_flight = true;
+    }
+  }
+  if (status == CT_R_OK && D != P) status = CT_R_UNSCHEDULABLE;
+
+  // ---- per-replica summary (A-8) --------------------------------------------------------------
+  __syncwarp();
+  const int64_t ri = r - a.r_begin;
+  int64_t jsum = 0, jmax = 0, p50 = 0, p99 = 0;
+  if (status == CT_R_OK) {
+    int64_t ls = 0;
+    uint32_t lm = 0;
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+      const int p = lane + 32 * s;
+      if (p < P) { ls += req[p]; lm = max(lm, req[p]); }
+    }
+    jsum = (int64_t)warp_sum_u64((uint64_t)ls);
+    jmax = __reduce_max_sync(FULL_MASK, lm);
+    // nearest rank (R20): value v with #(x < v) < rank <= #(x <= v)
+    const int r50 = (50 * P + 99) / 100, r99 = (99 * P + 99) / 100;
+    uint32_t c50 = T32_INF, c99 = T32_INF;
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+      const int p = lane + 32 * s;
+      if (p < P) {
+        const uint32_t v = req[p];
+        int lt = 0, le = 0;
+        for (int q = 0; q < P; ++q) {
+          const uint32_t x = req[q];
+          lt += x < v;
+          le += x <= v;
+        }
+        if (lt < r50 && r50 <= le) c50 = v;
+        if (lt < r99 && r99 <= le) c99 = v;
+      }
+    }
+    p50 = __reduce_min_sync(FULL_MASK, c50);
+    p99 = __reduce_min_sync(FULL_MASK, c99);
+  }
+  int64_t av[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) av[k] = shfl64(accv, k);
+  if (lane == 0) {
+    ct_replica_summary o;
+    if (status == CT_R_OK) {
+      o.status = status;
+      o.n_done = D;
+      o.turns_done = turns_done;
+      o.sum_jct_us = jsum;
+      o.max_jct_us = jmax;
+      o.p50_jct_us = p50;
+      o.p99_jct_us = p99;
+      o.sum_bubble_us = av[ACC_BUBBLE];
+      o.makespan_us = now;  // the last event processed is the last completion; origin = arr0
+      o.iterations = n_it;
+      o.busy_us = av[ACC_BUSY];
+      o.prefill_tokens = av[ACC_PREFILL];
+      o.recompute_tokens = av[ACC_RECOMP];
+      o.pin_hits = av[ACC_HITS];
+      o.pin_expiries = av[ACC_EXP];
+      o.victims = av[ACC_VICT];
+      o.reloads = av[ACC_RELOAD];
+    } else {
+      int64_t* w = (int64_t*)&o;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) w[i] = 0;
+      o.status = status;
+    }
+    a.out[ri] = o;
+  }
+  if (a.jct) {
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+      const int p = lane + 32 * s;
+      if (p < P) a.jct[ri * P + p] = status == CT_R_OK ? (int64_t)req[p] : -1;
+    }
+  }
+  __syncwarp();
+  return true;
+}
+
 // VLLM: the vLLM engine of NEXT-2 (KV growth, chunked prefill), always through the
 // shared-memory path (also P <= 32).
 // MODE (default engine): P <= 32: 0 every policy generic; 1 every policy in the TTL-grid class
 // (32-bit times, fallback to the 64-bit TTL-grid path); 3 every policy in the program-FCFS class
 // (32-bit times with the estimator, fallback to the generic path); 2 mixed: program-FCFS-class
 // replicas as in 3, the others generic.  P > 32: 0 generic, 1 every policy in the program-FCFS
-// class.
+// class; 4 every policy in the program-FCFS class with 32-bit times (replay_one_ns32), replicas
+// that reach the horizon are queued for a second launch of MODE 1 over that list (from_list).
 template <int NS, int MINB, bool VLLM = false, int MODE = 0>
 __global__ void __launch_bounds__(128, MINB) replay_kernel(ReplayArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -1702,8 +2141,14 @@ __global__ void __launch_bounds__(128, MINB) replay_kernel(ReplayArgs a) {
     unsigned long long idx = 0;
     if (lane == 0) idx = atomicAdd(a.counter, 1ull);
     idx = __shfl_sync(FULL_MASK, idx, 0);
-    const int64_t r = a.r_begin + (int64_t)idx;
-    if (r >= a.r_end) break;
+    int64_t r;
+    if (a.from_list) {  // replicas queued by a MODE 4 launch earlier on the stream
+      if (idx >= *a.fb_count) break;
+      r = a.fb_list[idx];
+    } else {
+      r = a.r_begin + (int64_t)idx;
+      if (r >= a.r_end) break;
+    }
     if (NS == 1 && !VLLM) {
       if (MODE == 1) {
         if (!replay_one_t32<false>(a, r, (Stat*)wm, lane)) replay_one_w32<true>(a, r, (Stat*)wm, lane);
@@ -1712,8 +2157,12 @@ __global__ void __launch_bounds__(128, MINB) replay_kernel(ReplayArgs a) {
       } else {
         replay_one_w32<false>(a, r, (Stat*)wm, lane);
       }
-    } else
+    } else if (MODE == 4) {
+      if (!replay_one_ns32<NS>(a, r, wm, lane) && lane == 0)
+        a.fb_list[atomicAdd(a.fb_count, 1ull)] = r;
+    } else {
       replay_one_ns<NS, VLLM, (MODE == 1)>(a, r, wm, lane);
+    }
   }
 }
 
@@ -1728,6 +2177,9 @@ static int minb() {
   return g_minb;
 }
 
+#ifndef NS32_MINB
+#define NS32_MINB 7  // 7 CTAs of 4 warps per SM: 28 warps, <= 73 registers, 28 B SMEM per program
+#endif
 #ifndef NS_PROG_MINB
 #define NS_PROG_MINB 5  // 5 CTAs of 4 warps per SM: <= 102 registers, 48 B SMEM per program
 #endif
@@ -1763,13 +2215,20 @@ static void* pick(int ns, bool growth, int mode) {
         case 12: return (void*)replay_kernel<1, 12>;
         default: return (void*)replay_kernel<1, 8>;
       }
-    case 2: return mode == 1 ? (void*)replay_kernel<2, NS_PROG_MINB, false, 1> : (void*)replay_kernel<2, 1>;
-    case 3: return mode == 1 ? (void*)replay_kernel<3, NS_PROG_MINB, false, 1> : (void*)replay_kernel<3, 1>;
-    case 4: return mode == 1 ? (void*)replay_kernel<4, NS_PROG_MINB, false, 1> : (void*)replay_kernel<4, 1>;
-    case 5: return mode == 1 ? (void*)replay_kernel<5, NS_PROG_MINB, false, 1> : (void*)replay_kernel<5, 1>;
-    case 6: return mode == 1 ? (void*)replay_kernel<6, NS_PROG_MINB, false, 1> : (void*)replay_kernel<6, 1>;
-    case 7: return mode == 1 ? (void*)replay_kernel<7, NS_PROG_MINB, false, 1> : (void*)replay_kernel<7, 1>;
-    case 8: return mode == 1 ? (void*)replay_kernel<8, NS_PROG_MINB, false, 1> : (void*)replay_kernel<8, 1>;
+    case 2: return mode == 4 ? (void*)replay_kernel<2, NS32_MINB, false, 4>
+                 : mode == 1 ? (void*)replay_kernel<2, NS_PROG_MINB, false, 1> : (void*)replay_kernel<2, 1>;
+    case 3: return mode == 4 ? (void*)replay_kernel<3, NS32_MINB, false, 4>
+                 : mode == 1 ? (void*)replay_kernel<3, NS_PROG_MINB, false, 1> : (void*)replay_kernel<3, 1>;
+    case 4: return mode == 4 ? (void*)replay_kernel<4, NS32_MINB, false, 4>
+                 : mode == 1 ? (void*)replay_kernel<4, NS_PROG_MINB, false, 1> : (void*)replay_kernel<4, 1>;
+    case 5: return mode == 4 ? (void*)replay_kernel<5, NS32_MINB, false, 4>
+                 : mode == 1 ? (void*)replay_kernel<5, NS_PROG_MINB, false, 1> : (void*)replay_kernel<5, 1>;
+    case 6: return mode == 4 ? (void*)replay_kernel<6, NS32_MINB, false, 4>
+                 : mode == 1 ? (void*)replay_kernel<6, NS_PROG_MINB, false, 1> : (void*)replay_kernel<6, 1>;
+    case 7: return mode == 4 ? (void*)replay_kernel<7, NS32_MINB, false, 4>
+                 : mode == 1 ? (void*)replay_kernel<7, NS_PROG_MINB, false, 1> : (void*)replay_kernel<7, 1>;
+    case 8: return mode == 4 ? (void*)replay_kernel<8, NS32_MINB, false, 4>
+                 : mode == 1 ? (void*)replay_kernel<8, NS_PROG_MINB, false, 1> : (void*)replay_kernel<8, 1>;
   }
   return nullptr;
 }

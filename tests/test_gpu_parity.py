@@ -264,14 +264,15 @@ def test_fit_estimator_extremes(ctx, case):
 
 
 @pytest.mark.parametrize("kind", ["grid", "prog"])
-@pytest.mark.parametrize("P", [1, 17, 32])
+@pytest.mark.parametrize("P", [1, 17, 32, 33, 70, 130])
 def test_ttl_grid_32bit_horizon(ctx, P, kind):
-    """TTL-grid-only sweeps run the 32-bit-time kernel.  Long inter-arrival gaps (up to 2^30 µs),
+    """TTL-grid-only and program-FCFS-only sweeps run the 32-bit-time kernels (P <= 32: MODE 1 / 3;
+    P > 32: MODE 4 plus the list-driven 64-bit launch).  Long inter-arrival gaps (up to 2^30 µs),
     TTLs up to 2^40 µs and slow engines push replica horizons past 2^32 µs, where the replica
     must fall back to the 64-bit path: both must agree with the oracle byte for byte, as must the
     per-program bubble output (always the 64-bit path) and EVENT_BUDGET replicas."""
     import paper_2511_02230_b200 as ct
-    n_seeds = 4
+    n_seeds = 4 if P <= 32 else 2
     tr = traces.generate(n_seeds, P, n_bfcl=P // 2, mix="mix", ctx_cap=1500 * 16, stream=40 + P)
     gaps = [1 << 20, 300_000_000, (1 << 30) - 1]
     pols = [cf.ttl_grid(t) for t in (0, 1, 2_000_000, 600_000_000, 1 << 40)] + [cf.PROG_FCFS]
@@ -283,7 +284,7 @@ def test_ttl_grid_32bit_horizon(ctx, P, kind):
     span, budget = 0, False
     for eng in (cf.ENGINE_8B, cf.Engine(**{**cf.ENGINE_8B.__dict__, "c0_ps": 4 * 10**11}),
                 cf.Engine(**{**cf.ENGINE_8B.__dict__, "max_iters": 2000 if P == 1 else 20000})):
-        sw = cf.Sweep(n_seeds, gaps, [4096, 1600], pols, fitted=fitted)
+        sw = cf.Sweep(n_seeds, gaps, [4096 if P <= 32 else 30 * P, 1600], pols, fitted=fitted)
         os_, oj, ob = O.simulate(tr, sw, eng, n_threads=8, want_bubble=True)
         # without the bubble output: the 32-bit kernel (and its fallback); with it: 64-bit path
         s, j = ct.ct_simulate_batch(ctx, ct.DeviceTrace(tr), sw, eng, jct=True)
