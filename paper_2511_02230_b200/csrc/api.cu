@@ -267,12 +267,14 @@ int ct_simulate_batch_ex(ct_ctx* c, const ct_trace_set* tr, const ct_sweep* sw,
   int n_prog = 0;
   for (size_t i = 0; i < n_pol; ++i) n_prog += ct::prog_policy(sw->policies[i], E) ? 1 : 0;
   // P <= 32 32-bit-time kernels need d < 2^31 µs (a.d32); see replay.cu MODE
-  const int n_prog32 = a.d32 ? n_prog : 0;
+  int n_simple32 = 0;
+  if (a.d32)
+    for (size_t i = 0; i < n_pol; ++i) n_simple32 += ct::simple_policy(sw->policies[i], E) ? 1 : 0;
   const int mode = growth    ? 0
-                   : ns == 1 ? (n_fast == (int)n_pol     ? 1
-                                : n_prog32 == (int)n_pol ? 3
-                                : n_prog32 > 0           ? 2
-                                                         : 0)
+                   : ns == 1 ? (n_fast == (int)n_pol       ? 1
+                                : n_simple32 == (int)n_pol ? 3
+                                : n_simple32 > 0           ? 2
+                                                           : 0)
                              : (n_prog == (int)n_pol ? 1 : 0);
   const int wpb = 4;
   a.from_list = 0;

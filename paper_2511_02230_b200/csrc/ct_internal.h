@@ -47,6 +47,13 @@ inline __host__ __device__ bool prog_policy(const ct_policy& p, const ct_engine_
          p.pause != CT_PAUSE_INFERCEPT;
 }
 
+// The simple class, for which the P <= 32 replay has a 32-bit-time path with the estimator:
+// program or request FCFS; EVICT, FIXED, PAPER or FITTED; no DRAM tier; flags 0.
+inline __host__ __device__ bool simple_policy(const ct_policy& p, const ct_engine_params& E) {
+  return (p.priority == CT_PRIO_PROG_FCFS || p.priority == CT_PRIO_REQ_FCFS) && p.flags == 0 &&
+         (p.dram == 0 || E.dram_blocks <= 0) && p.pause != CT_PAUSE_INFERCEPT;
+}
+
 // Bytes of shared memory one replica (one warp) needs for `ns` slots per lane and F tools.
 // KV growth (NEXT-2) always runs the shared-memory path, also for P <= 32.
 int replay_smem_per_warp(int ns, int F, bool growth, int mode);

@@ -577,8 +577,8 @@ __device__ __forceinline__ uint32_t sat32(int64_t v) {  // v >= 0
   return v >= (int64_t)T32_LIM ? T32_LIM : (uint32_t)v;
 }
 
-// STATS = false: the TTL-grid class (fast_policy); STATS = true: the program-FCFS class with
-// the estimator (prog32_policy: EVICT, FIXED with a threshold, PAPER CalcTTL, FITTED), whose
+// STATS = false: the TTL-grid class (fast_policy); STATS = true: program or request FCFS with
+// the estimator (simple_policy: EVICT, FIXED with a threshold, PAPER CalcTTL, FITTED), whose
 // statistic rows live in shared memory as on the 64-bit path.
 template <bool STATS>
 __device__ __forceinline__ bool replay_one_t32(const ReplayArgs& a, int64_t r, Stat* stats,
@@ -592,6 +592,7 @@ __device__ __forceinline__ bool replay_one_t32(const ReplayArgs& a, int64_t r, S
   const ct_policy* polp = a.pols + pol_i;
   // TTL-grid class: FIXED with CT_ALWAYS pins for t_pin; EVICT never pins (fast_policy)
   const int pause = polp->pause;
+  const int prio = polp->priority;  // STATS: program or request FCFS (simple_policy)
   const int64_t ttl_fixed = pause == CT_PAUSE_FIXED ? polp->t_pin_us : 0;
   const int F = a.F;
   const ct_estimator_params& est = a.est;
@@ -761,8 +762,15 @@ __device__ __forceinline__ bool replay_one_t32(const ReplayArgs& a, int64_t r, S
         const uint32_t mq = __ballot_sync(FULL_MASK, st == S_QUEUED);
         if (!mq) break;
         if (n_run >= E.max_batch) break;
-        const uint32_t mp = __ballot_sync(FULL_MASK, st == S_QUEUED && pin);
-        const int h = __ffs(mp ? mp : mq) - 1;
+        int h;
+        if (!STATS || prio == CT_PRIO_PROG_FCFS) {  // pinned-queued first, then queued, by index
+          const uint32_t mp = __ballot_sync(FULL_MASK, st == S_QUEUED && pin);
+          h = __ffs(mp ? mp : mq) - 1;
+        } else {  // REQ_FCFS (vanilla vLLM): earliest request, ties by index
+          const bool q = st == S_QUEUED;
+          const uint32_t mr = __reduce_min_sync(FULL_MASK, q ? req : T32_INF);
+          h = __ffs(__ballot_sync(FULL_MASK, q && req == mr)) - 1;
+        }
         const int32_t hctx = __shfl_sync(FULL_MASK, ctx, h);
         const int32_t hg = __shfl_sync(FULL_MASK, gblk, h);
         const int32_t hnew = __shfl_sync(FULL_MASK, rec.x, h);
@@ -2127,9 +2135,9 @@ __device__ __forceinline__ bool replay_one_ns32(const ReplayArgs& a, int64_t r,
 // VLLM: the vLLM engine of NEXT-2 (KV growth, chunked prefill), always through the
 // shared-memory path (also P <= 32).
 // MODE (default engine): P <= 32: 0 every policy generic; 1 every policy in the TTL-grid class
-// (32-bit times, fallback to the 64-bit TTL-grid path); 3 every policy in the program-FCFS class
-// (32-bit times with the estimator, fallback to the generic path); 2 mixed: program-FCFS-class
-// replicas as in 3, the others generic.  P > 32: 0 generic, 1 every policy in the program-FCFS
+// (32-bit times, fallback to the 64-bit TTL-grid path); 3 every policy in the simple class
+// (program or request FCFS, 32-bit times with the estimator, fallback to the generic path);
+// 2 mixed: simple-class replicas as in 3, the others generic.  P > 32: 0 generic, 1 every policy in the program-FCFS
 // class; 4 every policy in the program-FCFS class with 32-bit times (replay_one_ns32), replicas
 // that reach the horizon are queued for a second launch of MODE 1 over that list (from_list).
 template <int NS, int MINB, bool VLLM = false, int MODE = 0>
@@ -2152,7 +2160,7 @@ __global__ void __launch_bounds__(128, MINB) replay_kernel(ReplayArgs a) {
     if (NS == 1 && !VLLM) {
       if (MODE == 1) {
         if (!replay_one_t32<false>(a, r, (Stat*)wm, lane)) replay_one_w32<true>(a, r, (Stat*)wm, lane);
-      } else if (MODE == 3 || (MODE == 2 && prog_policy(a.pols[(int)(r % a.n_pol)], a.eng))) {
+      } else if (MODE == 3 || (MODE == 2 && simple_policy(a.pols[(int)(r % a.n_pol)], a.eng))) {
         if (!replay_one_t32<true>(a, r, (Stat*)wm, lane)) replay_one_w32<false>(a, r, (Stat*)wm, lane);
       } else {
         replay_one_w32<false>(a, r, (Stat*)wm, lane);

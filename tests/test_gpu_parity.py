@@ -281,6 +281,8 @@ def test_ttl_grid_32bit_horizon(ctx, P, kind):
         fitted = np.tile(np.array([[0, 200_000, 3_000_000, 1 << 40]], np.int64), (tr.n_tools, 1))
         pols = [cf.CONTINUUM, cf.simplified(5_000_000, 2_000_000), cf.simplified(1 << 40, 10**9),
                 cf.CONTINUUM_FITTED, cf.ttl_grid(2_000_000), cf.PROG_FCFS]
+        if P <= 32:  # request FCFS is in the P <= 32 simple class (MODE 3)
+            pols += [cf.VLLM, cf.Policy(cf.PRIO_REQ_FCFS, cf.PAUSE_PAPER)]
     span, budget = 0, False
     for eng in (cf.ENGINE_8B, cf.Engine(**{**cf.ENGINE_8B.__dict__, "c0_ps": 4 * 10**11}),
                 cf.Engine(**{**cf.ENGINE_8B.__dict__, "max_iters": 2000 if P == 1 else 20000})):
