@@ -409,7 +409,9 @@ def main():
                        "parallelism": "replicas sharded (contiguous), all_gather of summaries"
                        if world > 1 else "1 GPU"},
             "roofline": roofline, "roofline_fit": rf, "cpu_baseline": cb, "e2e": e2e,
-            "gpu_launches": 4 * args.steps, "launch": launch, "clocks": clocks,
+            # per step: fit_hist + fit_scan, the replay launch(es), jct_stats
+            "gpu_launches": (3 + int(launch["launches"])) * args.steps, "launch": launch,
+            "clocks": clocks,
             "peaks": peak_kind}
     print(json.dumps(line), flush=True)
     if world > 1:
