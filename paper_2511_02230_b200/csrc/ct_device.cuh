@@ -78,6 +78,23 @@ __device__ __forceinline__ uint64_t isqrt_u64(uint64_t x) {
 // double estimate has relative error < 2^-50.5 (three roundings), so it is within one of the
 // quotient and a single integer correction against num - q den makes it exact.  Larger
 // quotients take the generic 128-bit division.
+// div_u128_r takes a precomputed reciprocal rden = 1.0 / (double)den, or its exact power-of-two
+// scaling, so several quotients by one divisor share one double division.  rden then adds at
+// most two roundings and the product one, for six in all: the relative error stays below
+// 2^-50.4, and the estimate is still within one of any quotient below 2^50.
+__device__ __forceinline__ u128_t div_u128_r(u128_t num, uint64_t den, double rden) {
+  const double dn = (double)(uint64_t)(num >> 64) * 18446744073709551616.0 + (double)(uint64_t)num;
+  const double est = dn * rden;
+  if (est < 1125899906842624.0) {  // 2^50
+    uint64_t q = (uint64_t)est;
+    const u128_t prod = (u128_t)q * den;
+    if (prod > num) q -= 1;
+    else if (num - prod >= den) q += 1;
+    return q;
+  }
+  return num / den;
+}
+
 __device__ __forceinline__ u128_t div_u128_u64(u128_t num, uint64_t den) {
   const double dn = (double)(uint64_t)(num >> 64) * 18446744073709551616.0 + (double)(uint64_t)num;
   const double est = dn / (double)den;
@@ -99,9 +116,12 @@ struct Stat {  // one estimator row: n, sum t~, sum t~^2 (128-bit as lo/hi)
 // Empirical Bernstein bound B(delta), fixed point (C-1):
 // floor(s1/n) + isqrt(floor(2 v L_q / (n 2^32))) + floor(3 b L_q / (n 2^32)),
 // v = floor((n s2 - s1^2) / (n (n-1))) for n >= 2, else 0.
+// The three quotients by n and by n 2^32 share one reciprocal of n.
 __device__ __forceinline__ int64_t bernstein(const Stat& s, uint64_t lq, int64_t b_us) {
   const int64_t n = s.n;
-  int64_t mu = s.s1 / n;
+  const double rn = 1.0 / (double)n;           // n < 2^31 (validated): exact conversion
+  const double rnsh = rn * 2.3283064365386963e-10;  // 2^-32: exact scaling
+  const int64_t mu = (int64_t)div_u128_r((u128_t)(uint64_t)s.s1, (uint64_t)n, rn);
   u128_t v = 0;
   if (n >= 2) {
     u128_t s2 = ((u128_t)s.s2hi << 64) | s.s2lo;
@@ -110,9 +130,9 @@ __device__ __forceinline__ int64_t bernstein(const Stat& s, uint64_t lq, int64_t
     v = div_u128_u64(num, den);
   }
   uint64_t nsh = (uint64_t)n << 32;
-  u128_t a2 = div_u128_u64((u128_t)2 * v * lq, nsh);
+  u128_t a2 = div_u128_r((u128_t)2 * v * lq, nsh, rnsh);
   uint64_t t2 = isqrt_u64((uint64_t)a2);
-  u128_t t3 = div_u128_u64((u128_t)3 * (uint64_t)b_us * lq, nsh);
+  u128_t t3 = div_u128_r((u128_t)3 * (uint64_t)b_us * lq, nsh, rnsh);
   return mu + (int64_t)t2 + (int64_t)t3;
 }
 
