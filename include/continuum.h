@@ -357,6 +357,11 @@ typedef struct {
   int64_t launches;         /* kernels launched by the last ct_simulate_batch */
   float replay_ms;          /* last replay_kernel duration */
   float fit_hist_ms;        /* last fit_hist_kernel duration */
+  int32_t kernel_mode;      /* replay specialisation of the last call: 0 generic,
+                               1 TTL-grid class (P <= 32, 32-bit times) or program-FCFS class
+                               (P > 32, 64-bit), 2 mixed, 3 simple class (P <= 32, 32-bit),
+                               4 program-FCFS class (P > 32, 32-bit) + list-driven 64-bit launch */
+  int32_t reserved;
 } ct_launch_info;
 int ct_last_launch(ct_ctx* ctx, ct_launch_info* info);
 int ct_ctx_set_timing(ct_ctx* ctx, int enable);

@@ -77,7 +77,7 @@ class TtlTable(C.Structure):
 class LaunchInfo(C.Structure):
     _fields_ = [("grid", i32), ("block", i32), ("warps_per_block", i32), ("slots_per_lane", i32),
                 ("smem_per_block", i64), ("launches", i64), ("replay_ms", C.c_float),
-                ("fit_hist_ms", C.c_float)]
+                ("fit_hist_ms", C.c_float), ("kernel_mode", i32), ("reserved", i32)]
 
 
 assert C.sizeof(Policy) == 48 and C.sizeof(EngineParams) == 80 and C.sizeof(EstimatorParams) == 64

@@ -320,6 +320,7 @@ int ct_simulate_batch_ex(ct_ctx* c, const ct_trace_set* tr, const ct_sweep* sw,
   c->last.slots_per_lane = ns;
   c->last.smem_per_block = smem;
   c->last.launches = ns32 ? 2 : 1;
+  c->last.kernel_mode = mode1;
   return CT_OK;
 }
 

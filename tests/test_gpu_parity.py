@@ -292,6 +292,9 @@ def test_ttl_grid_32bit_horizon(ctx, P, kind):
         s, j = ct.ct_simulate_batch(ctx, ct.DeviceTrace(tr), sw, eng, jct=True)
         torch.cuda.synchronize()
         assert_same(s.cpu().numpy(), j.cpu().numpy(), os_, oj)
+        li = ctx.last_launch()  # the specialised 32-bit kernel ran (DESIGN.md §8 MODE)
+        assert li["kernel_mode"] == (4 if P > 32 else 1 if kind == "grid" else 3), li
+        assert li["launches"] == (2 if P > 32 else 1)
         s, j, b = ct.ct_simulate_batch(ctx, ct.DeviceTrace(tr), sw, eng, jct=True, bubble=True)
         torch.cuda.synchronize()
         assert_same(s.cpu().numpy(), j.cpu().numpy(), os_, oj)
