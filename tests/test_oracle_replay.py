@@ -491,3 +491,47 @@ def test_chunked_prefill_huge_budget_is_unchunked():
     assert np.all((a[0][:, 0] & 0xFFFFFFFF) == 0)
     for x, y in zip(a, b):
         assert np.array_equal(x, y)
+
+
+# ---------------------------------------------------------------------------------------------
+# enumeration of schedules (SURVEY.md §8(c) "Replay, small instances")
+# ---------------------------------------------------------------------------------------------
+def _serial_jcts(order, arr, svc):
+    """JCTs when requests run one at a time in `order`, each admitted at the later of its
+    arrival and the previous finish (the finish frees the pool at an iteration boundary)."""
+    t, out = 0, {}
+    for i in order:
+        t = max(t, arr[i]) + svc[i]
+        out[i] = t - arr[i]
+    return [out[i] for i in range(len(arr))]
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_schedule_enumeration_single_slot_pool(seed):
+    """P <= 3 single-turn programs whose requests pairwise overflow the pool: every feasible
+    schedule runs them one at a time.  Enumerate all admission orders with their closed-form
+    JCTs; the oracle's JCTs must be exactly those of the policy's priority order (program FCFS
+    = request FCFS here: arrival, then index) and of no other order,
+    and no order that overlaps two requests may appear (it would exceed the pool)."""
+    import itertools
+    rng = random.Random(seed)
+    P = rng.randint(2, 3)
+    news = rng.sample(range(30, 50), P)  # distinct prefill sizes => distinct service times
+    decs = [rng.randint(1, 4) for _ in range(P)]
+    arr = sorted(rng.choice([0, 0, 1, 3, 7]) for _ in range(P))
+    need = [n + d for n, d in zip(news, decs)]  # bs = 1: blocks = tokens
+    pool = max(need)
+    assert all(need[i] + need[j] > pool for i in range(P) for j in range(i + 1, P))
+    # UNIT engine: prefill iteration 1 + new µs (c0 = c_pf = 1e6 ps, c_kv = 0), decodes 1 µs
+    svc = [1 + n + (d - 1) for n, d in zip(news, decs)]
+    tr = traces.tiny([(a, [(n, d, -1, 0)]) for a, n, d in zip(arr, news, decs)])
+    matches = []
+    for order in itertools.permutations(range(P)):
+        matches.append((order, _serial_jcts(order, arr, svc)))
+    for pol in (cf.PROG_FCFS, cf.VLLM, cf.CONTINUUM, cf.ttl_grid(10**6)):
+        s, j = run(tr, pol, pool)
+        assert O.status(s) == cf.STATUS_OK
+        hit = [o for o, jc in matches if list(j) == jc]
+        assert hit == [tuple(range(P))], (pol, list(j), matches)
+        # the pool never held two requests: the sum of JCTs is that of a serial schedule
+        assert int(s[10]) == sum(news)  # every prompt prefilled exactly once
