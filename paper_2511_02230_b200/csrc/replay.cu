@@ -1717,8 +1717,16 @@ __device__ __forceinline__ void replay_one_ns(const ReplayArgs& a, int64_t r, un
 // bubble output; the caller queues it for the 64-bit kernel (replay_one_ns<NS, false, true>),
 // which replays it from scratch.  Otherwise identical to that path step for step.
 int replay_ns32_smem_per_warp(int ns, int F) {
-  return ((28 * 32 * ns + 15) & ~15) + ((32 * (F + 1) + 48 + 15) & ~15);
+  return ((28 * 32 * ns + 15) & ~15) + ((32 * (F + 1) + 48 + 15) & ~15) + 16 * F;
 }
+
+// CalcTTL cache of one tool row (PAPER mode, P > 32 32-bit kernel).  Once n_f >= N the offset
+// depends only on row f's statistics and on (D, turns_done) (g.n >= f.n >= N),
+// and n_f grows by one per recorded sample: the key (n_f, D) identifies the inputs exactly.
+struct TtlCache {
+  uint64_t key;  // n_f << 32 | D, ~0 = empty
+  int64_t ttl;
+};
 
 template <int NS>
 __device__ __forceinline__ bool replay_one_ns32(const ReplayArgs& a, int64_t r,
@@ -1733,6 +1741,7 @@ __device__ __forceinline__ bool replay_one_ns32(const ReplayArgs& a, int64_t r,
   int32_t* gblk = ctx + PM;
   int32_t* turn = gblk + PM;
   Stat* stats = (Stat*)(wm + ((28 * PM + 15) & ~15));
+  TtlCache* tcache = (TtlCache*)(wm + ((28 * PM + 15) & ~15) + ((32 * (a.F + 1) + 48 + 15) & ~15));
 
   const int P = a.P, F = a.F;
   const int64_t npol = a.n_pol, nkv = a.n_kv, nrate = a.n_rate;
@@ -1768,6 +1777,8 @@ __device__ __forceinline__ bool replay_one_ns32(const ReplayArgs& a, int64_t r,
   }
   if (need_stats)
     for (int i = lane; i < 4 * (F + 1); i += 32) ((int64_t*)stats)[i] = 0;
+  if (pause == CT_PAUSE_PAPER)
+    for (int i = lane; i < F; i += 32) tcache[i].key = ~0ull;
   __syncwarp();
 
   uint32_t qb = 0, pb = 0, rb = 0, tb = 0;  // per-lane sets over this lane's slots
@@ -1955,7 +1966,19 @@ __device__ __forceinline__ bool replay_one_ns32(const ReplayArgs& a, int64_t r,
           if (pause == CT_PAUSE_FIXED) {
             ttl = simplified_ttl(stats[F], stats[f], est, polp->t_pin_us, polp->t_thresh_us);
           } else if (pause == CT_PAUSE_PAPER) {
-            ttl = calc_ttl(stats[F], stats[f], est, D, turns_done);
+            const int64_t nf = stats[f].n;
+            if (nf >= est.n_min) {  // cached per (n_f, D): see TtlCache
+              const uint64_t key = ((uint64_t)nf << 32) | (uint32_t)D;
+              if (tcache[f].key == key) {
+                ttl = tcache[f].ttl;
+              } else {
+                ttl = calc_ttl(stats[F], stats[f], est, D, turns_done);
+                __syncwarp();
+                if (lane == 0) { tcache[f].key = key; tcache[f].ttl = ttl; }
+              }
+            } else {
+              ttl = calc_ttl(stats[F], stats[f], est, D, turns_done);
+            }
           } else if (pause == CT_PAUSE_FITTED) {
             ttl = __ldg(&a.fitted[(int64_t)f * a.J + min(tp, a.J - 1)]);
           }
