@@ -174,7 +174,14 @@ def cpu_baseline(w, budget_s, n_threads):
         for x in ex.map(one, reps):
             turns += x
     dt = time.time() - t0
+    cpu = ""
+    try:
+        with open("/proc/cpuinfo") as fh:
+            cpu = next((l.split(":", 1)[1].strip() for l in fh if l.startswith("model name")), "")
+    except OSError:
+        pass
     return {"value": turns / dt, "unit": UNIT, "cores": n_threads, "kind": "oracle",
+            "cpu_model": cpu,
             "est_turns_per_step": turns / len(reps) * R,
             "sample": "%d of %d replicas (every %d-th), %d replica-turns, %.1f s wall on %d threads"
                       % (len(reps), R, stride, turns, dt, n_threads)}
