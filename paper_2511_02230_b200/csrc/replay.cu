@@ -576,6 +576,30 @@ __device__ __forceinline__ void replay_one_w32(const ReplayArgs& a, int64_t r, S
 // path (replay_one_w32<true>): the saturated values are only ever compared, never applied.
 // Otherwise identical to replay_one_w32<true> step for step (C-5/C-6); the parity
 // tests cover both, including horizons beyond 2^32 µs.
+// CalcTTL cache of one tool row (PAPER mode, P > 32 32-bit kernel; measured 2-3 % slower in the
+// P <= 32 one, which does not use it).  Once n_f >= N the offset depends
+// only on row f's statistics and on (D, turns_done) (g.n >= f.n >= N), and n_f
+// grows by one per recorded sample: the key (n_f, D) identifies the inputs exactly.
+struct TtlCache {
+  uint64_t key;  // n_f << 32 | D, ~0 = empty
+  int64_t ttl;
+};
+
+// PAPER-mode TTL of a finish with tool f through the cache (warp-uniform; lane 0 writes).
+__device__ __forceinline__ int64_t calc_ttl_cached(const Stat* stats, TtlCache* tcache, int F,
+                                                   int f, const ct_estimator_params& est,
+                                                   int32_t D, int32_t turns_done, int lane) {
+  const int64_t nf = stats[f].n;
+  if (nf < est.n_min) return calc_ttl(stats[F], stats[f], est, D, turns_done);
+  const uint64_t key = ((uint64_t)nf << 32) | (uint32_t)D;
+  if (tcache[f].key == key) return tcache[f].ttl;
+  const int64_t ttl = calc_ttl(stats[F], stats[f], est, D, turns_done);
+  __syncwarp();
+  if (lane == 0) { tcache[f].key = key; tcache[f].ttl = ttl; }
+  __syncwarp();
+  return ttl;
+}
+
 constexpr uint32_t T32_INF = 0xFFFFFFFFu;
 constexpr uint32_t T32_LIM = 0xFFFFFFF0u;
 
@@ -748,7 +772,7 @@ __device__ __forceinline__ bool replay_one_t32(const ReplayArgs& a, int64_t r, S
             if (pause == CT_PAUSE_FIXED) {
               ttl = simplified_ttl(stats[F], stats[ptool], est, polp->t_pin_us, polp->t_thresh_us);
             } else if (pause == CT_PAUSE_PAPER) {
-              ttl = calc_ttl(stats[F], stats[ptool], est, D, turns_done);
+              ttl = calc_ttl(stats[F], stats[ptool], est, D, turns_done);  // cache measured slower here
             } else if (pause == CT_PAUSE_FITTED) {
               ttl = __ldg(&a.fitted[(int64_t)ptool * a.J + min(pt, a.J - 1)]);
             }
@@ -1720,13 +1744,6 @@ int replay_ns32_smem_per_warp(int ns, int F) {
   return ((28 * 32 * ns + 15) & ~15) + ((32 * (F + 1) + 48 + 15) & ~15) + 16 * F;
 }
 
-// CalcTTL cache of one tool row (PAPER mode, P > 32 32-bit kernel).  Once n_f >= N the offset
-// depends only on row f's statistics and on (D, turns_done) (g.n >= f.n >= N),
-// and n_f grows by one per recorded sample: the key (n_f, D) identifies the inputs exactly.
-struct TtlCache {
-  uint64_t key;  // n_f << 32 | D, ~0 = empty
-  int64_t ttl;
-};
 
 template <int NS>
 __device__ __forceinline__ bool replay_one_ns32(const ReplayArgs& a, int64_t r,
@@ -1966,19 +1983,7 @@ __device__ __forceinline__ bool replay_one_ns32(const ReplayArgs& a, int64_t r,
           if (pause == CT_PAUSE_FIXED) {
             ttl = simplified_ttl(stats[F], stats[f], est, polp->t_pin_us, polp->t_thresh_us);
           } else if (pause == CT_PAUSE_PAPER) {
-            const int64_t nf = stats[f].n;
-            if (nf >= est.n_min) {  // cached per (n_f, D): see TtlCache
-              const uint64_t key = ((uint64_t)nf << 32) | (uint32_t)D;
-              if (tcache[f].key == key) {
-                ttl = tcache[f].ttl;
-              } else {
-                ttl = calc_ttl(stats[F], stats[f], est, D, turns_done);
-                __syncwarp();
-                if (lane == 0) { tcache[f].key = key; tcache[f].ttl = ttl; }
-              }
-            } else {
-              ttl = calc_ttl(stats[F], stats[f], est, D, turns_done);
-            }
+            ttl = calc_ttl_cached(stats, tcache, F, f, est, D, turns_done, lane);
           } else if (pause == CT_PAUSE_FITTED) {
             ttl = __ldg(&a.fitted[(int64_t)f * a.J + min(tp, a.J - 1)]);
           }
