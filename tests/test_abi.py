@@ -61,10 +61,11 @@ def test_struct_sizes_match_header(lib):
 #include <stdio.h>
 #include "continuum.h"
 int main(void) {
-  printf("%zu %zu %zu %zu %zu %zu %zu %zu %zu %zu %zu %zu\n", sizeof(ct_program), sizeof(ct_turn),
-         sizeof(ct_trace_set), sizeof(ct_estimator_params), sizeof(ct_engine_params),
-         sizeof(ct_policy), sizeof(ct_sweep), sizeof(ct_replica_summary), sizeof(ct_cell_stats),
-         sizeof(ct_samples), sizeof(ct_cost_params), sizeof(ct_ttl_table));
+  printf("%zu %zu %zu %zu %zu %zu %zu %zu %zu %zu %zu %zu %zu %zu %zu\n", sizeof(ct_program),
+         sizeof(ct_turn), sizeof(ct_trace_set), sizeof(ct_estimator_params),
+         sizeof(ct_engine_params), sizeof(ct_policy), sizeof(ct_sweep), sizeof(ct_replica_summary),
+         sizeof(ct_cell_stats), sizeof(ct_samples), sizeof(ct_cost_params), sizeof(ct_ttl_table),
+         sizeof(ct_launch_info), sizeof(ct_synth_params), sizeof(ct_replay_outputs));
   return 0;
 }
 """
@@ -77,7 +78,8 @@ int main(void) {
         sizes = [int(x) for x in subprocess.check_output([exe]).split()]
     assert sizes[0] == 16 and sizes[1] == 16 and sizes[7] == 128 and sizes[8] == 64
     mirrors = [lib.TraceSet, lib.EstimatorParams, lib.EngineParams, lib.Policy, lib.Sweep, None,
-               None, lib.Samples, lib.CostParams, lib.TtlTable]
+               None, lib.Samples, lib.CostParams, lib.TtlTable, lib.LaunchInfo, lib.SynthParams,
+               lib.ReplayOutputs]
     for got, m in zip(sizes[2:], mirrors):
         if m is not None:
             assert C.sizeof(m) == got, m
