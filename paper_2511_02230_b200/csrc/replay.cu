@@ -2249,12 +2249,12 @@ static void* pick(int ns, bool growth, int mode) {
   }
   switch (ns) {
     case 1:
-      if (mode == 1) {  // TTL-grid class: 32 registers, 64 warps/SM measured best (cfg3)
-        switch (getenv("CT_REPLAY_MINB") ? minb() : 16) {
+      if (mode == 1) {  // TTL-grid class: 48 registers, 40 warps/SM measured best (cfg3)
+        switch (getenv("CT_REPLAY_MINB") ? minb() : 10) {
           case 8: return (void*)replay_kernel<1, 8, false, 1>;
-          case 10: return (void*)replay_kernel<1, 10, false, 1>;
           case 12: return (void*)replay_kernel<1, 12, false, 1>;
-          default: return (void*)replay_kernel<1, 16, false, 1>;
+          case 16: return (void*)replay_kernel<1, 16, false, 1>;
+          default: return (void*)replay_kernel<1, 10, false, 1>;
         }
       }
       if (mode == 2) return (void*)replay_kernel<1, 8, false, 2>;
