@@ -295,6 +295,10 @@ def test_ttl_grid_32bit_horizon(ctx, P, kind):
         li = ctx.last_launch()  # the specialised 32-bit kernel ran (DESIGN.md §8 MODE)
         assert li["kernel_mode"] == (4 if P > 32 else 1 if kind == "grid" else 3), li
         assert li["launches"] == (2 if P > 32 else 1)
+        R = sw.n_replicas  # a shard: fallback replicas are indexed relative to replica_begin
+        s, j = ct.ct_simulate_batch(ctx, ct.DeviceTrace(tr), sw, eng, R // 3, 2 * R // 3, jct=True)
+        torch.cuda.synchronize()
+        assert_same(s.cpu().numpy(), j.cpu().numpy(), os_[R // 3: 2 * R // 3], oj[R // 3: 2 * R // 3])
         s, j, b = ct.ct_simulate_batch(ctx, ct.DeviceTrace(tr), sw, eng, jct=True, bubble=True)
         torch.cuda.synchronize()
         assert_same(s.cpu().numpy(), j.cpu().numpy(), os_, oj)
