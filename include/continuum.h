@@ -360,7 +360,8 @@ typedef struct {
   int32_t kernel_mode;      /* replay specialisation of the last call: 0 generic,
                                1 TTL-grid class (P <= 32, 32-bit times) or program-FCFS class
                                (P > 32, 64-bit), 2 mixed, 3 simple class (P <= 32, 32-bit),
-                               4 program-FCFS class (P > 32, 32-bit) + list-driven 64-bit launch */
+                               4 program-FCFS class (P > 32, 32-bit) + list-driven 64-bit launch,
+                               5 as 4 with request FCFS (simple class) */
   int32_t reserved;
 } ct_launch_info;
 int ct_last_launch(ct_ctx* ctx, ct_launch_info* info);

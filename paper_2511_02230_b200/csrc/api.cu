@@ -282,14 +282,16 @@ int ct_simulate_batch_ex(ct_ctx* c, const ct_trace_set* tr, const ct_sweep* sw,
   a.fb_count = c->counter + 1;
   // P > 32, program-FCFS class: the 32-bit kernel (MODE 4) first, then MODE 1 over the replicas
   // it handed back (horizon reached, or the bubble output requested)
-  const bool ns32 = ns > 1 && mode == 1 && a.d32 && !a.bubble;
+  // (simple class: program or request FCFS; the fallback launch is MODE 1 when every policy is
+  // in the program-FCFS class, else the generic kernel)
+  const bool ns32 = ns > 1 && !growth && n_simple32 == (int)n_pol && !a.bubble;
   if (ns32) {
     rc = ensure(&c->fb, &c->fb_cap, 8 * (size_t)(re - rb));
     if (rc) return rc;
     a.fb_list = (int64_t*)c->fb;
     CT_CUDA(cudaMemsetAsync(c->counter + 1, 0, 16, s));
   }
-  const int mode1 = ns32 ? 4 : mode;
+  const int mode1 = ns32 ? (mode == 1 ? 4 : 5) : mode;
   a.smem_per_warp = ns32 ? ct::replay_ns32_smem_per_warp(ns, F)
                          : ct::replay_smem_per_warp(ns, F, growth, mode);
   const int smem = a.smem_per_warp * wpb;

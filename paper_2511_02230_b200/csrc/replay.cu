@@ -1733,19 +1733,20 @@ __device__ __forceinline__ void replay_one_ns(const ReplayArgs& a, int64_t r, un
 }
 
 // -----------------------------------------------------------------------------------------------
-// 32 < P <= 256, program-FCFS class (prog_policy), default engine, with 32-bit replica-relative
-// times (as replay_one_t32: µs since the first arrival, saturated at T32_LIM; iteration indices
-// stay below the time).  28 B of shared memory per program (tev, texp, req/JCT, fin as u32;
-// ctx, gblk, turn), so 28 warps (all 4,096 replicas of cfg2) fit on the GPU at once.  Returns
-// false, before writing any output, when the replica reaches the horizon or asks for the
-// bubble output; the caller queues it for the 64-bit kernel (replay_one_ns<NS, false, true>),
-// which replays it from scratch.  Otherwise identical to that path step for step.
+// 32 < P <= 256, simple class (simple_policy: program or request FCFS), default engine, with
+// 32-bit replica-relative times (as replay_one_t32: µs since the first arrival, saturated at
+// T32_LIM; iteration indices stay below the time).  28 B of shared memory per program (tev,
+// texp, req/JCT, fin as u32; ctx, gblk, turn), so 28 warps (all 4,096 replicas of cfg2) fit on
+// the GPU at once.  Returns false, before writing any output, when the replica reaches the
+// horizon or asks for the bubble output; the caller queues it for a 64-bit launch (the
+// program-FCFS kernel when every policy is in that class, else the generic one), which
+// replays it from scratch.  Otherwise identical to the 64-bit path step for step.
 int replay_ns32_smem_per_warp(int ns, int F) {
   return ((28 * 32 * ns + 15) & ~15) + ((32 * (F + 1) + 48 + 15) & ~15) + 16 * F;
 }
 
 
-template <int NS>
+template <int NS, bool REQ>
 __device__ __forceinline__ bool replay_one_ns32(const ReplayArgs& a, int64_t r,
                                                 unsigned char* wm, int lane) {
   constexpr int PM = 32 * NS;
@@ -1768,6 +1769,8 @@ __device__ __forceinline__ bool replay_one_ns32(const ReplayArgs& a, int64_t r,
   const int64_t seed = r / (npol * nkv * nrate);
   const ct_policy* polp = a.pols + pol_i;
   const int pause = polp->pause;
+  // REQ: the sweep has request-FCFS policies (MODE 5); else every policy is program FCFS
+  const int prio = REQ ? polp->priority : CT_PRIO_PROG_FCFS;
   const int64_t gap = a.gap[rate_i];
   const ct_program* prog = a.progs + seed * P;
   const ct_engine_params& E = a.eng;
@@ -2011,12 +2014,24 @@ __device__ __forceinline__ bool replay_one_ns32(const ReplayArgs& a, int64_t r,
       for (;;) {
         if (!__any_sync(FULL_MASK, qb != 0)) break;
         if (n_run >= E.max_batch) break;
-        // lowest index among pinned-queued, else queued
-        uint32_t sel = qb & pb;
-        uint32_t slots = __reduce_or_sync(FULL_MASK, sel);
-        if (!slots) { sel = qb; slots = __reduce_or_sync(FULL_MASK, sel); }
-        const int s0 = __ffs(slots) - 1;
-        const int h = 32 * s0 + __ffs(__ballot_sync(FULL_MASK, (sel >> s0) & 1u)) - 1;
+        int h;
+        if (prio == CT_PRIO_PROG_FCFS) {  // lowest index among pinned-queued, else queued
+          uint32_t sel = qb & pb;
+          uint32_t slots = __reduce_or_sync(FULL_MASK, sel);
+          if (!slots) { sel = qb; slots = __reduce_or_sync(FULL_MASK, sel); }
+          const int s0 = __ffs(slots) - 1;
+          h = 32 * s0 + __ffs(__ballot_sync(FULL_MASK, (sel >> s0) & 1u)) - 1;
+        } else {  // REQ_FCFS (vanilla vLLM): earliest request, ties by index
+          uint32_t bk = T32_INF;
+          int bp = 0x7fffffff;
+#pragma unroll
+          for (int s = 0; s < NS; ++s) {
+            const int pl = lane + 32 * s;
+            if (((qb >> s) & 1u) && req[pl] < bk) { bk = req[pl]; bp = pl; }
+          }
+          const uint32_t mk = __reduce_min_sync(FULL_MASK, bk);
+          h = (int)__reduce_min_sync(FULL_MASK, (uint32_t)(bk == mk ? bp : 0x7fffffff));
+        }
         const int4 tr = turn_rec(h, turn[h]);
         const int64_t hctx = ctx[h];
         const int64_t hg = gblk[h];
@@ -2181,7 +2196,8 @@ __device__ __forceinline__ bool replay_one_ns32(const ReplayArgs& a, int64_t r,
 // (program or request FCFS, 32-bit times with the estimator, fallback to the generic path);
 // 2 mixed: simple-class replicas as in 3, the others generic.  P > 32: 0 generic, 1 every policy in the program-FCFS
 // class; 4 every policy in the program-FCFS class with 32-bit times (replay_one_ns32), replicas
-// that reach the horizon are queued for a second launch of MODE 1 over that list (from_list).
+// that reach the horizon are queued for a second launch of MODE 1 over that list (from_list);
+// 5 the same for the simple class with request FCFS (fallback launch: the generic kernel).
 template <int NS, int MINB, bool VLLM = false, int MODE = 0>
 __global__ void __launch_bounds__(128, MINB) replay_kernel(ReplayArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -2207,8 +2223,8 @@ __global__ void __launch_bounds__(128, MINB) replay_kernel(ReplayArgs a) {
       } else {
         replay_one_w32<false>(a, r, (Stat*)wm, lane);
       }
-    } else if (MODE == 4) {
-      if (!replay_one_ns32<NS>(a, r, wm, lane) && lane == 0)
+    } else if (MODE == 4 || MODE == 5) {
+      if (!replay_one_ns32<NS, MODE == 5>(a, r, wm, lane) && lane == 0)
         a.fb_list[atomicAdd(a.fb_count, 1ull)] = r;
     } else {
       replay_one_ns<NS, VLLM, (MODE == 1)>(a, r, wm, lane);
@@ -2266,18 +2282,25 @@ static void* pick(int ns, bool growth, int mode) {
         default: return (void*)replay_kernel<1, 8>;
       }
     case 2: return mode == 4 ? (void*)replay_kernel<2, NS32_MINB, false, 4>
+                 : mode == 5 ? (void*)replay_kernel<2, NS32_MINB, false, 5>
                  : mode == 1 ? (void*)replay_kernel<2, NS_PROG_MINB, false, 1> : (void*)replay_kernel<2, 1>;
     case 3: return mode == 4 ? (void*)replay_kernel<3, NS32_MINB, false, 4>
+                 : mode == 5 ? (void*)replay_kernel<3, NS32_MINB, false, 5>
                  : mode == 1 ? (void*)replay_kernel<3, NS_PROG_MINB, false, 1> : (void*)replay_kernel<3, 1>;
     case 4: return mode == 4 ? (void*)replay_kernel<4, NS32_MINB, false, 4>
+                 : mode == 5 ? (void*)replay_kernel<4, NS32_MINB, false, 5>
                  : mode == 1 ? (void*)replay_kernel<4, NS_PROG_MINB, false, 1> : (void*)replay_kernel<4, 1>;
     case 5: return mode == 4 ? (void*)replay_kernel<5, NS32_MINB, false, 4>
+                 : mode == 5 ? (void*)replay_kernel<5, NS32_MINB, false, 5>
                  : mode == 1 ? (void*)replay_kernel<5, NS_PROG_MINB, false, 1> : (void*)replay_kernel<5, 1>;
     case 6: return mode == 4 ? (void*)replay_kernel<6, NS32_MINB, false, 4>
+                 : mode == 5 ? (void*)replay_kernel<6, NS32_MINB, false, 5>
                  : mode == 1 ? (void*)replay_kernel<6, NS_PROG_MINB, false, 1> : (void*)replay_kernel<6, 1>;
     case 7: return mode == 4 ? (void*)replay_kernel<7, NS32_MINB, false, 4>
+                 : mode == 5 ? (void*)replay_kernel<7, NS32_MINB, false, 5>
                  : mode == 1 ? (void*)replay_kernel<7, NS_PROG_MINB, false, 1> : (void*)replay_kernel<7, 1>;
     case 8: return mode == 4 ? (void*)replay_kernel<8, NS32_MINB, false, 4>
+                 : mode == 5 ? (void*)replay_kernel<8, NS32_MINB, false, 5>
                  : mode == 1 ? (void*)replay_kernel<8, NS_PROG_MINB, false, 1> : (void*)replay_kernel<8, 1>;
   }
   return nullptr;

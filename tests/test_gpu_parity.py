@@ -281,8 +281,9 @@ def test_ttl_grid_32bit_horizon(ctx, P, kind):
         fitted = np.tile(np.array([[0, 200_000, 3_000_000, 1 << 40]], np.int64), (tr.n_tools, 1))
         pols = [cf.CONTINUUM, cf.simplified(5_000_000, 2_000_000), cf.simplified(1 << 40, 10**9),
                 cf.CONTINUUM_FITTED, cf.ttl_grid(2_000_000), cf.PROG_FCFS]
-        if P <= 32:  # request FCFS is in the P <= 32 simple class (MODE 3)
-            pols += [cf.VLLM, cf.Policy(cf.PRIO_REQ_FCFS, cf.PAUSE_PAPER)]
+        # request FCFS is in the simple class too (P <= 32: MODE 3; P > 32: MODE 4 with the
+        # generic 64-bit kernel as the fallback launch)
+        pols += [cf.VLLM, cf.Policy(cf.PRIO_REQ_FCFS, cf.PAUSE_PAPER)]
     span, budget = 0, False
     for eng in (cf.ENGINE_8B, cf.Engine(**{**cf.ENGINE_8B.__dict__, "c0_ps": 4 * 10**11}),
                 cf.Engine(**{**cf.ENGINE_8B.__dict__, "max_iters": 2000 if P == 1 else 20000})):
@@ -293,7 +294,8 @@ def test_ttl_grid_32bit_horizon(ctx, P, kind):
         torch.cuda.synchronize()
         assert_same(s.cpu().numpy(), j.cpu().numpy(), os_, oj)
         li = ctx.last_launch()  # the specialised 32-bit kernel ran (DESIGN.md §8 MODE)
-        assert li["kernel_mode"] == (4 if P > 32 else 1 if kind == "grid" else 3), li
+        assert li["kernel_mode"] == ((4 if kind == "grid" else 5) if P > 32 else
+                                     1 if kind == "grid" else 3), li
         assert li["launches"] == (2 if P > 32 else 1)
         R = sw.n_replicas  # a shard: fallback replicas are indexed relative to replica_begin
         s, j = ct.ct_simulate_batch(ctx, ct.DeviceTrace(tr), sw, eng, R // 3, 2 * R // 3, jct=True)
