@@ -17,7 +17,8 @@ for P, mix in ((16, "mix"), (70, "mix")):
 # specialised kernels: TTL-grid class (32-bit times, with a horizon fallback at the long gap)
 # and the program-FCFS class for P > 32
 for P, pols in ((16, [cf.ttl_grid(0), cf.ttl_grid(2_000_000), cf.PROG_FCFS]),
-                (70, [cf.CONTINUUM, cf.ttl_grid(500_000), cf.PROG_FCFS])):
+                (70, [cf.CONTINUUM, cf.ttl_grid(500_000), cf.PROG_FCFS]),
+                (70, [cf.VLLM, cf.CONTINUUM]), (16, [cf.VLLM, cf.CONTINUUM])):
     tr = traces.generate(2, P, mix="mix", ctx_cap=8192, stream=P + 1)
     sw = cf.Sweep(2, [300_000, (1 << 30) - 1], [3000], pols)
     s, j = ct.ct_simulate_batch(ctx, ct.DeviceTrace(tr), sw, cf.ENGINE_8B, jct=True)
