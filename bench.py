@@ -294,10 +294,15 @@ def main():
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream()
     kev = []
+    # a FITTED policy (cfg4) replays with this step's ct_fit_ttl table (per-tool rows)
+    fitted_policy = any(p.pause == cf.PAUSE_FITTED for p in sw.policies)
+    n_tools = tr.n_tools
 
     def step(timed):
         flush.zero_()  # L2 flush (256 MiB > 126 MB L2)
         arg, pap, _ = ct.ct_fit_ttl(ctx, dur, off, cp, sw.estimator, want_stats=False)
+        if fitted_policy:
+            sw.fitted = arg[:n_tools]
         if timed:
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(stream)
@@ -354,6 +359,8 @@ def main():
             d = h_dur.to(dev, non_blocking=True)
             arg, _, _ = ct.ct_fit_ttl(ctx, d, off, cp, sw.estimator, want_stats=False)
             h_tab.copy_(arg, non_blocking=True)
+            if fitted_policy:
+                sw.fitted = arg[:n_tools]
             ct.ct_simulate_batch_host(ctx, tr, sw, eng, rb, re_, out=h_out, programs=h_prog,
                                       turns=h_turn)
 
@@ -400,6 +407,8 @@ def main():
     if not args.no_fit_bandwidth:
         rf = fit_bandwidth(ctx, ct, cf, args.fit_log2n, dev, peaks, consts)
         rf["peak_kind"] = peak_kind
+    if fitted_policy:  # the oracle reads the (identical, deterministic) table from the host
+        sw.fitted = sw.fitted.cpu().numpy()
     cb = None
     if world == 1 and not args.no_cpu_baseline:
         cb = cpu_baseline(w, args.cpu_seconds, os.cpu_count() or 1)
