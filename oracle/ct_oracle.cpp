@@ -210,6 +210,11 @@ struct Prog {
   int64_t chunk = 0;    // prefill tokens computed in the iteration in flight
   bool emit = false;    // emits a token at the end of the iteration in flight
   bool preempted = false;  // recompute-preempted, back in Q (NEXT-2, R28)
+  // JCT accounting: time spent in each lifecycle state, accumulated at every
+  // state change, and the tool time the trace prescribes
+  int64_t since = 0;
+  int64_t in_state[7] = {0, 0, 0, 0, 0, 0, 0};
+  int64_t tool_us = 0;
 };
 
 struct Row { int64_t n = 0, s1 = 0; u128 s2 = 0; };
@@ -245,6 +250,13 @@ struct Sim {
   int32_t prog_nturns(int i) const { int32_t v; std::memcpy(&v, progs + 16 * (size_t)(seed * P + i) + 12, 4); return v; }
   const int32_t* turn_rec(int i, int t) const { return turns + 4 * ((int64_t)prog_turn0(i) + t); }
   int64_t arrival_time(int i) const { return (int64_t)(((i128)prog_arr_q(i) * gap) >> 20); }
+
+  // every lifecycle transition goes through here, so in_state[] partitions [arrival, completion]
+  void set_state(int i, int st) {
+    p[i].in_state[p[i].st] += now - p[i].since;
+    p[i].since = now;
+    p[i].st = st;
+  }
 
   bool dram_on() const { return pol[2] != 0 && eng[6] > 0; }
   bool growth() const { return eng[8] != 0; }  // NEXT-2 block-by-block KV growth (R27)
@@ -316,7 +328,7 @@ struct Sim {
     if (p[i].turn == prog_nturns(i) - 1) {  // last request: free KV, program completes
       free_blk += p[i].gblk; p[i].gblk = 0;
       dram_free += p[i].dblk; p[i].dblk = 0;
-      p[i].completion = now; p[i].st = DONE;
+      p[i].completion = now; set_state(i, DONE);
       D += 1; turns_done += prog_nturns(i);
       return;
     }
@@ -327,7 +339,8 @@ struct Sim {
       evict(i);
     }
     p[i].t_ret = now + tr[3];
-    p[i].st = TOOL;
+    p[i].tool_us += tr[3];
+    set_state(i, TOOL);
   }
 
   int head() {  // argmax priority over Q
@@ -361,7 +374,7 @@ struct Sim {
   void preempt(int v) {
     free_blk += p[v].gblk;
     p[v].gblk = 0;
-    p[v].st = QUEUED;
+    set_state(v, QUEUED);
     p[v].preempted = true;
     p[v].req_arr = now;
   }
@@ -400,7 +413,7 @@ struct Sim {
     if (growth()) grow_running();
     // (b) loaded requests join the batch
     for (int i = 0; i < P; ++i)
-      if (p[i].st == READY) { p[i].st = RUNNING; p[i].prem = unc[i]; }
+      if (p[i].st == READY) { set_state(i, RUNNING); p[i].prem = unc[i]; }
     // chunked prefill (R31/R32): the running requests take their share of the budget first
     int64_t left = budget() > 0 ? assign_running() : 1;
     // (c) admit loop (victims PAPER.md:645-655)
@@ -452,9 +465,9 @@ struct Sim {
       prefill += uncached;
       unc[h] = uncached;
       if (loading) {
-        p[h].st = LOADING;
+        set_state(h, LOADING);
       } else {
-        p[h].st = RUNNING;
+        set_state(h, RUNNING);
         p[h].prem = uncached;
         if (budget() > 0) {  // R32: a new request takes what is left (a decode takes one token)
           p[h].chunk = std::min(uncached, left);
@@ -556,17 +569,19 @@ struct Sim {
           const int32_t* tr = turn_rec(i, p[i].turn);
           record(tr[2], tr[3]);  // Δ_obs = now - t_finish = dur_us
           p[i].turn += 1;
-          p[i].st = QUEUED;
+          set_state(i, QUEUED);
           p[i].req_arr = now;
           p[i].emitted = 0;
         }
       // LoadDone
       for (int i = 0; i < P; ++i)
-        if (p[i].st == LOADING && p[i].load_done == now) p[i].st = READY;
+        if (p[i].st == LOADING && p[i].load_done == now) set_state(i, READY);
       // ProgramArrival
       while (next_arr < P && p[next_arr].arrival == now) {
         Prog& q = p[next_arr];
-        q.st = QUEUED; q.turn = 0; q.ctx = 0; q.req_arr = now;
+        q.since = now;  // the program's lifetime starts at its arrival
+        set_state(next_arr, QUEUED);
+        q.turn = 0; q.ctx = 0; q.req_arr = now;
         next_arr++;
       }
       // IterationEnd: every batch member emits one token; finishes in index order
@@ -585,6 +600,16 @@ struct Sim {
     }
     if (status == ST_OK && D != P) status = ST_UNSCHED;
     if (status == ST_OK && pins_created != hits + expiries + victims) status = ST_INVARIANT;
+    // JCT = sum of bubbles + in-engine time + tool time + load stalls, per program.
+    // Bubbles come from the req_arr bookkeeping of the admit loop, tool time from the trace,
+    // engine and load time from the state clock; the queue-state clock must equal the bubbles.
+    for (int i = 0; status == ST_OK && i < P; ++i) {
+      const Prog& q = p[i];
+      const int64_t engine = q.in_state[RUNNING], load = q.in_state[LOADING] + q.in_state[READY];
+      if (q.completion - q.arrival != q.bubble + engine + q.tool_us + load ||
+          q.in_state[QUEUED] != q.bubble || q.in_state[TOOL] != q.tool_us)
+        status = ST_INVARIANT;
+    }
     std::memset(summary, 0, 16 * 8);
     if (status != ST_OK) {
       summary[0] = (int64_t)(uint32_t)status;

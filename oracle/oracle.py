@@ -21,6 +21,9 @@ SUMMARY_FIELDS = ["status_ndone", "turns_done", "sum_jct", "max_jct", "p50_jct",
 
 
 def build(force: bool = False) -> str:
+    alt = os.environ.get("CT_ORACLE_LIB")  # tools/oracle_mutations.py: a mutated oracle build
+    if alt:
+        return alt
     if force or not os.path.exists(LIB) or os.path.getmtime(LIB) < os.path.getmtime(SRC):
         subprocess.check_call(["g++", "-O2", "-std=c++17", "-shared", "-fPIC", "-o", LIB, SRC,
                                "-lpthread"])

@@ -5,7 +5,10 @@ Used only by tests on tiny instances (P <= 3, T <= 3, horizons of a few hundred
 compared against the clock each µs, and a scheduling pass runs at every µs in
 which something fired while no iteration is in flight (R3).  Agreement
 with the event-driven oracle checks its next-event selection, the R1 order of
-same-instant events and the bookkeeping, by a different control structure.  EAGER expiry only.
+same-instant events and the bookkeeping, by a different control structure.  Both expiry
+readings (R4): EAGER releases a stale pin the first µs with now > expiry; STEP
+(flag 2, §5.3 literal) releases stale pins of programs not waiting in the queue
+only at the start of a scheduling pass.
 
 Semantics followed (C-5/C-6, Alg. 1 and §5.3):
   * pin hit iff tool duration <= TTL (expiry checked as now > expiry)
@@ -41,7 +44,7 @@ def simulate(trace, gap_us, kv, pol, est, eng, fitted=None, horizon=200000):
     prio, pause, dram, flags, t_pin, t_thresh = [int(x) for x in pol[:6]]
     dram_on = dram != 0 and dram_cap > 0
     victims_any = bool(flags & 1)
-    assert not (flags & 2), "brute force covers EAGER expiry only"
+    step_expiry = bool(flags & 2)
 
     arr = [(int(progs["arr_q"][i]) * gap_us) >> 20 for i in range(P)]
     t0 = [int(progs["turn0"][i]) for i in range(P)]
@@ -106,7 +109,7 @@ def simulate(trace, gap_us, kv, pol, est, eng, fitted=None, horizon=200000):
         # 1) pins that became stale this µs (first instant with now > expiry)
         for i in range(P):
             s = S[i]
-            if s["where"] == "tool" and s["pin"] is not None and now == s["pin"] + 1:
+            if not step_expiry and s["where"] == "tool" and s["pin"] is not None and now == s["pin"] + 1:
                 drop(i)
                 s["pin"] = None
                 cnt["exp"] += 1
@@ -170,6 +173,14 @@ def simulate(trace, gap_us, kv, pol, est, eng, fitted=None, horizon=200000):
                         s["where"] = "tool"
         # 6) scheduling pass at an event instant with no iteration in flight (R3)
         if engine_until is None and fired:
+            if step_expiry:  # unpin_requests() at the beginning of the scheduling step
+                for i in range(P):
+                    s = S[i]
+                    if s["pin"] is not None and s["where"] != "queue" and now > s["pin"]:
+                        drop(i)
+                        s["pin"] = None
+                        cnt["exp"] += 1
+
             def rank(i):  # smaller ranks first
                 if prio == 0:
                     return (i,)

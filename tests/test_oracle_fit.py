@@ -134,3 +134,39 @@ def test_paper_stats_clamp_at_b():
     _, _, st = O.fit(dur, off, cost(), [16], [0], est())
     assert st[0, 1] == 10 + b + b
     assert int(np.uint64(st[0, 2])) + (int(np.uint64(st[0, 3])) << 64) == 100 + 2 * b * b
+
+
+def test_point_mass_rational_turn_factor_and_block_ceiling():
+    """V_j = floor(c_pf ctx_j (a_den + a_num w_j) / a_den) and C_j = c_pin ceil(ctx_j / bs)
+    (C-4) with a_den > 1, a_num > 0 and ctx_j % bs != 0, on point masses placed at
+    d = floor(V/C) + {-1, 0, +1}: tau* = ceil(d/step) step iff V > C d.  The expected V and C
+    use Fraction arithmetic (exact rationals, then floor / ceiling), so the pin fails if the
+    oracle drops /a_den, floors ceil(ctx/bs), or rounds V up."""
+    from fractions import Fraction
+    rng = random.Random(6)
+    flips = {"a_den": 0, "ceil": 0, "round": 0}
+    for i in range(600):
+        exact = i % 3 == 0  # a third of the cases sit exactly on V = C d with V's floor active
+        while True:
+            bs = rng.randint(2, 32)
+            ctx = rng.randint(1, 6) * bs + rng.randint(1, bs - 1)        # ctx % bs != 0
+            a_den, a_num, w = rng.randint(2, 9), rng.randint(1, 5), rng.randint(1, 8)
+            c_pf, c_pin = rng.randint(1, 3000), rng.randint(1, 40)
+            Vq = Fraction(c_pf * ctx * (a_den + a_num * w), a_den)
+            V = math.floor(Vq)
+            nb = math.ceil(Fraction(ctx, bs))
+            C = c_pin * nb
+            if not exact or (V % C == 0 and Vq.denominator != 1):
+                break
+        d = max(1, V // C + (0 if exact else rng.choice([-1, 0, 1])))
+        step = max(1, -(-(d + 1) // 500))
+        dur, off = csr([[d] * rng.randint(1, 5)])
+        arg, _, _ = O.fit(dur, off, [c_pf, c_pin, bs, a_num, a_den, step, 1024, 1], [ctx], [w],
+                          est(1))
+        want = -(-d // step) * step if V > C * d else 0
+        assert int(arg[0, 0]) == want, (bs, ctx, a_den, a_num, w, c_pf, c_pin, d)
+        # the cases below would change under the named mistake
+        flips["a_den"] += (c_pf * ctx * (a_den + a_num * w) > C * d) != (V > C * d)
+        flips["ceil"] += (V > c_pin * (ctx // bs) * d) != (V > C * d)
+        flips["round"] += (math.ceil(Vq) > C * d) != (V > C * d)
+    assert min(flips.values()) >= 5, flips

@@ -7,7 +7,10 @@
   * invariants asserted inside the oracle on every event (status -1 if violated);
   * SPEC acceptance criteria 3, 4, 6, 7 and SPEC.md:492 as directional checks.
 """
+import math
 import random
+from dataclasses import replace
+from fractions import Fraction
 
 import numpy as np
 import pytest
@@ -63,9 +66,25 @@ def test_golden_G2():
         assert list(run(G2, pol, 20)[1]) == [47, 26]
 
 
+def test_golden_step_expiry():
+    """STEP reading of R4: pins are released only by the sweep at the start of a
+    scheduling point, for programs not in Q."""
+    step = lambda tau: replace(cf.ttl_grid(tau), flags=cf.FLAG_STEP_EXPIRY)  # noqa: E731
+    # G1: the only scheduling points are 0, 11, 12 and 17; at 17 A is back in Q -> hit (EAGER: 33)
+    s, j = run(G1, step(4), 100)
+    assert list(j) == [21] and s[12] == 1 and s[13] == 0
+    # G2', pool 30: A finishes turn 0 at 22, B's iterations end at 23..26, A returns at 42
+    s, j = run(G2, step(3), 30)   # expiry 25: released by the sweep at 26
+    assert list(j) == [57, 25] and s[13] == 1 and s[12] == 0
+    s, j = run(G2, step(4), 30)   # expiry 26: no scheduling point with now > 26 before 42
+    assert list(j) == [45, 25] and s[12] == 1 and s[13] == 0
+    s, j = run(G2, cf.ttl_grid(4), 30)  # EAGER: PinExpiry at 27
+    assert list(j) == [57, 25] and s[13] == 1
+
+
 def test_golden_fixture_consistent():
     lines = [l for l in open("tests/golden/replay_goldens.txt") if l.strip() and not l.startswith("#")]
-    assert len(lines) == 9
+    assert len(lines) == 12
 
 
 # ---------------------------------------------------------------------------------------------
@@ -155,6 +174,53 @@ def test_invariants_and_determinism():
     assert np.all(s1[ok, 3] == j1[ok].max(axis=1))
     # a pin can only hit, expire or be victimised; TTL 0 policies have none
     assert np.all(s1[ok][:, 12:15][::len(ALL_POLICIES)] == 0)
+    # R20 nearest rank from the JCT vector of every completed replica
+    srt = np.sort(j1[ok], axis=1)
+    assert np.array_equal(s1[ok, 4], srt[:, math.ceil(P * 50 / 100) - 1])
+    assert np.array_equal(s1[ok, 5], srt[:, math.ceil(P * 99 / 100) - 1])
+    # ct_jct_stats: per sweep cell sums over seeds, written independently with numpy
+    cells = O.jct_stats(s1, sw.n_cells)
+    assert np.array_equal(cells, numpy_cell_stats(s1, sw.n_cells))
+    assert cells[:, 1].sum() == (~ok).sum()
+
+
+@pytest.mark.parametrize("P", [1, 2, 99, 100, 101, 150, 200, 256])
+def test_nearest_rank_percentiles(P):
+    """R20: p50/p99 = sorted JCTs at rank ceil(q n), on sizes where ceil and
+    floor + 1 differ (even P) and where rank 99 % is below P (P > 100)."""
+    tr = small_workload(3, P=P, n_seeds=2, cap=16384 * 16)
+    sw = cf.Sweep(2, [2_000_000], [16384], [cf.CONTINUUM, cf.VLLM])
+    s, j = O.simulate(tr, sw, cf.ENGINE_8B)
+    assert np.all((s[:, 0] & 0xFFFFFFFF) == 0)
+    for row, jj in zip(s, j):
+        assert row[4] == nearest_rank(jj, Fraction(50, 100))
+        assert row[5] == nearest_rank(jj, Fraction(99, 100))
+
+
+def numpy_cell_stats(summ, n_cells):
+    """Cell c = replicas r with r % n_cells == c (the policy/kv/rate digits of the mixed
+    radix): {n_ok, n_bad, sum n_done, sum turns, sum JCT, max JCT, sum bubble, sum makespan}
+    over completed replicas; failed replicas only count in n_bad."""
+    cell = np.arange(len(summ)) % n_cells
+    ok = (summ[:, 0] & 0xFFFFFFFF) == 0
+    out = np.zeros((n_cells, 8), np.int64)
+    np.add.at(out[:, 0], cell[ok], 1)
+    np.add.at(out[:, 1], cell[~ok], 1)
+    for col, field in ((2, summ[:, 0] >> 32), (3, summ[:, 1]), (4, summ[:, 2]), (6, summ[:, 6]),
+                       (7, summ[:, 7])):
+        np.add.at(out[:, col], cell[ok], field[ok])
+    np.maximum.at(out[:, 5], cell[ok], summ[ok, 3])
+    return out
+
+
+def test_jct_stats_against_numpy_random_summaries():
+    """ct_jct_stats' oracle on arbitrary summary rows (failed replicas mixed in)."""
+    rng = np.random.default_rng(7)
+    for n_cells, n_seeds in ((1, 5), (7, 3), (64, 4)):
+        s = rng.integers(0, 10**9, size=(n_cells * n_seeds, 16), dtype=np.int64)
+        st = rng.choice([0, 0, 0, 1, 2], size=len(s))
+        s[:, 0] = (rng.integers(0, 256, size=len(s)) << 32) | st
+        assert np.array_equal(O.jct_stats(s, n_cells), numpy_cell_stats(s, n_cells))
 
 
 # ---------------------------------------------------------------------------------------------
@@ -191,22 +257,36 @@ def random_policy(rng):
     pause = rng.choice([cf.PAUSE_EVICT, cf.PAUSE_FIXED, cf.PAUSE_FIXED, cf.PAUSE_PAPER,
                         cf.PAUSE_FITTED, cf.PAUSE_INFERCEPT])
     return cf.Policy(priority=rng.choice([0, 0, 1, 2]), pause=pause, dram=rng.choice([0, 1]),
-                     flags=rng.choice([0, 0, cf.FLAG_VICTIMS_ANY]), t_pin_us=rng.randint(0, 30),
+                     flags=rng.choice([0, 0, cf.FLAG_VICTIMS_ANY, cf.FLAG_STEP_EXPIRY,
+                                       cf.FLAG_STEP_EXPIRY | cf.FLAG_VICTIMS_ANY]),
+                     t_pin_us=rng.randint(0, 30),
                      t_thresh_us=rng.choice([cf.ALWAYS, cf.ALWAYS, rng.randint(1, 30)]))
 
 
-@pytest.mark.parametrize("seed", range(10))
+def nearest_rank(jct, q):
+    """R20: the value at rank ceil(q n) of the sorted JCTs, q = 50/100, 99/100."""
+    s = np.sort(np.asarray(jct, np.int64))
+    return int(s[math.ceil(q * len(s)) - 1])
+
+
+@pytest.mark.parametrize("seed", range(12))
 def test_bruteforce_tiny(seed):
     """Seeds 0-5: admission reserves the request (R12); seeds 6-7: KV growth with recompute
     preemption (NEXT-2, R27-R30) on smaller pools, so preemption is frequent; seeds 8-9:
-    chunked prefill with small token budgets (R31-R32)."""
+    chunked prefill with small token budgets (R31-R32); seeds 10-11: every policy under STEP
+    expiry (R4 alternative).  Every summary field is compared, p50/p99 by nearest
+    rank of the brute force's JCTs."""
     rng = random.Random(100 + seed)
     growth = seed in (6, 7)
-    chunked = seed >= 8
-    agree = thrown = 0
-    for _ in range(150):
+    chunked = seed in (8, 9)
+    step_only = seed >= 10
+    agree = thrown = step_exp = 0
+    for _ in range(200 if growth else 150):
         tr = random_tiny_growth(rng) if growth else random_tiny(rng)
         pol = random_policy(rng)
+        if step_only:
+            pol = replace(pol, flags=pol.flags | cf.FLAG_STEP_EXPIRY,
+                          pause=rng.choice([cf.PAUSE_FIXED, cf.PAUSE_PAPER, cf.PAUSE_FITTED]))
         eng = cf.Engine(c0_ps=rng.randint(1, 3 * 10**6), c_pf_ps=rng.choice([0, 5 * 10**5, 10**6]),
                         c_kv_ps=rng.choice([0, 10**4, 2 * 10**5]), c_h2d_ps=rng.randint(1, 2 * 10**6),
                         bs=rng.choice([1, 2] if growth else [1, 2, 4]),
@@ -232,16 +312,19 @@ def test_bruteforce_tiny(seed):
         assert list(j) == bj
         assert list(bb[0]) == cnt["waited"]
         thrown += cnt["thrown"]
-        want = [cnt["turns"], sum(bj), max(bj), None, None, cnt["bubble"], cnt["makespan"],
+        want = [cnt["turns"], sum(bj), max(bj), nearest_rank(bj, Fraction(50, 100)),
+                nearest_rank(bj, Fraction(99, 100)), cnt["bubble"], cnt["makespan"],
                 cnt["iters"], cnt["busy"], cnt["prefill"], cnt["recompute"], cnt["hits"], cnt["exp"],
                 cnt["vict"], cnt["reload"]]
         got = list(s[1:16])
-        for k, (a, b) in enumerate(zip(got, want)):
-            if b is not None:
-                assert a == b, (k, got, want)
+        assert got == want, (got, want)
+        if pol.flags & cf.FLAG_STEP_EXPIRY:
+            step_exp += cnt["exp"]
         agree += 1
     assert agree > (60 if growth else 90)
-    assert thrown > 20 if growth else thrown == 0
+    assert thrown > 20 if growth else thrown == 0, (agree, thrown)
+    if step_only:
+        assert step_exp > 10  # STEP releases really happen on these instances
 
 
 # ---------------------------------------------------------------------------------------------
