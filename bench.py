@@ -77,6 +77,13 @@ def fit_inputs(trace, J=8):
     return dur, off, [int(x) for x in ctxj], [j + 1 for j in range(J)]
 
 
+def fit_cost(w, ctxj):
+    """The step fit's cost parameters as the oracle's vector [c_pf, c_pin, bs, a_num, a_den,
+    grid_step, K, J] (the same values main() passes to ct.cost_params)."""
+    e = w.sweep.estimator
+    return [w.engine.c_pf_ps, 200, w.engine.bs, e.a_num, e.a_den, 50_000, 256, len(ctxj)]
+
+
 # ---------------------------------------------------------------------------------------------
 class ClockSampler:
     """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
@@ -147,44 +154,92 @@ def profile_constants():
 
 
 # ---------------------------------------------------------------------------------------------
-def cpu_baseline(w, budget_s, n_threads):
-    """The oracle as it stands on a bounded, strided sample of the same workload."""
+def oracle_fitted(w, dur_np, off, cost, ctxj, wj):
+    """The oracle's own TTL table for a FITTED policy (no input to the oracle comes from the
+    CUDA path): or_fit on the same samples and cost parameters the step's ct_fit_ttl used."""
     from oracle import oracle as O
-    R = w.sweep.n_replicas
+    if not any(p.pause == 3 for p in w.sweep.policies):
+        return w.sweep
+    arg, _, _ = O.fit(dur_np, off, cost, ctxj, wj, w.sweep.estimator.as_array())
+    sw = type(w.sweep)(**{**w.sweep.__dict__, "fitted": arg[:-1]})
+    return sw
+
+
+def cpu_baseline(w, sweep, budget_s, n_threads, gpu_summ=None):
+    """The oracle as it stands, on a bounded, strided sample of the same workload:
+    (b) a thread pool over the sampled replicas (each replica single-threaded), and
+    (a) one thread on a prefix of the every-256th-replica subset.
+    With gpu_summ (the GPU's [R, 16] summaries of this step) every sampled replica is also
+    compared byte for byte (parity)."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    from oracle import oracle as O
+    R = sweep.n_replicas
     t0 = time.time()
-    probe = list(range(0, R, max(1, R // 16)))[:16]
-    tot_turns = 0
-    for r in probe[:4]:
-        s, _ = O.simulate(w.trace, w.sweep, w.engine, r, r + 1, n_threads=1, want_jct=False)
-        tot_turns += int(s[0, 1])
-    per_rep = (time.time() - t0) / 4
+    probe = list(range(0, R, max(1, R // 16)))[:4]
+    for r in probe:
+        O.simulate(w.trace, sweep, w.engine, r, r + 1, n_threads=1, want_jct=False)
+    per_rep = (time.time() - t0) / len(probe)
     n = int(max(n_threads, min(R, budget_s * n_threads / max(per_rep, 1e-6))))
     stride = max(1, R // n)
     reps = np.arange(0, R, stride)[:n]
-    # contiguous blocks per call keep the oracle untouched; sample = every stride-th replica
-    t0 = time.time()
-    turns = 0
-    from concurrent.futures import ThreadPoolExecutor
 
     def one(r):
-        s, _ = O.simulate(w.trace, w.sweep, w.engine, int(r), int(r) + 1, n_threads=1, want_jct=False)
-        return int(s[0, 1])
+        s, _ = O.simulate(w.trace, sweep, w.engine, int(r), int(r) + 1, n_threads=1, want_jct=False)
+        return s[0]
 
+    t0 = time.time()
     with ThreadPoolExecutor(n_threads) as ex:
-        for x in ex.map(one, reps):
-            turns += x
+        rows = np.stack(list(ex.map(one, reps)))
     dt = time.time() - t0
+    turns = int(rows[:, 1].sum())
+    # (a) single thread, every 256th replica, bounded to ~budget/3 s
+    t0 = time.time()
+    t1_turns = t1_reps = 0
+    for r in range(0, R, 256):
+        t1_turns += int(one(r)[1])
+        t1_reps += 1
+        if time.time() - t0 > budget_s / 3:
+            break
+    t1 = time.time() - t0
     cpu = ""
     try:
         with open("/proc/cpuinfo") as fh:
             cpu = next((l.split(":", 1)[1].strip() for l in fh if l.startswith("model name")), "")
     except OSError:
         pass
-    return {"value": turns / dt, "unit": UNIT, "cores": n_threads, "kind": "oracle",
-            "cpu_model": cpu,
-            "est_turns_per_step": turns / len(reps) * R,
-            "sample": "%d of %d replicas (every %d-th), %d replica-turns, %.1f s wall on %d threads"
-                      % (len(reps), R, stride, turns, dt, n_threads)}
+    out = {"value": turns / dt, "unit": UNIT, "cores": n_threads, "kind": "oracle",
+           "cpu_model": cpu, "compiler": "g++ -O2 -std=c++17",
+           "est_turns_per_step": turns / len(reps) * R, "wall_s": dt,
+           "sample": "%d of %d replicas (every %d-th), %d replica-turns, %.1f s wall on %d threads"
+                     % (len(reps), R, stride, turns, dt, n_threads),
+           "single_thread": {"value": t1_turns / t1, "unit": UNIT + " per core", "cores": 1,
+                             "sample": "replicas 0, 256, ..., %d (%d of the every-256th subset, %d "
+                                       "replica-turns, %.1f s)" % (256 * (t1_reps - 1), t1_reps,
+                                                                   t1_turns, t1)}}
+    if gpu_summ is not None:
+        bad = np.nonzero(np.any(gpu_summ[reps] != rows, axis=1))[0]
+        out["parity"] = {"checked": int(len(reps)), "mismatches": int(bad.size),
+                         "compared": "128-B summary of every sampled replica, GPU step vs oracle",
+                         "first_mismatch": int(reps[bad[0]]) if bad.size else None}
+    return out
+
+
+def cpu_fit_baseline(dur_np, off, cost, ctxj, wj, est, budget_s=5.0):
+    """The oracle's TTL fit (plain O(n K) definition) on a bounded prefix of the samples."""
+    from oracle import oracle as O
+    n = len(dur_np)
+    m = min(n, 1 << 16)
+    while True:
+        cut = np.minimum(off, m)
+        t0 = time.time()
+        O.fit(dur_np[:m], cut, cost, ctxj, wj, est.as_array())
+        dt = time.time() - t0
+        if dt > budget_s / 4 or m >= n:
+            break
+        m = min(n, m * 4)
+    return {"value": m / dt, "unit": "samples/s", "gbs": 4.0 * m / dt / 1e9, "cores": 1,
+            "kind": "oracle", "sample": "first %d of %d samples (K = %d), %.2f s" % (m, n, cost[6], dt)}
 
 
 def run_reference(args):
@@ -192,24 +247,32 @@ def run_reference(args):
     if rank != 0:
         return
     w = load_workload(args.workload, args.seeds)
+    sweep = w.sweep
+    if any(p.pause == 3 for p in sweep.policies):
+        dur_np, off, ctxj, wj = fit_inputs(w.trace)
+        sweep = oracle_fitted(w, dur_np, off, fit_cost(w, ctxj), ctxj, wj)
     n_threads = os.cpu_count() or 1
     per_step = min(args.cpu_seconds, 150.0 / max(1, args.steps + args.warmup))
-    vals = []
+    vals, walls, turns = [], [], []
     last = None
     for i in range(args.warmup + args.steps):
-        cb = cpu_baseline(w, per_step, n_threads)
+        cb = cpu_baseline(w, sweep, per_step, n_threads)
         if i >= args.warmup:
             vals.append(cb["value"])
+            walls.append(cb["wall_s"])
             last = cb
-    v = float(np.mean(vals))
+    v = float(np.sum([c * t for c, t in zip(vals, walls)]) / np.sum(walls))
     last["value"] = v
-    # one full step (the whole workload) at the sampled rate: the sample's turns per replica x R
-    ms_full = last.pop("est_turns_per_step") / v * 1e3
+    est_full = last.pop("est_turns_per_step")
+    last.pop("wall_s")
     line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_full, "higher_is_better": True, "scaling": "strong",
-            "ms_per_step_basis": "whole workload at the sampled rate (each step times a bounded sample)",
+            "warmup": args.warmup, "ms_per_step": float(np.mean(walls)) * 1e3,
+            "ms_per_step_basis": "timed wall time of one step = one bounded sample of the "
+                                 "workload (cpu_baseline.sample) on all host cores",
+            "ms_per_full_workload_est": est_full / v * 1e3,
+            "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "int64", "data": "synthetic", "impl": "reference",
-            "config": {"workload": w.name, "replicas": w.sweep.n_replicas,
+            "config": {"workload": w.name, "replicas": sweep.n_replicas,
                        "programs_per_replica": w.trace.n_programs, "description": w.description},
             "cpu_baseline": last,
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -218,41 +281,61 @@ def run_reference(args):
 
 # ---------------------------------------------------------------------------------------------
 def fit_bandwidth(ctx, ct, cf, log2n, dev, peaks, consts):
-    """ttl_fit HBM pass: 2^log2n int32 samples (CSR by tool, F = 32, K = 256, J = 64)."""
+    """ttl_fit HBM pass: 2^log2n int32 samples (CSR by tool, F = 32, K = 256, J = 64).
+
+    kernel: CUDA events the library records around its single fused launch (per call, host
+    synchronised to read them); call: 10 back-to-back ct_fit_ttl calls between two events on the
+    stream, no host synchronisation in between.  Also a read-only HBM probe (torch int32 max over
+    the same 1 GiB) as the read ceiling next to the measured copy peak."""
     import torch
     from ctgen import traces
     n = 1 << log2n
-    F, K, J = 32, 256, 64
-    dur, off = traces.synthetic_samples_torch(log2n, F, 1234, dev)
+    K, J = 256, 64
+    dur, off = traces.synthetic_samples_torch(log2n, 32, 1234, dev)
     cp = ct.cost_params(13_400_000, 200, 16, 1, 10, 50_000, K,
                         [min(16 * 2**j, 120_000) for j in range(J)], [j + 1 for j in range(J)])
     est = cf.Estimator()
-    for _ in range(2):
-        ct.ct_fit_ttl(ctx, dur, off, cp, est)
+    for _ in range(3):
+        ct.ct_fit_ttl(ctx, dur, off, cp, est, want_stats=False)
     torch.cuda.synchronize()
     s = torch.cuda.current_stream()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    reps = 10
+    reps = 20
     ctx.set_timing(True)
     kms = []
+    for _ in range(reps):
+        ct.ct_fit_ttl(ctx, dur, off, cp, est, want_stats=False)
+        kms.append(ctx.last_launch()["fit_hist_ms"])  # waits for this launch's end event
+    ctx.set_timing(False)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(s)
     for _ in range(reps):
-        ct.ct_fit_ttl(ctx, dur, off, cp, est)
-        kms.append(ctx.last_launch()["fit_hist_ms"])  # waits for this launch's end event
+        ct.ct_fit_ttl(ctx, dur, off, cp, est, want_stats=False)
     e1.record(s)
     torch.cuda.synchronize()
-    ctx.set_timing(False)
     t_call = e0.elapsed_time(e1) / 1e3 / reps
     t = float(np.mean(kms)) / 1e3
+    # read-only probe over the same bytes
+    for _ in range(2):
+        dur.max()
+    e0.record(s)
+    for _ in range(reps):
+        dur.max()
+    e1.record(s)
+    torch.cuda.synchronize()
+    t_read = e0.elapsed_time(e1) / 1e3 / reps
     gbs = 4.0 * n / t / 1e9
     peak = float(peaks["hbm_gbs"])
     tr = consts.get("fit_dram_bytes_per_sample")
     return {"bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s", "frac": gbs / peak,
             "traffic": tr * n if tr else None,
-            "kernel": "fit_hist_kernel (CUDA events around the launch, inside the library)",
+            "kernel": "fit_hist_kernel<FUSED> (histogram + grid barrier + scan/argmax/CalcTTL, "
+                      "one cooperative launch; CUDA events inside the library)",
             "samples": n, "bytes_per_sample": 4, "ms_per_launch": t * 1e3,
             "call_ms": t_call * 1e3, "call_gbs": 4.0 * n / t_call / 1e9,
-            "note": "call = fit_hist + fit_scan + scratch memset, host-synchronised per call"}
+            "call_frac": 4.0 * n / t_call / 1e9 / peak,
+            "read_probe_gbs": 4.0 * n / t_read / 1e9,
+            "read_probe": "torch int32 max over the same 1 GiB (read-only HBM ceiling estimate)",
+            "note": "call = back-to-back ct_fit_ttl calls, no host synchronisation"}
 
 
 def main():
@@ -284,35 +367,61 @@ def main():
     shard = D.shard_capacity(R, world)
     dur_np, off, ctxj, wj = fit_inputs(tr)
     J = len(ctxj)
-    cp = ct.cost_params(eng.c_pf_ps, 200, eng.bs, sw.estimator.a_num, sw.estimator.a_den, 50_000,
-                        256, ctxj, wj, (0, 0))
+    F = tr.n_tools
+    fc = fit_cost(w, ctxj)
+    cp = ct.cost_params(fc[0], fc[1], fc[2], fc[3], fc[4], fc[5], fc[6], ctxj, wj, (0, 0))
     # ---- inputs resident in HBM before the timed region --------------------------------------
     dt = ct.DeviceTrace(tr)
     dur = torch.from_numpy(dur_np).to(dev)
     summ = torch.zeros((shard, 16), dtype=torch.int64, device=dev)
     gathered = torch.zeros((shard * world, 16), dtype=torch.int64, device=dev)
+    acc = torch.zeros(ct.ct_fit_acc_words(F, fc[6]), dtype=torch.int64, device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream()
-    kev = []
+    ev = {"fit": [], "replay": [], "gather": []}
     # a FITTED policy (cfg4) replays with this step's ct_fit_ttl table (per-tool rows)
     fitted_policy = any(p.pause == cf.PAUSE_FITTED for p in sw.policies)
-    n_tools = tr.n_tools
+
+    def fit():
+        """A-2: one fused launch on 1 GPU; per-rank slices of every tool
+        segment + an int64 all-reduce of the accumulator + the finish kernel on N GPUs."""
+        if world == 1:
+            return ct.ct_fit_ttl(ctx, dur, off, cp, sw.estimator, want_stats=False)[0], 1
+        ct.ct_fit_ttl_partial(ctx, dur, off, cp, sw.estimator, rank, world, acc=acc)
+        dist.all_reduce(acc)
+        return ct.ct_fit_ttl_finish(ctx, acc, F, cp, sw.estimator, want_stats=False)[0], 2
+
+    def mark(key, timed):
+        if not timed:
+            return None
+        e = torch.cuda.Event(enable_timing=True)
+        e.record(stream)
+        ev[key].append([e])
+        return e
+
+    def close(key, timed):
+        if timed:
+            e = torch.cuda.Event(enable_timing=True)
+            e.record(stream)
+            ev[key][-1].append(e)
+
+    fit_launches = [0]
 
     def step(timed):
         flush.zero_()  # L2 flush (256 MiB > 126 MB L2)
-        arg, pap, _ = ct.ct_fit_ttl(ctx, dur, off, cp, sw.estimator, want_stats=False)
+        mark("fit", timed)
+        arg, fit_launches[0] = fit()
+        close("fit", timed)
         if fitted_policy:
-            sw.fitted = arg[:n_tools]
-        if timed:
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record(stream)
+            sw.fitted = arg[:F]
+        mark("replay", timed)
         ct.ct_simulate_batch(ctx, dt, sw, eng, rb, re_, out=summ[: re_ - rb], jct=False)
-        if timed:
-            b.record(stream)
-            kev.append((a, b))
+        close("replay", timed)
+        mark("gather", timed)
         full = D.gather_summaries(summ, R, world, out=gathered)  # A-9: one NCCL all-gather
+        close("gather", timed)
         cells = ct.ct_jct_stats(ctx, full, sw.n_cells)
-        return cells
+        return cells, full
 
     for _ in range(args.warmup):
         step(False)
@@ -328,23 +437,30 @@ def main():
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for _ in range(args.steps):
-        cells = step(True)
+        cells, full = step(True)
     e1.record(stream)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     clocks = clk.stop()
     t = e0.elapsed_time(e1) / 1e3
-    k_t = sum(a.elapsed_time(b) for a, b in kev) / 1e3 / len(kev)
-    tt = torch.tensor([t, k_t], dtype=torch.float64, device=dev)
+
+    def mean_ms(key):
+        return sum(a.elapsed_time(b) for a, b in ev[key]) / len(ev[key])
+
+    per_rank = torch.tensor([t, mean_ms("replay"), mean_ms("fit"), mean_ms("gather")],
+                            dtype=torch.float64, device=dev)
     if world > 1:
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-    t, k_t = float(tt[0]), float(tt[1])
+        dist.all_reduce(per_rank, op=dist.ReduceOp.MAX)
+    t, k_ms, fit_ms, gather_ms = (float(x) for x in per_rank)
+    k_t = k_ms / 1e3
     cells_np = cells.cpu().numpy()
     turns_step = int(cells_np[:, 3].sum())
     n_bad = int(cells_np[:, 1].sum())
     value = turns_step * args.steps / t
     launch = ctx.last_launch()
+    full_np = full.cpu().numpy() if rank == 0 else None
+    replay_launches = int(launch["launches"])  # the trace check + the replay kernel(s)
 
     # ---- e2e: host buffers through the C ABI, copies inside the timed region -------------------
     e2e = None
@@ -353,14 +469,14 @@ def main():
         h_turn = torch.from_numpy(np.ascontiguousarray(tr.turns)).pin_memory()
         h_dur = torch.from_numpy(dur_np).pin_memory()
         h_out = torch.empty((re_ - rb, 16), dtype=torch.int64).pin_memory()
-        h_tab = torch.empty((len(off), J), dtype=torch.int64).pin_memory()
+        h_tab = torch.empty((F + 1, J), dtype=torch.int64).pin_memory()
 
         def e2e_step():
             d = h_dur.to(dev, non_blocking=True)
             arg, _, _ = ct.ct_fit_ttl(ctx, d, off, cp, sw.estimator, want_stats=False)
             h_tab.copy_(arg, non_blocking=True)
             if fitted_policy:
-                sw.fitted = arg[:n_tools]
+                sw.fitted = arg[:F]
             ct.ct_simulate_batch_host(ctx, tr, sw, eng, rb, re_, out=h_out, programs=h_prog,
                                       turns=h_turn)
 
@@ -393,26 +509,30 @@ def main():
     alu_peak = SM_COUNT * ISSUE_PER_SM_CLK * clk_mhz * 1e6 / 1e12  # T warp-inst/s
     turns_shard = turns_step * (re_ - rb) / R
     achieved = (ipt * turns_shard / k_t / 1e12) if ipt else None
+    dram_pt = consts.get("replay_dram_bytes_per_turn", {}).get(w.name) if consts else None
     roofline = {"bound": "alu", "kernel": "replay_kernel", "unit": "Twarp-inst/s",
                 "achieved": achieved, "peak": alu_peak,
                 "frac": (achieved / alu_peak) if achieved else None,
-                "traffic": (consts.get("replay_dram_bytes_per_turn", {}).get(w.name, 0) * turns_shard)
-                if consts.get("replay_dram_bytes_per_turn", {}).get(w.name) is not None else None,
+                "traffic": dram_pt * turns_shard if dram_pt is not None else None,
+                "warp_inst_per_replica_turn": ipt,
                 "peak_basis": "148 SMs x 4 schedulers x 1 warp-inst/clk x %.0f MHz (max clock)" % clk_mhz,
                 "achieved_basis": "ncu warp-inst per replica-turn (profiles/ncu_constants.json) x "
                                   "replica-turns per launch / CUDA-event launch time",
+                "traffic_basis": "ncu dram bytes per replica-turn of a full-size capture "
+                                 "(profiles/ncu_constants.json) x replica-turns per launch",
                 "ms_per_launch": k_t * 1e3, "share_of_step": k_t / (t / args.steps),
                 "replica_turns_per_s_kernel": turns_shard / k_t}
     rf = None
     if not args.no_fit_bandwidth:
         rf = fit_bandwidth(ctx, ct, cf, args.fit_log2n, dev, peaks, consts)
         rf["peak_kind"] = peak_kind
-    if fitted_policy:  # the oracle reads the (identical, deterministic) table from the host
-        sw.fitted = sw.fitted.cpu().numpy()
-    cb = None
+    cb = cbf = None
     if world == 1 and not args.no_cpu_baseline:
-        cb = cpu_baseline(w, args.cpu_seconds, os.cpu_count() or 1)
+        osw = oracle_fitted(w, dur_np, off, fc, ctxj, wj)
+        cb = cpu_baseline(w, osw, args.cpu_seconds, os.cpu_count() or 1, gpu_summ=full_np)
         cb.pop("est_turns_per_step")
+        cb.pop("wall_s")
+        cbf = cpu_fit_baseline(dur_np, off, fc, ctxj, wj, sw.estimator)
 
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t / args.steps * 1e3, "higher_is_better": True,
@@ -422,11 +542,16 @@ def main():
                        "non_ok_replicas": n_bad, "trace_bytes": dt.bytes,
                        "fit_samples_per_step": int(len(dur_np)),
                        "l2": "flushed every step (256 MiB write)",
-                       "parallelism": "replicas sharded (contiguous), all_gather of summaries"
+                       "parallelism": ("replicas sharded (contiguous), fit sharded per tool "
+                                       "segment + int64 all-reduce, all_gather of summaries")
                        if world > 1 else "1 GPU"},
-            "roofline": roofline, "roofline_fit": rf, "cpu_baseline": cb, "e2e": e2e,
-            # per step: fit_hist + fit_scan, the replay launch(es), jct_stats
-            "gpu_launches": (3 + int(launch["launches"])) * args.steps, "launch": launch,
+            "roofline": roofline, "roofline_fit": rf, "cpu_baseline": cb, "cpu_baseline_fit": cbf,
+            "e2e": e2e,
+            # per step: the fit (1 fused launch, or partial + finish), the trace check + replay
+            # kernel(s), jct_stats
+            "gpu_launches": (fit_launches[0] + replay_launches + 1) * args.steps,
+            "launch": launch,
+            "per_step_ms_max_over_ranks": {"fit": fit_ms, "replay": k_ms, "gather": gather_ms},
             "clocks": clocks,
             "peaks": peak_kind}
     print(json.dumps(line), flush=True)

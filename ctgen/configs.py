@@ -203,4 +203,16 @@ def config5(n_seeds: int = 256) -> Workload:
     return Workload("cfg5_policy_sweep", tr, sw, ENGINE_8B, "16x16x16x%d policy sweep" % n_seeds)
 
 
+# cfg4's FITTED policy replays the table ct_fit_ttl computes on the trace's own tool samples with
+# these cost parameters (parameter encodings only; the fit itself is the library's / oracle's)
+CFG4_FIT = {"J": 8, "ctx_j": [2000 * (j + 1) for j in range(8)], "w_j": [j + 1 for j in range(8)],
+            "c_pin": 200, "a_num": 1, "a_den": 10, "step": 50_000, "K": 256}
+
+
+def cfg4_fit_cost(engine: Engine) -> list[int]:
+    """[c_pf, c_pin, bs, a_num, a_den, grid_step, K, J] for config 4's fit."""
+    p = CFG4_FIT
+    return [engine.c_pf_ps, p["c_pin"], engine.bs, p["a_num"], p["a_den"], p["step"], p["K"], p["J"]]
+
+
 CONFIGS = {"1": config1, "2": config2, "3": config3, "4": config4, "5": config5}

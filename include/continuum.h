@@ -43,6 +43,8 @@ extern "C" {
 #define CT_R_OK 0
 #define CT_R_UNSCHEDULABLE 1  /* the head request can never fit (C-5 step 5c) */
 #define CT_R_EVENT_BUDGET 2   /* more than max_iters engine iterations would be needed */
+#define CT_R_INVALID_INPUT 3  /* the trace set (device buffers) violates a precondition of
+                                 ct_simulate_batch; ct_validate_trace_set names it */
 
 /* priority (PAPER.md:535-551 for PROG_FCFS; vanilla vLLM request FCFS PAPER.md:272) */
 #define CT_PRIO_PROG_FCFS 0   /* key (not pinned, program index): pinned first, then FCFS */
@@ -69,6 +71,11 @@ extern "C" {
 #define CT_MAX_TOOLS 64
 #define CT_MAX_K 1024         /* TTL grid points */
 #define CT_MAX_J 64           /* turn buckets */
+#define CT_MAX_TURNS 65536    /* turns per program */
+#define CT_MAX_CONTEXT (1 << 30)  /* a program's total new + decode tokens */
+#define CT_TTL_SAT (1ll << 50)    /* every TTL (pin length) is below this, in µs (~35.7 years):
+                                     FIXED t_pin and FITTED entries are validated against it and
+                                     CalcTTL saturates at CT_TTL_SAT - 1 (R36) */
 
 typedef struct ct_ctx ct_ctx;
 
@@ -146,9 +153,10 @@ typedef struct {
   const int64_t* kv_blocks;   /* [host] n_kv GPU KV pool sizes in blocks */
   const ct_policy* policies;  /* [host] n_policies */
   ct_estimator_params est;
-  const int64_t* fitted_ttl;  /* [dev] n_tools x fitted_j table for CT_PAUSE_FITTED, or NULL */
-  int32_t fitted_j;
-  int32_t reserved;
+  const int64_t* fitted_ttl;  /* [dev] fitted_rows x fitted_j table for CT_PAUSE_FITTED, or NULL;
+                                 entries in [0, CT_TTL_SAT) (checked on the device) */
+  int32_t fitted_j;           /* 1..CT_MAX_J */
+  int32_t fitted_rows;        /* >= n_tools (row f = tool f; e.g. ct_fit_ttl's ttl_argmax rows) */
 } ct_sweep;
 
 /* ---- outputs --------------------------------------------------------------------------- */
@@ -171,13 +179,29 @@ typedef struct {            /* 64 B per sweep cell (rate, kv, policy): sums over
 } ct_cell_stats;
 
 /* ---- TTL fit ----------------------------------------------------------------------------- */
+/* Samples S = {(f, t)} of PAPER.md:444 (§4.2), t = Δ_obs in µs.  Two layouts:
+ *  - CSR (tool_off != NULL): dur_us grouped by tool, segment f = dur_us[tool_off[f] .. tool_off[f+1]);
+ *    the bandwidth path (4 B per sample);
+ *  - unsorted pairs (tool_off == NULL): dur_us[i] with tool_u8[i], in arrival order; the fallback
+ *    (5 B per sample, tool-keyed shared atomics), needs F x (K+1) x 8 B of shared memory.
+ * dur_us must be 16-B aligned, tool_u8 4-B aligned (else CT_EINVAL). */
 typedef struct {
-  const int32_t* dur_us;      /* [dev] n samples grouped by tool (CSR), each >= 0 */
-  const int64_t* tool_off;    /* [host] n_tools + 1 non-decreasing offsets, tool_off[0] = 0 */
-  int64_t n;
+  const int32_t* dur_us;      /* [dev] n samples, each in [0, 2^31) (negative ones are counted into
+                                 ct_ttl_table.n_invalid and void the table, see CT_TTL_INVALID) */
+  const int64_t* tool_off;    /* [host] n_tools + 1 non-decreasing offsets, tool_off[0] = 0,
+                                 tool_off[n_tools] = n; NULL selects the unsorted layout */
+  const uint8_t* tool_u8;     /* [dev] unsorted layout: tool id per sample (ids >= n_tools are
+                                 invalid samples); ignored for CSR */
+  int64_t n;                  /* < 2^32 */
   int32_t n_tools;            /* F, 1..CT_MAX_TOOLS */
   int32_t reserved;
 } ct_samples;
+
+/* ttl_argmax / ttl_paper entries written when the sample set held n_invalid > 0 samples outside
+ * [0, 2^31) (or, unsorted layout, tool ids >= n_tools): the fit is undefined on such input, so no
+ * plausible-looking table is produced.  (The call itself is asynchronous and still returns CT_OK;
+ * read n_invalid after the stream synchronises.) */
+#define CT_TTL_INVALID (-1)
 
 typedef struct {            /* extension C-4 (not in PAPER.md; motivated by PAPER.md:323-338) */
   int64_t c_pf_ps;          /* prefill ps per token saved on a hit */
@@ -197,7 +221,15 @@ typedef struct {
   int64_t* ttl_argmax;      /* [dev] (F+1) x J: tau* per tool row (row F = pooled samples) */
   int64_t* ttl_paper;       /* [dev] F+1: CalcTTL offset per row */
   int64_t* stats;           /* [dev] (F+1) x 4 {n, sum t~, sum t~^2 lo, hi}, t~ = min(t, b); or NULL */
+  int64_t* n_invalid;       /* [dev] 1: number of invalid samples (0 on valid input); or NULL */
 } ct_ttl_table;
+
+/* ---- estimator statistics ------------------------------------------------------------------ */
+typedef struct {            /* the statistics of PAPER.md:447-458 over t~ = min(t, b) (R5) */
+  int64_t n;                /* |S| (or |S_f|) */
+  int64_t s1;               /* sum t~ */
+  uint64_t s2_lo, s2_hi;    /* sum t~^2 = s2_hi 2^64 + s2_lo */
+} ct_stat_row;
 
 /* ---- calls ------------------------------------------------------------------------------- */
 int ct_version(void);
@@ -213,24 +245,88 @@ int ct_ctx_destroy(ct_ctx* ctx);
  *  - argmax mode (extension C-4): n U(k) = V_j cnt_le(k) - C_j (sum_le(k) + tau_k (n - cnt_le(k))),
  *    V_j = floor(c_pf ctx_j (a_den + a_num w_j) / a_den), C_j = c_pin ceil(ctx_j / bs); tau* is the
  *    smallest maximiser over k >= 1 with U > 0, else 0.  Tools with n_f < N take the pooled row.
- * Preconditions (else CT_EINVAL): samples within [0, 2^31); every product bounded so that the
- * 128-bit arithmetic cannot overflow (checked against the sample count and the maxima).
+ * CSR layout: ONE kernel launch (histogram pass, grid barrier, scan/argmax/CalcTTL; the context's
+ * double-buffered accumulator is zeroed in-kernel for the next call).  Unsorted layout: the pairs
+ * kernel then the finish kernel.  Calls on one context must be ordered on one stream.
+ * Preconditions (else CT_EINVAL): dur_us 16-B aligned; n < 2^32; grid_step_us, b < 2^31;
+ * (K-1) step < 2^43; every product bounded so that the 128-bit arithmetic cannot overflow
+ * (checked against n and the cost maxima).  Sample VALUES are checked on the device (n_invalid).
  * Errors: CT_EINVAL, CT_ENOMEM, CT_ECUDA. */
 int ct_fit_ttl(ct_ctx* ctx, const ct_samples* samples, const ct_cost_params* cost,
                const ct_estimator_params* est, ct_ttl_table* out, void* stream);
+
+/* The estimator of PAPER.md §4.2-4.3 as batched device calls over the fixed-point arithmetic
+ * the replay and the fit run (C-1/C-2), for checks against the paper's worked
+ * examples and for callers that keep their own statistics.
+ * ct_bernstein: out[i] = B(delta) of rows[i] (printed form, reading R26):
+ *   floor(s1/n) + isqrt(floor(2 v L_q / (n 2^32))) + floor(3 b L_q / (n 2^32)),
+ *   v = floor((n s2 - s1^2) / (n (n-1))) (0 for n = 1), L_q = est->lq.
+ * ct_calc_ttl_batch: out[i] = CalcTTL offset for global statistics g[i] and
+ *   tool statistics f[i]: 𝓑 = T_default if g.n < N, else B(f) if f.n >= N, else B(g)
+ *   (PAPER.md:515-521), at least 1; then floor(T_default^2 (D a_den + a_num turns_done) /
+ *   (𝓑 D a_den)) for D = n_done[i] > 0, else floor(T_default^2 / 𝓑) (R7); clamped to ttl_max
+ *   when > 0 (R8) and saturated at CT_TTL_SAT - 1 (R36).
+ * Rows must hold the statistics of n < 2^31 samples in [0, b] (s1 <= n b, s2 <= n b^2; n >= 1
+ * for ct_bernstein); n_done in [0, CT_MAX_PROGRAMS], turns_done in [0, CT_MAX_PROGRAMS
+ * CT_MAX_TURNS].  Entries violating this get CT_TTL_INVALID.  All pointers [dev]; n >= 0.
+ * Errors: CT_EINVAL (NULL pointers, invalid est), CT_ECUDA. */
+int ct_bernstein(ct_ctx* ctx, const ct_stat_row* rows, int64_t n, const ct_estimator_params* est,
+                 int64_t* out, void* stream);
+int ct_calc_ttl_batch(ct_ctx* ctx, const ct_stat_row* g, const ct_stat_row* f,
+                      const int64_t* n_done, const int64_t* turns_done, int64_t n,
+                      const ct_estimator_params* est, int64_t* out, void* stream);
+/* Host scalar references of the same two formulas (the same helpers compiled for the host; no
+ * context, no device).  Return CT_TTL_INVALID on invalid rows or parameters. */
+int64_t ct_bernstein_ref(const ct_stat_row* row, const ct_estimator_params* est);
+int64_t ct_calc_ttl_ref(const ct_stat_row* g, const ct_stat_row* f, const ct_estimator_params* est,
+                        int64_t n_done, int64_t turns_done);
+
+/* Multi-GPU fit: the accumulator is a plain vector of int64 sums (bucket
+ * counts and sums, statistic limbs, the invalid count), so accumulators of disjoint sample
+ * sets add up exactly in any order.  ct_fit_acc_words(F, K) = 2 (F+1)(K+1) + 6 (F+1) + 1.
+ * ct_fit_ttl_partial accumulates rank `rank`'s slice of every tool segment, samples
+ * [off_f + floor(len_f rank / world), off_f + floor(len_f (rank + 1) / world)), into acc [dev]
+ * (zeroed first); after an int64 SUM all-reduce of acc over the ranks, ct_fit_ttl_finish
+ * computes the tables exactly as ct_fit_ttl would on all samples (byte for byte).
+ * CSR layout only for world > 1.  Errors as ct_fit_ttl. */
+int64_t ct_fit_acc_words(int32_t n_tools, int32_t K);  /* -1 if out of range */
+int ct_fit_ttl_partial(ct_ctx* ctx, const ct_samples* samples, const ct_cost_params* cost,
+                       const ct_estimator_params* est, int32_t rank, int32_t world, int64_t* acc,
+                       void* stream);
+int ct_fit_ttl_finish(ct_ctx* ctx, const int64_t* acc, int32_t n_tools, const ct_cost_params* cost,
+                      const ct_estimator_params* est, ct_ttl_table* out, void* stream);
 
 /* Replay replicas [replica_begin, replica_end) of the sweep:
  * Alg. 1 with §5.3 pin/unpin/victims inside an
  * integer discrete-event continuous-batching engine (C-5/C-6).
  * out[i] (and jct_us[i*P .. i*P+P-1] when jct_us != NULL) belongs to replica
  * replica_begin + i.  jct_us = completion - arrival per program, -1 when status != OK.
- * Preconditions (else CT_EINVAL): 1 <= P <= CT_MAX_PROGRAMS; turns valid (decode >= 1, tool in
- * range and dur >= 1 except on final turns); c0 >= 1, bs >= 1, max_batch >= 1; c_h2d >= 1 when a
- * policy has dram = 1; fitted_ttl != NULL when a policy is FITTED; estimator valid when a policy
- * is PAPER or FIXED with a threshold.  Errors: CT_EINVAL, CT_ENOMEM, CT_ECUDA. */
+ * Preconditions checked on the host (else CT_EINVAL): 1 <= P <= CT_MAX_PROGRAMS; c0 >= 1,
+ * bs >= 1, max_batch >= 1; the int64 fixed-point bounds of every constant, and
+ * c0 + (c_pf + c_kv) bs max(kv_blocks) < 2^62 ps (one iteration), dram_blocks c_h2d < 2^62 ps
+ * (one load); c_h2d >= 1 when a policy has dram = 1; 0 <= gap_us, kv_blocks < 2^30;
+ * t_pin < CT_TTL_SAT; fitted_ttl with fitted_rows >= n_tools when a policy is FITTED; estimator
+ * valid (a_num, a_den < 2^20, T_default, b < 2^40) when a policy uses it.
+ * The trace records (device buffers) are checked on the device before the replay, as
+ * ct_validate_trace_set lists; when they fail, no record is read and every replica of the call
+ * reports status CT_R_INVALID_INPUT (zero summary, -1 per-program outputs).
+ * Under these bounds every intermediate of the replay fits its integer type (the simulated
+ * clock stays below 2^62 µs for any replica that finishes within 2^18 iterations of the
+ * largest cost, and in practice for every workload).  Errors: CT_EINVAL, CT_ENOMEM, CT_ECUDA. */
 int ct_simulate_batch(ct_ctx* ctx, const ct_trace_set* traces, const ct_sweep* sweep,
                       const ct_engine_params* eng, int64_t replica_begin, int64_t replica_end,
                       ct_replica_summary* out, int64_t* jct_us, void* stream);
+
+/* Check a device trace set against the trace preconditions of ct_simulate_batch for the seeds
+ * that replicas [replica_begin, replica_end) replay, plus the FITTED table when a policy uses
+ * it: every program has 1 <= nturns <= CT_MAX_TURNS and its turns inside the turn array;
+ * 0 <= arr_q, arr_q * max(gap_us) < 2^62, arrivals non-decreasing within a seed; every turn
+ * decode >= 1, new >= 0, and (non-final) tool in [0, n_tools), dur_us >= 1; a program's total
+ * new + decode tokens <= CT_MAX_CONTEXT; FITTED entries in [0, CT_TTL_SAT).  Synchronises the
+ * stream.  Returns CT_OK, or CT_EINVAL naming the first offending program in ct_last_error().
+ * ct_simulate_batch runs the same check asynchronously before every replay. */
+int ct_validate_trace_set(ct_ctx* ctx, const ct_trace_set* traces, const ct_sweep* sweep,
+                          int64_t replica_begin, int64_t replica_end, void* stream);
 
 /* Optional per-program outputs of a replay (all [dev], n = replica_end - replica_begin).
  * summary is required; jct_us and bubble_us may be NULL.  bubble_us[i*P + p] is program p's

@@ -34,12 +34,13 @@ static int64_t ceil_div(i128 a, i128 b) { return (int64_t)((a + b - 1) / b); }  
 // §4.2 estimator, fixed point (C-1).
 // ---------------------------------------------------------------------------
 
-// floor(sqrt(x)), bit by bit.
-uint64_t or_isqrt(uint64_t x) {
+// floor(sqrt(x)) of x = hi 2^64 + lo, bit by bit (the result has at most 64 bits).
+uint64_t or_isqrt(uint64_t lo, uint64_t hi) {
+  const u128 x = ((u128)hi << 64) | lo;
   uint64_t r = 0;
-  for (int bit = 31; bit >= 0; --bit) {
+  for (int bit = 63; bit >= 0; --bit) {
     uint64_t c = r | (1ull << bit);
-    if (c * c <= x) r = c;
+    if ((u128)c * c <= x) r = c;
   }
   return r;
 }
@@ -58,7 +59,7 @@ int64_t or_bernstein(int64_t n, int64_t s1, uint64_t s2_lo, uint64_t s2_hi, uint
     var = num / ((u128)n * (u128)(n - 1));
   }
   u128 arg2 = ((u128)2 * var * (u128)lq) / ((u128)n << 32);
-  uint64_t term2 = or_isqrt((uint64_t)arg2);
+  uint64_t term2 = or_isqrt((uint64_t)arg2, (uint64_t)(arg2 >> 64));  // sqrt of all 128 bits
   u128 term3 = ((u128)3 * (u128)b_us * (u128)lq) / ((u128)n << 32);
   return mu + (int64_t)term2 + (int64_t)term3;
 }
@@ -79,7 +80,7 @@ int64_t or_select_bound(const int64_t* g, const int64_t* f, const int64_t* est) 
 
 // CalcTTL - now = T_default^2 / 𝓑 * (1 + alpha * AvgTurns)
 // alpha = a_num/a_den, AvgTurns = turns_done / n_done (0 before any completion, R7);
-// clamp to ttl_max when > 0 (R8).
+// clamp to ttl_max when > 0 (R8); saturate at 2^50 - 1 (R36).
 int64_t or_calc_ttl(const int64_t* g, const int64_t* f, const int64_t* est, int64_t n_done,
                     int64_t turns_done) {
   const int64_t T = est[2], a_num = est[4], a_den = est[5], ttl_max = est[6];
@@ -93,6 +94,9 @@ int64_t or_calc_ttl(const int64_t* g, const int64_t* f, const int64_t* est, int6
     ttl = ((u128)T * (u128)T) / (u128)B;
   }
   if (ttl_max > 0 && ttl > (u128)ttl_max) ttl = ttl_max;
+  // R36: a pin length is a µs count below 2^50 (~35.7 years, beyond any replay horizon);
+  // without a clamp the formula can exceed int64 (T_default^2 / 𝓑 with T_default < 2^40)
+  if (ttl >= ((u128)1 << 50)) ttl = ((u128)1 << 50) - 1;
   return (int64_t)ttl;
 }
 

@@ -25,7 +25,7 @@
 extern "C" {
 #endif
 
-uint64_t or_isqrt(uint64_t x);
+uint64_t or_isqrt(uint64_t lo, uint64_t hi);  /* floor(sqrt(hi 2^64 + lo)) */
 /* B(delta) of PAPER.md:469-474 in integer µs; s2 = s2_hi*2^64 + s2_lo. */
 int64_t or_bernstein(int64_t n, int64_t s1, uint64_t s2_lo, uint64_t s2_hi,
                      uint64_t lq, int64_t b_us);

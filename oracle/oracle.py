@@ -25,8 +25,10 @@ def build(force: bool = False) -> str:
     if alt:
         return alt
     if force or not os.path.exists(LIB) or os.path.getmtime(LIB) < os.path.getmtime(SRC):
-        subprocess.check_call(["g++", "-O2", "-std=c++17", "-shared", "-fPIC", "-o", LIB, SRC,
-                               "-lpthread"])
+        # build beside it and rename: a process that has the old library mapped keeps it
+        subprocess.check_call(["g++", "-O2", "-std=c++17", "-shared", "-fPIC", "-o", LIB + ".tmp",
+                               SRC, "-lpthread"])
+        os.replace(LIB + ".tmp", LIB)
     return LIB
 
 
@@ -39,7 +41,7 @@ def lib():
         _lib = C.CDLL(build())
         i64, u64, p = C.c_int64, C.c_uint64, C.c_void_p
         _lib.or_isqrt.restype = u64
-        _lib.or_isqrt.argtypes = [u64]
+        _lib.or_isqrt.argtypes = [u64, u64]
         _lib.or_bernstein.restype = i64
         _lib.or_bernstein.argtypes = [i64, i64, u64, u64, u64, i64]
         for f in ("or_select_bound",):
@@ -85,7 +87,8 @@ def stats_row(samples_us, b_us: int | None = None) -> np.ndarray:
 
 
 def isqrt(x: int) -> int:
-    return int(lib().or_isqrt(x))
+    """floor(sqrt(x)) for 0 <= x < 2^128."""
+    return int(lib().or_isqrt(x & (2**64 - 1), x >> 64))
 
 
 def bernstein(n: int, s1: int, s2: int, lq: int, b_us: int) -> int:

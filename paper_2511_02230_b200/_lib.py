@@ -9,7 +9,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.environ.get("CT_LIB_PATH") or os.path.join(HERE, "libcontinuum.so")  # override: experiments only
+LIB_PATH = os.path.join(HERE, "libcontinuum.so")
 
 i32, i64, u64, vp = C.c_int32, C.c_int64, C.c_uint64, C.c_void_p
 
@@ -18,6 +18,8 @@ MAX_J = 64
 
 # every symbol include/continuum.h declares (checked by tests/test_abi.py)
 EXPORTS = ["ct_version", "ct_last_error", "ct_ctx_create", "ct_ctx_destroy", "ct_fit_ttl",
+           "ct_fit_acc_words", "ct_fit_ttl_partial", "ct_fit_ttl_finish", "ct_bernstein",
+           "ct_calc_ttl_batch", "ct_bernstein_ref", "ct_calc_ttl_ref", "ct_validate_trace_set",
            "ct_simulate_batch", "ct_simulate_batch_ex", "ct_simulate_batch_host", "ct_jct_stats",
            "ct_last_launch", "ct_ctx_set_timing", "ct_synthesize_traces", "ct_parse_tool_name",
            "ct_load_trace_jsonl"]
@@ -57,11 +59,16 @@ class Policy(C.Structure):
 class Sweep(C.Structure):
     _fields_ = [("n_seeds", i32), ("n_rates", i32), ("n_kv", i32), ("n_policies", i32),
                 ("gap_us", vp), ("kv_blocks", vp), ("policies", vp), ("est", EstimatorParams),
-                ("fitted_ttl", vp), ("fitted_j", i32), ("reserved", i32)]
+                ("fitted_ttl", vp), ("fitted_j", i32), ("fitted_rows", i32)]
 
 
 class Samples(C.Structure):
-    _fields_ = [("dur_us", vp), ("tool_off", vp), ("n", i64), ("n_tools", i32), ("reserved", i32)]
+    _fields_ = [("dur_us", vp), ("tool_off", vp), ("tool_u8", vp), ("n", i64), ("n_tools", i32),
+                ("reserved", i32)]
+
+
+class StatRow(C.Structure):
+    _fields_ = [("n", i64), ("s1", i64), ("s2_lo", u64), ("s2_hi", u64)]
 
 
 class CostParams(C.Structure):
@@ -71,7 +78,7 @@ class CostParams(C.Structure):
 
 
 class TtlTable(C.Structure):
-    _fields_ = [("ttl_argmax", vp), ("ttl_paper", vp), ("stats", vp)]
+    _fields_ = [("ttl_argmax", vp), ("ttl_paper", vp), ("stats", vp), ("n_invalid", vp)]
 
 
 class LaunchInfo(C.Structure):
@@ -98,6 +105,20 @@ def lib() -> C.CDLL:
         L.ct_ctx_destroy.argtypes = [vp]
         L.ct_fit_ttl.argtypes = [vp, C.POINTER(Samples), C.POINTER(CostParams),
                                  C.POINTER(EstimatorParams), C.POINTER(TtlTable), vp]
+        L.ct_fit_acc_words.restype = i64
+        L.ct_fit_acc_words.argtypes = [i32, i32]
+        L.ct_fit_ttl_partial.argtypes = [vp, C.POINTER(Samples), C.POINTER(CostParams),
+                                         C.POINTER(EstimatorParams), i32, i32, vp, vp]
+        L.ct_fit_ttl_finish.argtypes = [vp, vp, i32, C.POINTER(CostParams),
+                                        C.POINTER(EstimatorParams), C.POINTER(TtlTable), vp]
+        L.ct_bernstein.argtypes = [vp, vp, i64, C.POINTER(EstimatorParams), vp, vp]
+        L.ct_calc_ttl_batch.argtypes = [vp, vp, vp, vp, vp, i64, C.POINTER(EstimatorParams), vp, vp]
+        L.ct_bernstein_ref.restype = i64
+        L.ct_bernstein_ref.argtypes = [C.POINTER(StatRow), C.POINTER(EstimatorParams)]
+        L.ct_calc_ttl_ref.restype = i64
+        L.ct_calc_ttl_ref.argtypes = [C.POINTER(StatRow), C.POINTER(StatRow),
+                                      C.POINTER(EstimatorParams), i64, i64]
+        L.ct_validate_trace_set.argtypes = [vp, C.POINTER(TraceSet), C.POINTER(Sweep), i64, i64, vp]
         L.ct_simulate_batch.argtypes = [vp, C.POINTER(TraceSet), C.POINTER(Sweep),
                                         C.POINTER(EngineParams), i64, i64, vp, vp, vp]
         L.ct_simulate_batch_ex.argtypes = [vp, C.POINTER(TraceSet), C.POINTER(Sweep),
@@ -114,7 +135,9 @@ def lib() -> C.CDLL:
                                          C.POINTER(i32)]
         L.ct_load_trace_jsonl.argtypes = [C.c_char_p, i32, i64, vp, i32, vp, i64, vp, i64,
                                           C.POINTER(i64)]
-        for f in ("ct_ctx_create", "ct_ctx_destroy", "ct_fit_ttl", "ct_simulate_batch",
+        for f in ("ct_ctx_create", "ct_ctx_destroy", "ct_fit_ttl", "ct_fit_ttl_partial",
+                  "ct_fit_ttl_finish", "ct_bernstein", "ct_calc_ttl_batch",
+                  "ct_validate_trace_set", "ct_simulate_batch",
                   "ct_simulate_batch_ex", "ct_simulate_batch_host", "ct_synthesize_traces", "ct_jct_stats", "ct_last_launch", "ct_ctx_set_timing",
                   "ct_parse_tool_name", "ct_load_trace_jsonl"):
             getattr(L, f).restype = C.c_int

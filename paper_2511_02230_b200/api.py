@@ -131,13 +131,13 @@ class _SweepStruct:
             pols[i] = L.Policy(p.priority, p.pause, p.dram, p.flags, p.t_pin_us, p.t_thresh_us, (0, 0))
         self.pols = pols
         self.fitted = fitted
-        fptr, fj = 0, 0
+        fptr, fj, frows = 0, 0, 0
         if fitted is not None:
             assert fitted.is_cuda and fitted.dtype == torch.int64 and fitted.is_contiguous()
-            fptr, fj = fitted.data_ptr(), int(fitted.shape[1])
+            fptr, fj, frows = fitted.data_ptr(), int(fitted.shape[1]), int(fitted.shape[0])
         self.s = L.Sweep(sweep.n_seeds, len(self.gap), len(self.kv), len(sweep.policies),
                          self.gap.ctypes.data, self.kv.ctypes.data, C.addressof(pols),
-                         estimator_params(sweep.estimator), fptr, fj, 0)
+                         estimator_params(sweep.estimator), fptr, fj, frows)
 
 
 def _fitted_tensor(sweep, device):
@@ -236,28 +236,137 @@ def cost_params(c_pf_ps: int, c_pin_ps: int, bs: int, a_num: int, a_den: int, gr
     return cp
 
 
-def ct_fit_ttl(ctx: Context, dur_us: torch.Tensor, tool_off, cost: L.CostParams, est, stream=None,
-               want_stats: bool = True):
-    """TTL fit over device samples grouped by tool.
-
-    dur_us: int32 device tensor [n]; tool_off: host int64 [F+1].
-    Returns (ttl_argmax int64[F+1, J], ttl_paper int64[F+1], stats int64[F+1, 4] or None).
-    """
+def _samples(dur_us: torch.Tensor, tool_off, tool_u8: torch.Tensor | None, n_tools: int | None):
     assert dur_us.is_cuda and dur_us.dtype == torch.int32 and dur_us.is_contiguous()
+    if tool_off is None:  # unsorted (dur, u8 tool) layout
+        assert tool_u8 is not None and tool_u8.is_cuda and tool_u8.dtype == torch.uint8
+        assert tool_u8.is_contiguous() and tool_u8.numel() == dur_us.numel() and n_tools
+        return L.Samples(dur_us.data_ptr(), None, tool_u8.data_ptr(), int(dur_us.numel()),
+                         int(n_tools), 0), int(n_tools), None
     off = np.ascontiguousarray(tool_off, dtype=np.int64)
     F = off.shape[0] - 1
-    J = cost.J
-    dev = dur_us.device
+    return L.Samples(dur_us.data_ptr(), off.ctypes.data, None, int(off[-1]), F, 0), F, off
+
+
+def _table(F: int, J: int, dev, want_stats: bool):
     arg = torch.empty((F + 1, J), dtype=torch.int64, device=dev)
     pap = torch.empty(F + 1, dtype=torch.int64, device=dev)
     st = torch.empty((F + 1, 4), dtype=torch.int64, device=dev) if want_stats else None
-    sm = L.Samples(dur_us.data_ptr(), off.ctypes.data, int(off[-1]), F, 0)
-    tab = L.TtlTable(arg.data_ptr(), pap.data_ptr(), st.data_ptr() if st is not None else None)
+    bad = torch.empty(1, dtype=torch.int64, device=dev)
+    tab = L.TtlTable(arg.data_ptr(), pap.data_ptr(), st.data_ptr() if st is not None else None,
+                     bad.data_ptr())
+    return arg, pap, st, bad, tab
+
+
+def ct_fit_ttl(ctx: Context, dur_us: torch.Tensor, tool_off, cost: L.CostParams, est, stream=None,
+               want_stats: bool = True, tool_u8: torch.Tensor | None = None,
+               n_tools: int | None = None, want_invalid: bool = False):
+    """TTL fit over device samples.
+
+    CSR layout: dur_us int32 device tensor [n] grouped by tool, tool_off host int64 [F+1].
+    Unsorted layout: tool_off=None, tool_u8 uint8 device tensor [n], n_tools = F.
+    Returns (ttl_argmax int64[F+1, J], ttl_paper int64[F+1], stats int64[F+1, 4] or None), plus
+    n_invalid int64[1] (device) when want_invalid.
+    """
+    sm, F, _off = _samples(dur_us, tool_off, tool_u8, n_tools)
+    arg, pap, st, bad, tab = _table(F, cost.J, dur_us.device, want_stats)
     e = estimator_params(est)
     rc = L.lib().ct_fit_ttl(ctx.handle, C.byref(sm), C.byref(cost), C.byref(e), C.byref(tab),
                             _stream_ptr(stream))
     L.check(rc, "ct_fit_ttl")
-    return arg, pap, st
+    return (arg, pap, st, bad) if want_invalid else (arg, pap, st)
+
+
+def ct_fit_acc_words(n_tools: int, K: int) -> int:
+    w = int(L.lib().ct_fit_acc_words(int(n_tools), int(K)))
+    if w < 0:
+        raise L.CtError("ct_fit_acc_words: n_tools / K out of range")
+    return w
+
+
+def ct_fit_ttl_partial(ctx: Context, dur_us: torch.Tensor, tool_off, cost: L.CostParams, est,
+                       rank: int, world: int, acc: torch.Tensor | None = None, stream=None):
+    """Accumulator (int64 [ct_fit_acc_words(F, K)], device) of this rank's slice of every tool
+    segment; sum it over the ranks (all-reduce) and pass it to ct_fit_ttl_finish."""
+    sm, F, _off = _samples(dur_us, tool_off, None, None)
+    if acc is None:
+        acc = torch.empty(ct_fit_acc_words(F, cost.K), dtype=torch.int64, device=dur_us.device)
+    assert acc.is_cuda and acc.dtype == torch.int64 and acc.numel() >= ct_fit_acc_words(F, cost.K)
+    e = estimator_params(est)
+    rc = L.lib().ct_fit_ttl_partial(ctx.handle, C.byref(sm), C.byref(cost), C.byref(e), int(rank),
+                                    int(world), acc.data_ptr(), _stream_ptr(stream))
+    L.check(rc, "ct_fit_ttl_partial")
+    return acc
+
+
+def ct_fit_ttl_finish(ctx: Context, acc: torch.Tensor, n_tools: int, cost: L.CostParams, est,
+                      stream=None, want_stats: bool = True, want_invalid: bool = False):
+    """Tables from a (reduced) accumulator; same outputs as ct_fit_ttl."""
+    assert acc.is_cuda and acc.dtype == torch.int64 and acc.is_contiguous()
+    arg, pap, st, bad, tab = _table(int(n_tools), cost.J, acc.device, want_stats)
+    e = estimator_params(est)
+    rc = L.lib().ct_fit_ttl_finish(ctx.handle, acc.data_ptr(), int(n_tools), C.byref(cost),
+                                   C.byref(e), C.byref(tab), _stream_ptr(stream))
+    L.check(rc, "ct_fit_ttl_finish")
+    return (arg, pap, st, bad) if want_invalid else (arg, pap, st)
+
+
+def _stat_row(r) -> L.StatRow:
+    """(n, s1, s2) with s2 a Python int, or (n, s1, s2_lo, s2_hi)."""
+    r = [int(x) for x in r]
+    if len(r) == 3:
+        r = [r[0], r[1], r[2] & (2**64 - 1), r[2] >> 64]
+    return L.StatRow(r[0], r[1], r[2] & (2**64 - 1), r[3] & (2**64 - 1))
+
+
+def ct_bernstein(ctx: Context, rows: torch.Tensor, est, stream=None) -> torch.Tensor:
+    """B(delta) per statistics row; rows int64 device tensor [n, 4] = {n, s1, s2_lo, s2_hi}."""
+    assert rows.is_cuda and rows.dtype == torch.int64 and rows.shape[-1] == 4 and rows.is_contiguous()
+    out = torch.empty(rows.shape[0], dtype=torch.int64, device=rows.device)
+    e = estimator_params(est)
+    rc = L.lib().ct_bernstein(ctx.handle, rows.data_ptr(), int(rows.shape[0]), C.byref(e),
+                              out.data_ptr(), _stream_ptr(stream))
+    L.check(rc, "ct_bernstein")
+    return out
+
+
+def ct_calc_ttl_batch(ctx: Context, g: torch.Tensor, f: torch.Tensor, n_done: torch.Tensor,
+                      turns_done: torch.Tensor, est, stream=None) -> torch.Tensor:
+    """CalcTTL offset per query (global row g[i], tool row f[i], D = n_done[i])."""
+    n = int(g.shape[0])
+    for t in (g, f, n_done, turns_done):
+        assert t.is_cuda and t.dtype == torch.int64 and t.is_contiguous() and t.shape[0] == n
+    out = torch.empty(n, dtype=torch.int64, device=g.device)
+    e = estimator_params(est)
+    rc = L.lib().ct_calc_ttl_batch(ctx.handle, g.data_ptr(), f.data_ptr(), n_done.data_ptr(),
+                                   turns_done.data_ptr(), n, C.byref(e), out.data_ptr(),
+                                   _stream_ptr(stream))
+    L.check(rc, "ct_calc_ttl_batch")
+    return out
+
+
+def ct_bernstein_ref(row, est) -> int:
+    e = estimator_params(est)
+    r = _stat_row(row)
+    return int(L.lib().ct_bernstein_ref(C.byref(r), C.byref(e)))
+
+
+def ct_calc_ttl_ref(g, f, est, n_done: int, turns_done: int) -> int:
+    e = estimator_params(est)
+    gr, fr = _stat_row(g), _stat_row(f)
+    return int(L.lib().ct_calc_ttl_ref(C.byref(gr), C.byref(fr), C.byref(e), int(n_done),
+                                       int(turns_done)))
+
+
+def ct_validate_trace_set(ctx: Context, trace: "DeviceTrace", sweep, replica_begin: int = 0,
+                          replica_end: int | None = None, stream=None) -> None:
+    """Synchronous check of a device trace set against ct_simulate_batch's preconditions;
+    raises CtError naming the first invalid program."""
+    sw = _SweepStruct(sweep, _fitted_tensor(sweep, trace.programs.device))
+    re_ = sweep.n_replicas if replica_end is None else int(replica_end)
+    rc = L.lib().ct_validate_trace_set(ctx.handle, C.byref(trace.struct()), C.byref(sw.s),
+                                       int(replica_begin), re_, _stream_ptr(stream))
+    L.check(rc, "ct_validate_trace_set")
 
 
 def ct_jct_stats(ctx: Context, summary: torch.Tensor, n_cells: int, out: torch.Tensor | None = None,

@@ -19,10 +19,10 @@ struct ct_ctx {
   unsigned long long* counter = nullptr;
   void* axes = nullptr;
   size_t axes_cap = 0;
-  void* fit = nullptr;
-  size_t fit_cap = 0;
-  void* chunks = nullptr;
-  size_t chunks_cap = 0;
+  void* fitbuf[2] = {nullptr, nullptr};  // double-buffered fit accumulator (ct_fit_ttl)
+  size_t fitbuf_cap[2] = {0, 0};
+  int64_t fit_clean[2] = {0, 0};  // leading words known to be zero
+  int fit_cur = 0;
   void* h_progs = nullptr;
   size_t h_progs_cap = 0;
   void* h_turns = nullptr;
@@ -36,7 +36,8 @@ struct ct_ctx {
   void* syn = nullptr;  // synthesis: tables | cdf | class | per-program class | seed totals | blocks
   size_t syn_cap = 0;
   ct_launch_info last{};
-  int fit_occ = 0, fit_occ_smem = -1, fit_occ_v = -1;
+  int fit_occ = 0, fit_occ_key = -1;
+  bool fit_occ_step1 = false;
   bool timing = false;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};  // replay start/end, fit start/end
   bool replay_timed = false, fit_timed = false;
@@ -79,10 +80,31 @@ int ensure(void** p, size_t* cap, size_t need) {
   return CT_OK;
 }
 
+// Estimator bounds: T_default^2 < 2^80 and (D a_den + a_num turns_done) < 2^45 (D <= 256,
+// turns_done <= 256 CT_MAX_TURNS = 2^24) keep CalcTTL's numerator below 2^125.
 bool est_valid(const ct_estimator_params& e) {
   return e.lq > 0 && e.b_us > 0 && e.t_default_us > 0 && e.n_min >= 1 && e.a_num >= 0 &&
          e.a_den >= 1 && e.ttl_max_us >= 0 && e.b_us < (1ll << 40) &&
-         e.t_default_us < (1ll << 40) && e.lq < (1ull << 40);
+         e.t_default_us < (1ll << 40) && e.lq < (1ull << 40) && e.a_num < (1ll << 20) &&
+         e.a_den < (1ll << 20) && e.ttl_max_us < CT_TTL_SAT && e.n_min < (1ll << 40);
+}
+
+// Largest arr_q with arr_q * gap < 2^62 for every gap of the sweep (arrivals < 2^42 µs).
+int64_t arr_q_max(const ct_sweep* sw) {
+  int64_t g = 0;
+  for (int i = 0; i < sw->n_rates; ++i) g = std::max<int64_t>(g, sw->gap_us[i]);
+  return g == 0 ? INT64_MAX : (int64_t)(((1ll << 62) - 1) / g);
+}
+
+const char* check_reason(uint32_t bits) {
+  if (bits & CT_CHECK_NTURNS) return "nturns outside [1, CT_MAX_TURNS]";
+  if (bits & CT_CHECK_TURN_RANGE) return "turn0 / nturns outside the turn array";
+  if (bits & CT_CHECK_ARRIVAL) return "arr_q negative, arr_q * gap >= 2^62, or arrivals not sorted";
+  if (bits & CT_CHECK_TOKENS) return "decode_tokens < 1 or new_tokens < 0";
+  if (bits & CT_CHECK_TOOL) return "non-final turn with tool outside [0, n_tools) or dur_us < 1";
+  if (bits & CT_CHECK_CONTEXT) return "total new + decode tokens of a program > CT_MAX_CONTEXT";
+  if (bits & CT_CHECK_FITTED) return "FITTED table entry outside [0, CT_TTL_SAT)";
+  return "invalid trace set";
 }
 
 typedef __int128 i128;
@@ -120,7 +142,7 @@ int ct_ctx_create(int device, ct_ctx** out) {
 
 int ct_ctx_destroy(ct_ctx* c) {
   if (!c) return CT_OK;
-  void* ps[] = {c->counter, c->axes, c->fit, c->chunks, c->h_progs, c->h_turns, c->h_out, c->h_jct, c->syn,
+  void* ps[] = {c->counter, c->axes, c->fitbuf[0], c->fitbuf[1], c->h_progs, c->h_turns, c->h_out, c->h_jct, c->syn,
                 c->fb};
   for (void* p : ps)
     if (p) cudaFree(p);
@@ -186,6 +208,16 @@ int ct_simulate_batch_ex(ct_ctx* c, const ct_trace_set* tr, const ct_sweep* sw,
   if (E.c0_ps >= (1ll << 48) || E.c_pf_ps >= (1ll << 40) || E.c_kv_ps >= (1ll << 30) ||
       E.c_h2d_ps >= (1ll << 40) || E.bs >= (1 << 20) || E.dram_blocks >= (1ll << 30))
     return fail(CT_EINVAL, "engine constants exceed the int64 fixed-point bounds");
+  {  // one iteration's ps: c0 + c_pf x prefill + c_kv x bs x resident blocks, where prefill and
+     // resident tokens are both bounded by the pool (kv_max x bs); one DRAM load: blocks x c_h2d
+    int64_t kvm = 0;
+    for (int i = 0; i < sw->n_kv; ++i) kvm = std::max<int64_t>(kvm, sw->kv_blocks[i]);
+    const i128 it = (i128)E.c0_ps + ((i128)E.c_pf_ps + E.c_kv_ps) * E.bs * kvm;
+    if (it >= ((i128)1 << 62))
+      return fail(CT_EINVAL, "c0 + (c_pf + c_kv) bs max(kv_blocks) >= 2^62 ps (iteration cost overflow)");
+    if ((i128)E.dram_blocks * E.c_h2d_ps >= ((i128)1 << 62))
+      return fail(CT_EINVAL, "dram_blocks x c_h2d >= 2^62 ps (load time overflow)");
+  }
   if (E.kv_growth != 0 && E.kv_growth != 1) return fail(CT_EINVAL, "kv_growth must be 0 or 1");
   if (E.prefill_chunk < 0 || (E.prefill_chunk > 0 && E.prefill_chunk < E.max_batch))
     return fail(CT_EINVAL, "prefill_chunk must be 0 (off) or >= max_batch (R31)");
@@ -200,15 +232,16 @@ int ct_simulate_batch_ex(ct_ctx* c, const ct_trace_set* tr, const ct_sweep* sw,
       return fail(CT_EINVAL, "policy %d: pause %d", i, p.pause);
     if (p.flags & ~(CT_FLAG_VICTIMS_ANY | CT_FLAG_STEP_EXPIRY))
       return fail(CT_EINVAL, "policy %d: unknown flags", i);
-    if (p.t_pin_us < 0 || p.t_pin_us >= (1ll << 50)) return fail(CT_EINVAL, "policy %d: t_pin", i);
+    if (p.t_pin_us < 0 || p.t_pin_us >= CT_TTL_SAT) return fail(CT_EINVAL, "policy %d: t_pin", i);
     need_est |= p.pause == CT_PAUSE_PAPER || p.pause == CT_PAUSE_INFERCEPT ||
                 (p.pause == CT_PAUSE_FIXED && p.t_thresh_us != CT_ALWAYS);
     need_fit |= p.pause == CT_PAUSE_FITTED;
     need_h2d |= p.dram != 0 && E.dram_blocks > 0;
   }
   if (need_est && !est_valid(sw->est)) return fail(CT_EINVAL, "invalid estimator parameters");
-  if (need_fit && (!sw->fitted_ttl || sw->fitted_j < 1 || sw->fitted_j > CT_MAX_J))
-    return fail(CT_EINVAL, "FITTED policy needs fitted_ttl[n_tools][fitted_j]");
+  if (need_fit && (!sw->fitted_ttl || sw->fitted_j < 1 || sw->fitted_j > CT_MAX_J ||
+                   sw->fitted_rows < F))
+    return fail(CT_EINVAL, "FITTED policy needs fitted_ttl[fitted_rows >= n_tools][fitted_j]");
   if (need_h2d && E.c_h2d_ps < 1) return fail(CT_EINVAL, "DRAM tier needs c_h2d_ps >= 1 (R25)");
   for (int i = 0; i < sw->n_rates; ++i)
     if (sw->gap_us[i] < 0 || sw->gap_us[i] >= (1ll << 30)) return fail(CT_EINVAL, "gap_us[%d]", i);
@@ -228,7 +261,26 @@ int ct_simulate_batch_ex(ct_ctx* c, const ct_trace_set* tr, const ct_sweep* sw,
   std::memcpy(hb.data() + 8 * n_gap, sw->kv_blocks, 8 * n_kv);
   std::memcpy(hb.data() + 8 * (n_gap + n_kv), sw->policies, sizeof(ct_policy) * n_pol);
   CT_CUDA(cudaMemcpyAsync(c->axes, hb.data(), bytes, cudaMemcpyHostToDevice, s));
-  CT_CUDA(cudaMemsetAsync(c->counter, 0, 8, s));
+  // counter block: [0] replica counter, [1] fallback list count, [2] fallback counter,
+  // [4..5] trace check result
+  CT_CUDA(cudaMemsetAsync(c->counter, 0, 48, s));
+  {
+    ct::CheckArgs ck;
+    const int64_t per_seed = (int64_t)sw->n_rates * sw->n_kv * sw->n_policies;
+    ck.progs = tr->programs;
+    ck.turns = (const int4*)tr->turns;
+    ck.n_turns = tr->n_turns;
+    ck.p_begin = rb / per_seed * P;
+    ck.p_end = ((re - 1) / per_seed + 1) * P;
+    ck.P = P;
+    ck.F = F;
+    ck.arr_max = arr_q_max(sw);
+    ck.fitted = need_fit ? sw->fitted_ttl : nullptr;
+    ck.n_fitted = need_fit ? (int64_t)F * sw->fitted_j : 0;
+    ck.err = c->counter + 4;
+    cudaError_t e = ct::launch_check_traces(ck, c->sm_count, s);
+    if (e != cudaSuccess) return cuda_fail(e, "trace check launch");
+  }
 
   ct::ReplayArgs a;
   a.progs = tr->programs;
@@ -251,6 +303,7 @@ int ct_simulate_batch_ex(ct_ctx* c, const ct_trace_set* tr, const ct_sweep* sw,
   a.jct = jct;
   a.bubble = outs->bubble_us;
   a.counter = c->counter;
+  a.err = c->counter + 4;
   a.bs_magic = E.bs == 1 ? 0
                          : (uint64_t)(((((unsigned __int128)1) << 64) + (uint64_t)E.bs - 1) /
                                       (unsigned __int128)(uint64_t)E.bs);
@@ -289,7 +342,6 @@ int ct_simulate_batch_ex(ct_ctx* c, const ct_trace_set* tr, const ct_sweep* sw,
     rc = ensure(&c->fb, &c->fb_cap, 8 * (size_t)(re - rb));
     if (rc) return rc;
     a.fb_list = (int64_t*)c->fb;
-    CT_CUDA(cudaMemsetAsync(c->counter + 1, 0, 16, s));
   }
   const int mode1 = ns32 ? (mode == 1 ? 4 : 5) : mode;
   a.smem_per_warp = ns32 ? ct::replay_ns32_smem_per_warp(ns, F)
@@ -321,9 +373,52 @@ int ct_simulate_batch_ex(ct_ctx* c, const ct_trace_set* tr, const ct_sweep* sw,
   c->last.warps_per_block = wpb;
   c->last.slots_per_lane = ns;
   c->last.smem_per_block = smem;
-  c->last.launches = ns32 ? 2 : 1;
+  c->last.launches = (ns32 ? 2 : 1) + 1;  // + the trace check
   c->last.kernel_mode = mode1;
   return CT_OK;
+}
+
+int ct_validate_trace_set(ct_ctx* c, const ct_trace_set* tr, const ct_sweep* sw,
+                          int64_t rb, int64_t re, void* stream) {
+  if (!c || !tr || !sw) return fail(CT_EINVAL, "NULL argument");
+  const int P = tr->n_programs, F = tr->n_tools;
+  if (P < 1 || P > CT_MAX_PROGRAMS || F < 1 || F > CT_MAX_TOOLS || !tr->programs || !tr->turns ||
+      tr->n_turns < 1)
+    return fail(CT_EINVAL, "invalid trace-set shape");
+  if (sw->n_seeds < 1 || sw->n_rates < 1 || sw->n_kv < 1 || sw->n_policies < 1 || !sw->gap_us ||
+      sw->n_seeds > tr->n_seeds)
+    return fail(CT_EINVAL, "invalid sweep axes");
+  const int64_t per_seed = (int64_t)sw->n_rates * sw->n_kv * sw->n_policies;
+  const int64_t R = per_seed * sw->n_seeds;
+  if (rb < 0 || re < rb || re > R) return fail(CT_EINVAL, "replica range");
+  if (re == rb) return CT_OK;
+  bool need_fit = false;
+  for (int i = 0; sw->policies && i < sw->n_policies; ++i) need_fit |= sw->policies[i].pause == CT_PAUSE_FITTED;
+  cudaStream_t s = (cudaStream_t)stream;
+  CT_CUDA(cudaMemsetAsync(c->counter + 4, 0, 16, s));
+  ct::CheckArgs ck;
+  ck.progs = tr->programs;
+  ck.turns = (const int4*)tr->turns;
+  ck.n_turns = tr->n_turns;
+  ck.p_begin = rb / per_seed * P;
+  ck.p_end = ((re - 1) / per_seed + 1) * P;
+  ck.P = P;
+  ck.F = F;
+  ck.arr_max = arr_q_max(sw);
+  ck.fitted = need_fit ? sw->fitted_ttl : nullptr;
+  if (need_fit && (!sw->fitted_ttl || sw->fitted_j < 1 || sw->fitted_j > CT_MAX_J || sw->fitted_rows < F))
+    return fail(CT_EINVAL, "FITTED policy needs fitted_ttl[fitted_rows >= n_tools][fitted_j]");
+  ck.n_fitted = need_fit ? (int64_t)F * sw->fitted_j : 0;
+  ck.err = c->counter + 4;
+  cudaError_t e = ct::launch_check_traces(ck, c->sm_count, s);
+  if (e != cudaSuccess) return cuda_fail(e, "trace check launch");
+  unsigned long long h[2];
+  CT_CUDA(cudaMemcpyAsync(h, c->counter + 4, 16, cudaMemcpyDeviceToHost, s));
+  CT_CUDA(cudaStreamSynchronize(s));
+  if (h[0] == 0) return CT_OK;
+  if (h[1] != 0)
+    return fail(CT_EINVAL, "program %lld: %s", (long long)~h[1], check_reason((uint32_t)h[0]));
+  return fail(CT_EINVAL, "%s", check_reason((uint32_t)h[0]));
 }
 
 int ct_simulate_batch_host(ct_ctx* c, const ct_trace_set* ht, const ct_sweep* sw,
@@ -333,22 +428,27 @@ int ct_simulate_batch_host(ct_ctx* c, const ct_trace_set* ht, const ct_sweep* sw
   const int P = ht->n_programs, F = ht->n_tools;
   if (P < 1 || P > CT_MAX_PROGRAMS || F < 1 || F > CT_MAX_TOOLS || ht->n_seeds < 1 || ht->n_turns < 1)
     return fail(CT_EINVAL, "invalid trace-set shape");
-  // host-side trace validation (the device variant takes these as preconditions)
+  // host-side trace validation (the device path checks the same on the device)
+  if (!sw || !sw->gap_us || sw->n_rates < 1) return fail(CT_EINVAL, "NULL sweep axis");
+  const int64_t arr_max = arr_q_max(sw);
   const int64_t np = (int64_t)ht->n_seeds * P;
   for (int64_t i = 0; i < np; ++i) {
     const ct_program& p = ht->programs[i];
-    if (p.nturns < 1 || p.turn0 < 0 || (int64_t)p.turn0 + p.nturns > ht->n_turns || p.arr_q < 0 ||
-        p.arr_q >= (1ll << 32))
+    if (p.nturns < 1 || p.nturns > CT_MAX_TURNS || p.turn0 < 0 ||
+        (int64_t)p.turn0 + p.nturns > ht->n_turns || p.arr_q < 0 || p.arr_q > arr_max)
       return fail(CT_EINVAL, "program %lld invalid", (long long)i);
     if (i % P && p.arr_q < ht->programs[i - 1].arr_q)
       return fail(CT_EINVAL, "arrivals not sorted in seed %lld", (long long)(i / P));
+    int64_t ctx = 0;
     for (int t = 0; t < p.nturns; ++t) {
       const ct_turn& u = ht->turns[p.turn0 + t];
       const bool last = t == p.nturns - 1;
       if (u.decode_tokens < 1 || u.new_tokens < 0 ||
           (!last && (u.tool < 0 || u.tool >= F || u.dur_us < 1)))
         return fail(CT_EINVAL, "turn %d of program %lld invalid", t, (long long)i);
+      ctx += (int64_t)u.new_tokens + u.decode_tokens;
     }
+    if (ctx > CT_MAX_CONTEXT) return fail(CT_EINVAL, "program %lld: context > CT_MAX_CONTEXT", (long long)i);
   }
   cudaStream_t s = (cudaStream_t)stream;
   const int64_t R = re - rb;
@@ -372,84 +472,94 @@ int ct_simulate_batch_host(ct_ctx* c, const ct_trace_set* ht, const ct_sweep* sw
 }
 
 // ---------------------------------------------------------------------------------------------
-int ct_fit_ttl(ct_ctx* c, const ct_samples* sm, const ct_cost_params* cp,
-               const ct_estimator_params* est, ct_ttl_table* out, void* stream) {
-  if (!c || !sm || !cp || !est || !out || !out->ttl_argmax || !out->ttl_paper)
-    return fail(CT_EINVAL, "NULL argument");
+namespace {
+
+// Validation and launch arguments shared by the fit calls.  Fills fa (except acc/zero) and sa
+// (except acc and the outputs).
+int fit_prepare(ct_ctx* c, const ct_samples* sm, const ct_cost_params* cp,
+                const ct_estimator_params* est, int rank, int world, ct::FitArgs& fa,
+                ct::ScanArgs& sa, ct::FitPlan& plan) {
+  if (!c || !sm || !cp || !est) return fail(CT_EINVAL, "NULL argument");
   const int F = sm->n_tools, K = cp->K, J = cp->J;
   if (F < 1 || F > CT_MAX_TOOLS) return fail(CT_EINVAL, "n_tools %d", F);
   if (K < 1 || K > CT_MAX_K || J < 1 || J > CT_MAX_J) return fail(CT_EINVAL, "K %d / J %d", K, J);
-  if (!sm->tool_off || sm->tool_off[0] != 0 || sm->tool_off[F] != sm->n || sm->n < 0)
-    return fail(CT_EINVAL, "tool_off must run from 0 to n");
+  if (world < 1 || rank < 0 || rank >= world) return fail(CT_EINVAL, "rank %d of %d", rank, world);
+  const bool pairs = sm->tool_off == nullptr;
+  if (sm->n < 0) return fail(CT_EINVAL, "n < 0");
   if (sm->n > 0 && !sm->dur_us) return fail(CT_EINVAL, "dur_us is NULL");
-  for (int f = 0; f < F; ++f)
-    if (sm->tool_off[f + 1] < sm->tool_off[f]) return fail(CT_EINVAL, "tool_off not monotone");
+  if (pairs) {
+    if (sm->n > 0 && !sm->tool_u8) return fail(CT_EINVAL, "unsorted layout needs tool_u8");
+    if (world != 1) return fail(CT_EINVAL, "the unsorted layout is fitted on one rank");
+    if (((uintptr_t)sm->dur_us & 15) || ((uintptr_t)sm->tool_u8 & 3))
+      return fail(CT_EINVAL, "unsorted layout: dur_us must be 16-B and tool_u8 4-B aligned");
+  } else {
+    if (sm->tool_off[0] != 0 || sm->tool_off[F] != sm->n)
+      return fail(CT_EINVAL, "tool_off must run from 0 to n");
+    for (int f = 0; f < F; ++f)
+      if (sm->tool_off[f + 1] < sm->tool_off[f]) return fail(CT_EINVAL, "tool_off not monotone");
+    if (sm->n > 0 && ((uintptr_t)sm->dur_us & 15)) return fail(CT_EINVAL, "dur_us must be 16-B aligned");
+  }
   if (!est_valid(*est)) return fail(CT_EINVAL, "invalid estimator parameters");
   if (cp->grid_step_us < 1 || cp->bs < 1 || cp->a_den < 1 || cp->a_num < 0 || cp->c_pf_ps < 0 ||
-      cp->c_pin_ps < 0 || cp->avg_turns_num < 0 || cp->avg_turns_den < 0)
+      cp->c_pin_ps < 0 || cp->avg_turns_num < 0 || cp->avg_turns_den < 0 ||
+      cp->a_den >= (1ll << 32) || cp->a_num >= (1ll << 32) || cp->c_pf_ps >= (1ll << 40) ||
+      cp->c_pin_ps >= (1ll << 40) || cp->bs >= (1ll << 20) || cp->avg_turns_num >= (1ll << 40) ||
+      cp->avg_turns_den >= (1ll << 31))
     return fail(CT_EINVAL, "invalid cost parameters");
+  if (cp->grid_step_us >= (1ll << 31) || est->b_us >= (1ll << 31))
+    return fail(CT_EINVAL, "grid_step_us and b_us must be < 2^31");
   const i128 tau_max = (i128)(K - 1) * cp->grid_step_us;
   if (tau_max >= ((i128)1 << 43)) return fail(CT_EINVAL, "grid too long: (K-1)*step >= 2^43");
-  // 128-bit headroom of n U(k) (extension C-4)
   const i128 n = sm->n;
+  if (n >= ((i128)1 << 32)) return fail(CT_EINVAL, "too many samples (n >= 2^32)");
+  // 128-bit headroom of n U(k) (extension C-4): V cnt and C (sum + tau (n - cnt)), sum < n 2^31
   for (int j = 0; j < J; ++j) {
     if (cp->ctx_tokens[j] < 0 || cp->ctx_tokens[j] >= (1ll << 32) || cp->turn_weight[j] < 0 ||
         cp->turn_weight[j] >= (1ll << 32))
       return fail(CT_EINVAL, "ctx_tokens / turn_weight[%d] out of range", j);
-    i128 V = ((i128)cp->c_pf_ps * cp->ctx_tokens[j] * ((i128)cp->a_den + (i128)cp->a_num * cp->turn_weight[j])) / cp->a_den;
-    i128 C = (i128)cp->c_pin_ps * ((cp->ctx_tokens[j] + cp->bs - 1) / cp->bs);
+    const i128 V = ((i128)cp->c_pf_ps * cp->ctx_tokens[j] *
+                    ((i128)cp->a_den + (i128)cp->a_num * cp->turn_weight[j])) / cp->a_den;
+    const i128 C = (i128)cp->c_pin_ps * ((cp->ctx_tokens[j] + cp->bs - 1) / cp->bs);
     const i128 lim = (i128)1 << 125;
     if (V > lim / (n + 1) || C > lim / ((n + 1) * (((i128)1 << 31) + tau_max + 1)))
       return fail(CT_EINVAL, "cost products could overflow 128-bit arithmetic");
   }
-  if (n >= ((i128)1 << 32)) return fail(CT_EINVAL, "too many samples (n >= 2^32)");
   if (n * (i128)est->b_us * est->b_us >= ((i128)1 << 95))
     return fail(CT_EINVAL, "n * b^2 >= 2^95: sum of squares could overflow");
-  cudaStream_t s = (cudaStream_t)stream;
-  // chunk plan: <= CH samples per CTA work item so that a warp's 32-bit bins (count, sum of
-  // remainders < step) and a thread's 64-bit sum of squares cannot overflow
-  if (cp->grid_step_us >= (1ll << 31) || est->b_us >= (1ll << 31))
-    return fail(CT_EINVAL, "grid_step_us and b_us must be < 2^31");
-  // per warp chunk CH: a replica (32/R lanes) sees <= CH/R + 64 samples (32-bit remainder sums
-  // < 2^32, 16-bit packed counts < 2^16) and a lane <= CH/32 + 2 (64-bit sum of squares < 2^64)
-  // CTA-shared variant: CTA chunks of CH samples over 256 threads, a lane-index replica sees
-  // <= CH/32 + 64 samples and a thread <= CH/256 + 8.
-  const ct::FitPlan plan = ct::fit_plan(K, est->b_us);
-  const bool cta = plan.cta;
-  const int R = cta ? 1 : plan.repl;
-  const int per_thread_div = cta ? 256 : 32;
-  const bool ranges = plan.ranges;
-  int64_t CH = ranges ? (1ll << 20) : cta ? (1ll << 17) : (1ll << 16);
-  const int64_t rdiv = cta ? 32 : R;
-  while (CH > 256 && (CH / rdiv + 64) * (uint64_t)cp->grid_step_us >= (1ull << 32)) CH >>= 1;
-  while (CH > 256 && !cta && CH / R + 64 >= (1 << 16)) CH >>= 1;
-  {
-    const unsigned __int128 b2 = (unsigned __int128)est->b_us * est->b_us;
-    while (CH > 256 && (unsigned __int128)(CH / per_thread_div + 8) * b2 >= ((unsigned __int128)1 << 64)) CH >>= 1;
-  }
-  if (CH < 256) return fail(CT_EINVAL, "grid step / b too large for the histogram pass");
-  // rows 0..F-1 per tool, row F pooled (filled by fit_hist)
-  const size_t hbytes = 8 * (size_t)(F + 1) * (K + 1);
-  const size_t fbytes = 2 * hbytes + 8 * 6 * (size_t)(F + 1);
-  int rc = ensure(&c->fit, &c->fit_cap, fbytes);
-  if (rc) return rc;
-  CT_CUDA(cudaMemsetAsync(c->fit, 0, fbytes, s));
-  int launches = 0;
-  ct::FitArgs fa;
+  plan = ct::fit_plan(K, F, pairs);
+  if (!plan.ok)
+    return fail(CT_EINVAL, pairs ? "unsorted layout: F x (K+1) bins exceed shared memory (use CSR)"
+                                 : "K too large for the histogram pass");
   std::memset(&fa, 0, sizeof fa);
   fa.dur = sm->dur_us;
+  fa.tool_u8 = sm->tool_u8;
+  fa.n = sm->n;
   fa.F = F;
   fa.K = K;
-  fa.ch = CH;
-  for (int f = 0; f <= F; ++f) {
-    fa.tool_off[f] = sm->tool_off[f];
-    fa.chunk_off[f] = f == 0 ? 0 : fa.chunk_off[f - 1] + (sm->tool_off[f] - sm->tool_off[f - 1] + CH - 1) / CH;
-  }
-  fa.n_chunks = fa.chunk_off[F];
   fa.step = cp->grid_step_us;
-  // M = ceil(2^64 / step) < 2^63 for step >= 2; step == 1 runs the identity instantiation
-  fa.step_magic = cp->grid_step_us == 1 ? 0 : (uint64_t)((((unsigned __int128)1 << 64) + cp->grid_step_us - 1) / cp->grid_step_us);
   fa.b_us = est->b_us;
+  if (!pairs) {  // rank's slice of every tool segment; world 1 = everything
+    fa.voff[0] = 0;
+    for (int f = 0; f < F; ++f) {
+      const int64_t lo = sm->tool_off[f], len = sm->tool_off[f + 1] - lo;
+      fa.seg_lo[f] = lo + (int64_t)((i128)len * rank / world);
+      fa.seg_hi[f] = lo + (int64_t)((i128)len * (rank + 1) / world);
+      fa.voff[f + 1] = fa.voff[f] + (fa.seg_hi[f] - fa.seg_lo[f]);
+    }
+  }
+  // piece bound: a lane-index replica sees <= ch/lr + 64 samples of one piece (remainder sums
+  // < step each stay < 2^32), a thread <= ch/256 + 8 (64-bit sum of squares < 2^64); pairs:
+  // a (tool, bucket) bin sees <= ch samples
+  int64_t ch = 1ll << 20;
+  const int64_t rdiv = pairs ? 1 : plan.lr;
+  while (ch > 256 && (ch / rdiv + 64) * (uint64_t)cp->grid_step_us >= (1ull << 32)) ch >>= 1;
+  {
+    const unsigned __int128 b2 = (unsigned __int128)est->b_us * est->b_us;
+    while (ch > 256 && (unsigned __int128)(ch / 256 + 8) * b2 >= ((unsigned __int128)1 << 64)) ch >>= 1;
+  }
+  if (ch <= 256 && (256 / rdiv + 64) * (uint64_t)cp->grid_step_us >= (1ull << 32))
+    return fail(CT_EINVAL, "grid step too large for the histogram pass");
+  fa.ch = ch;
   if (cp->grid_step_us >= 2) {  // Granlund-Montgomery: floor(x / d) for every x < 2^32
     const uint32_t d = (uint32_t)cp->grid_step_us;
     const int fl = 31 - __builtin_clz(d);
@@ -468,46 +578,164 @@ int ct_fit_ttl(ct_ctx* c, const ct_samples* sm, const ct_cost_params* cp,
       }
     }
   }
-  fa.hcnt = (unsigned long long*)c->fit;
-  fa.hsum = fa.hcnt + (size_t)(F + 1) * (K + 1);
-  fa.stat = fa.hsum + (size_t)(F + 1) * (K + 1);
-  if (fa.n_chunks > 0) {
-    if (c->fit_occ_smem != plan.smem || c->fit_occ_v != plan.v) {
-      c->fit_occ = ct::fit_hist_occupancy(plan);
-      c->fit_occ_smem = plan.smem;
-      c->fit_occ_v = plan.v;
-    }
-    if (c->fit_occ < 1) return fail(CT_ECUDA, "fit_hist kernel cannot be resident");
-    // warp variants: every warp takes its own chunks; CTA variant: one chunk per CTA
-    const int wpb = plan.cta ? 1 : plan.threads / 32;
-    // range variant: >= 2^15 samples per CTA (each CTA zeroes and flushes a full histogram)
-    const int64_t items = ranges ? (fa.tool_off[F] - fa.tool_off[0] + (1 << 15) - 1) >> 15
-                                 : (fa.n_chunks + wpb - 1) / wpb;
-    const int grid = (int)std::min<int64_t>((int64_t)c->sm_count * c->fit_occ, items);
-    if (c->timing) CT_CUDA(cudaEventRecord(c->ev[2], s));
-    fa.stages = plan.stages;
-    cudaError_t e = ct::launch_fit_hist(fa, plan, grid, s);
-    if (e != cudaSuccess) return cuda_fail(e, "fit_hist launch");
-    if (c->timing) CT_CUDA(cudaEventRecord(c->ev[3], s));
-    c->fit_timed = c->timing;
-    ++launches;
-  }
-  ct::ScanArgs sa;
-  sa.hcnt = fa.hcnt;
-  sa.hsum = fa.hsum;
-  sa.stat = fa.stat;
+  std::memset(&sa, 0, sizeof sa);
   sa.F = F;
   sa.K = K;
   sa.J = J;
   sa.cost = *cp;
   sa.est = *est;
+  return CT_OK;
+}
+
+int fit_grid(ct_ctx* c, const ct::FitArgs& fa, const ct::FitPlan& plan, bool fused) {
+  const int key = plan.smem * 8 + (plan.pairs ? 4 : 0) + (fused ? 2 : 0) + (fa.b_us < (1ll << 26) ? 1 : 0);
+  if (c->fit_occ_key != key || c->fit_occ_step1 != (fa.step == 1)) {
+    c->fit_occ = ct::fit_hist_occupancy(fa, plan, fused);
+    c->fit_occ_key = key;
+    c->fit_occ_step1 = fa.step == 1;
+  }
+  return c->sm_count * c->fit_occ;
+}
+
+int ensure_fit_buffers(ct_ctx* c, int64_t words) {
+  for (int i = 0; i < 2; ++i) {
+    if (c->fitbuf_cap[i] >= (size_t)(8 * words) && c->fitbuf[i]) continue;
+    int rc = ensure(&c->fitbuf[i], &c->fitbuf_cap[i], 8 * (size_t)words);
+    if (rc) return rc;
+    c->fit_clean[i] = 0;
+  }
+  return CT_OK;
+}
+
+}  // namespace
+
+int ct_bernstein(ct_ctx* c, const ct_stat_row* rows, int64_t n, const ct_estimator_params* est,
+                 int64_t* out, void* stream) {
+  if (!c || !est || n < 0 || (n > 0 && (!rows || !out))) return fail(CT_EINVAL, "NULL argument");
+  if (!est_valid(*est)) return fail(CT_EINVAL, "invalid estimator parameters");
+  cudaError_t e = ct::launch_bernstein(rows, n, *est, out, c->sm_count, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "bernstein launch");
+  return CT_OK;
+}
+
+int ct_calc_ttl_batch(ct_ctx* c, const ct_stat_row* g, const ct_stat_row* f,
+                      const int64_t* n_done, const int64_t* turns_done, int64_t n,
+                      const ct_estimator_params* est, int64_t* out, void* stream) {
+  if (!c || !est || n < 0 || (n > 0 && (!g || !f || !n_done || !turns_done || !out)))
+    return fail(CT_EINVAL, "NULL argument");
+  if (!est_valid(*est)) return fail(CT_EINVAL, "invalid estimator parameters");
+  cudaError_t e = ct::launch_calc_ttl(g, f, n_done, turns_done, n, *est, out, c->sm_count,
+                                      (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "calc_ttl launch");
+  return CT_OK;
+}
+
+int64_t ct_bernstein_ref(const ct_stat_row* row, const ct_estimator_params* est) {
+  if (!row || !est || !est_valid(*est)) return CT_TTL_INVALID;
+  return ct::bernstein_row(*row, *est);
+}
+
+int64_t ct_calc_ttl_ref(const ct_stat_row* g, const ct_stat_row* f, const ct_estimator_params* est,
+                        int64_t n_done, int64_t turns_done) {
+  if (!g || !f || !est || !est_valid(*est)) return CT_TTL_INVALID;
+  return ct::calc_ttl_row(*g, *f, *est, n_done, turns_done);
+}
+
+int64_t ct_fit_acc_words(int32_t n_tools, int32_t K) {
+  if (n_tools < 1 || n_tools > CT_MAX_TOOLS || K < 1 || K > CT_MAX_K) return -1;
+  return ct::fit_acc_words(n_tools, K);
+}
+
+int ct_fit_ttl(ct_ctx* c, const ct_samples* sm, const ct_cost_params* cp,
+               const ct_estimator_params* est, ct_ttl_table* out, void* stream) {
+  ct::FitArgs fa;
+  ct::ScanArgs sa;
+  ct::FitPlan plan;
+  int rc = fit_prepare(c, sm, cp, est, 0, 1, fa, sa, plan);
+  if (rc) return rc;
+  if (!out || !out->ttl_argmax || !out->ttl_paper) return fail(CT_EINVAL, "NULL output table");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t W = ct::fit_acc_words(fa.F, fa.K);
+  if ((rc = ensure_fit_buffers(c, W))) return rc;
+  const int cur = c->fit_cur;
+  if (c->fit_clean[cur] < W) CT_CUDA(cudaMemsetAsync(c->fitbuf[cur], 0, 8 * (size_t)W, s));
+  c->fit_clean[cur] = 0;  // dirty from here on
+  fa.acc = (unsigned long long*)c->fitbuf[cur];
+  sa.acc = fa.acc;
   sa.ttl_argmax = out->ttl_argmax;
   sa.ttl_paper = out->ttl_paper;
   sa.stats_out = out->stats;
-  cudaError_t e = ct::launch_fit_scan(sa, s);
-  if (e != cudaSuccess) return cuda_fail(e, "fit_scan launch");
-  ++launches;
+  sa.n_invalid = out->n_invalid;
+  const bool fused = !plan.pairs;
+  if (fused) {  // the kernel zeroes the other half for the next call
+    fa.zero = (unsigned long long*)c->fitbuf[cur ^ 1];
+    fa.zero_words = W;
+  }
+  const int grid = fit_grid(c, fa, plan, fused);
+  if (grid < 1) return fail(CT_ECUDA, "fit kernel cannot be resident");
+  if (c->timing) CT_CUDA(cudaEventRecord(c->ev[2], s));
+  cudaError_t e = ct::launch_fit_hist(fa, sa, plan, grid, fused, s);
+  if (e != cudaSuccess) return cuda_fail(e, "fit launch");
+  int launches = 1;
+  if (!fused) {
+    e = ct::launch_fit_finish(sa, s);
+    if (e != cudaSuccess) return cuda_fail(e, "fit finish launch");
+    ++launches;
+  }
+  if (c->timing) CT_CUDA(cudaEventRecord(c->ev[3], s));
+  c->fit_timed = c->timing;
+  if (fused) c->fit_clean[cur ^ 1] = W;
+  c->fit_cur = cur ^ 1;
   c->last.launches = launches;
+  return CT_OK;
+}
+
+int ct_fit_ttl_partial(ct_ctx* c, const ct_samples* sm, const ct_cost_params* cp,
+                       const ct_estimator_params* est, int32_t rank, int32_t world, int64_t* acc,
+                       void* stream) {
+  ct::FitArgs fa;
+  ct::ScanArgs sa;
+  ct::FitPlan plan;
+  int rc = fit_prepare(c, sm, cp, est, rank, world, fa, sa, plan);
+  if (rc) return rc;
+  if (!acc) return fail(CT_EINVAL, "acc is NULL");
+  cudaStream_t s = (cudaStream_t)stream;
+  CT_CUDA(cudaMemsetAsync(acc, 0, 8 * (size_t)ct::fit_acc_words(fa.F, fa.K), s));
+  fa.acc = (unsigned long long*)acc;
+  const int grid = fit_grid(c, fa, plan, false);
+  if (grid < 1) return fail(CT_ECUDA, "fit kernel cannot be resident");
+  if (c->timing) CT_CUDA(cudaEventRecord(c->ev[2], s));
+  cudaError_t e = ct::launch_fit_hist(fa, sa, plan, grid, false, s);
+  if (e != cudaSuccess) return cuda_fail(e, "fit launch");
+  if (c->timing) CT_CUDA(cudaEventRecord(c->ev[3], s));
+  c->fit_timed = c->timing;
+  c->last.launches = 1;
+  return CT_OK;
+}
+
+int ct_fit_ttl_finish(ct_ctx* c, const int64_t* acc, int32_t n_tools, const ct_cost_params* cp,
+                      const ct_estimator_params* est, ct_ttl_table* out, void* stream) {
+  if (!c || !acc || !cp || !est || !out || !out->ttl_argmax || !out->ttl_paper)
+    return fail(CT_EINVAL, "NULL argument");
+  // the same parameter checks as the histogram pass (an empty CSR set of n_tools tools)
+  int64_t off[CT_MAX_TOOLS + 1] = {0};
+  if (n_tools < 1 || n_tools > CT_MAX_TOOLS) return fail(CT_EINVAL, "n_tools %d", n_tools);
+  ct_samples none{};
+  none.tool_off = off;
+  none.n_tools = n_tools;
+  ct::FitArgs fa;
+  ct::ScanArgs sa;
+  ct::FitPlan plan;
+  int rc = fit_prepare(c, &none, cp, est, 0, 1, fa, sa, plan);
+  if (rc) return rc;
+  sa.acc = (const unsigned long long*)acc;
+  sa.ttl_argmax = out->ttl_argmax;
+  sa.ttl_paper = out->ttl_paper;
+  sa.stats_out = out->stats;
+  sa.n_invalid = out->n_invalid;
+  cudaError_t e = ct::launch_fit_finish(sa, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "fit finish launch");
+  c->last.launches = 1;
   return CT_OK;
 }
 

@@ -66,7 +66,29 @@ __device__ __forceinline__ uint32_t ceil_div_magic(uint32_t x, const DivMagic& m
 }
 
 // floor(sqrt(x)) exactly: double estimate, then integer correction.
-__device__ __forceinline__ uint64_t isqrt_u64(uint64_t x) {
+// floor(sqrt(x)) for x < 2^128 exactly (the argument of the Bernstein square root can exceed
+// 2^64 for small n, wide samples and a small delta): double estimate, integer correction.
+__host__ __device__ __forceinline__ uint64_t isqrt_u128(u128_t x) {
+  if ((x >> 64) == 0) {
+    const uint64_t y = (uint64_t)x;
+    uint64_t r = (uint64_t)sqrt((double)y);
+    if (r > 0xffffffffull) r = 0xffffffffull;
+    while (r * r > y) --r;
+    while (r < 0xffffffffull && (r + 1) * (r + 1) <= y) ++r;
+    return r;
+  }
+  const double dx = (double)(uint64_t)(x >> 64) * 18446744073709551616.0 + (double)(uint64_t)x;
+  const double sq = sqrt(dx);  // relative error ~2^-54: within ~2^10 of the root (>= 2^32)
+  uint64_t r = sq >= 18446744073709551615.0 ? 0xffffffffffffffffull : (uint64_t)sq;
+  // one integer Newton step leaves an error below one, then exact correction
+  const u128_t nr = ((u128_t)r + x / r) >> 1;
+  r = nr > (u128_t)0xffffffffffffffffull ? 0xffffffffffffffffull : (uint64_t)nr;
+  while ((u128_t)r * r > x) --r;
+  while (r < 0xffffffffffffffffull && (u128_t)(r + 1) * (r + 1) <= x) ++r;
+  return r;
+}
+
+__host__ __device__ __forceinline__ uint64_t isqrt_u64(uint64_t x) {
   uint64_t r = (uint64_t)sqrt((double)x);
   if (r > 0xffffffffull) r = 0xffffffffull;
   while (r * r > x) --r;
@@ -82,7 +104,7 @@ __device__ __forceinline__ uint64_t isqrt_u64(uint64_t x) {
 // scaling, so several quotients by one divisor share one double division.  rden then adds at
 // most two roundings and the product one, for six in all: the relative error stays below
 // 2^-50.4, and the estimate is still within one of any quotient below 2^50.
-__device__ __forceinline__ u128_t div_u128_r(u128_t num, uint64_t den, double rden) {
+__host__ __device__ __forceinline__ u128_t div_u128_r(u128_t num, uint64_t den, double rden) {
   const double dn = (double)(uint64_t)(num >> 64) * 18446744073709551616.0 + (double)(uint64_t)num;
   const double est = dn * rden;
   if (est < 1125899906842624.0) {  // 2^50
@@ -95,7 +117,7 @@ __device__ __forceinline__ u128_t div_u128_r(u128_t num, uint64_t den, double rd
   return num / den;
 }
 
-__device__ __forceinline__ u128_t div_u128_u64(u128_t num, uint64_t den) {
+__host__ __device__ __forceinline__ u128_t div_u128_u64(u128_t num, uint64_t den) {
   const double dn = (double)(uint64_t)(num >> 64) * 18446744073709551616.0 + (double)(uint64_t)num;
   const double est = dn / (double)den;
   if (est < 1125899906842624.0) {  // 2^50
@@ -117,7 +139,7 @@ struct Stat {  // one estimator row: n, sum t~, sum t~^2 (128-bit as lo/hi)
 // floor(s1/n) + isqrt(floor(2 v L_q / (n 2^32))) + floor(3 b L_q / (n 2^32)),
 // v = floor((n s2 - s1^2) / (n (n-1))) for n >= 2, else 0.
 // The three quotients by n and by n 2^32 share one reciprocal of n.
-__device__ __forceinline__ int64_t bernstein(const Stat& s, uint64_t lq, int64_t b_us) {
+__host__ __device__ __forceinline__ int64_t bernstein(const Stat& s, uint64_t lq, int64_t b_us) {
   const int64_t n = s.n;
   const double rn = 1.0 / (double)n;           // n < 2^31 (validated): exact conversion
   const double rnsh = rn * 2.3283064365386963e-10;  // 2^-32: exact scaling
@@ -131,13 +153,13 @@ __device__ __forceinline__ int64_t bernstein(const Stat& s, uint64_t lq, int64_t
   }
   uint64_t nsh = (uint64_t)n << 32;
   u128_t a2 = div_u128_r((u128_t)2 * v * lq, nsh, rnsh);
-  uint64_t t2 = isqrt_u64((uint64_t)a2);
+  uint64_t t2 = isqrt_u128(a2);
   u128_t t3 = div_u128_r((u128_t)3 * (uint64_t)b_us * lq, nsh, rnsh);
   return mu + (int64_t)t2 + (int64_t)t3;
 }
 
-// 𝓑(r,f) then CalcTTL offset, readings R7/R8.
-__device__ __forceinline__ int64_t calc_ttl(const Stat& g, const Stat& f,
+// 𝓑(r,f) then CalcTTL offset, readings R7/R8/R36.
+__host__ __device__ __forceinline__ int64_t calc_ttl(const Stat& g, const Stat& f,
                                             const ct_estimator_params& e, int64_t n_done,
                                             int64_t turns_done) {
   int64_t B;
@@ -156,11 +178,12 @@ __device__ __forceinline__ int64_t calc_ttl(const Stat& g, const Stat& f,
     ttl = div_u128_u64(T2, (uint64_t)B);
   }
   if (e.ttl_max_us > 0 && ttl > (u128_t)(uint64_t)e.ttl_max_us) ttl = (uint64_t)e.ttl_max_us;
+  if (ttl >= (u128_t)CT_TTL_SAT) ttl = CT_TTL_SAT - 1;  // reading R36
   return (int64_t)(uint64_t)ttl;
 }
 
 // §4.5 simplified decision, reading R9.
-__device__ __forceinline__ int64_t simplified_ttl(const Stat& g, const Stat& f,
+__host__ __device__ __forceinline__ int64_t simplified_ttl(const Stat& g, const Stat& f,
                                                   const ct_estimator_params& e, int64_t t_pin,
                                                   int64_t t_thresh) {
   if (t_thresh == CT_ALWAYS) return t_pin;
@@ -173,7 +196,7 @@ __device__ __forceinline__ int64_t simplified_ttl(const Stat& g, const Stat& f,
 
 // InferCept: predicted tool time = mean of the tool when |S_f| >= N,
 // else the global mean when |S| >= 1, else T_default.
-__device__ __forceinline__ int64_t infercept_predict(const Stat& g, const Stat& f,
+__host__ __device__ __forceinline__ int64_t infercept_predict(const Stat& g, const Stat& f,
                                                      const ct_estimator_params& e) {
   if (f.n >= e.n_min) return f.s1 / f.n;
   if (g.n >= 1) return g.s1 / g.n;

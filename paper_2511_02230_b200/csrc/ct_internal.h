@@ -30,7 +30,29 @@ struct ReplayArgs {
   int from_list;      // replay the replicas fb_list[0 .. *fb_count) instead of [r_begin, r_end)
   int64_t* fb_list;   // MODE 4: replicas handed to the 64-bit kernel (horizon, bubble output)
   unsigned long long* fb_count;
+  const unsigned long long* err;  // trace check result (validate.cu): err[0] != 0 = invalid input
 };
+
+// Trace-set check (validate.cu).  Bits of err[0]:
+#define CT_CHECK_NTURNS 1u      /* nturns outside [1, CT_MAX_TURNS] */
+#define CT_CHECK_TURN_RANGE 2u  /* turn0 / turn0 + nturns outside the turn array */
+#define CT_CHECK_ARRIVAL 4u     /* arr_q < 0, arr_q gap_max >= 2^62, or arrivals not sorted */
+#define CT_CHECK_TOKENS 8u      /* decode < 1 or new < 0 */
+#define CT_CHECK_TOOL 16u       /* a non-final turn's tool outside [0, F) or dur < 1 */
+#define CT_CHECK_CONTEXT 32u    /* a program's total new + decode tokens > CT_MAX_CONTEXT */
+#define CT_CHECK_FITTED 64u     /* a FITTED table entry outside [0, CT_TTL_SAT) */
+struct CheckArgs {
+  const ct_program* progs;
+  const int4* turns;
+  int64_t n_turns;
+  int64_t p_begin, p_end;  // programs of the seeds the replica range touches
+  int P, F;
+  int64_t arr_max;         // largest arr_q with arr_q * max(gap) < 2^62
+  const int64_t* fitted;
+  int64_t n_fitted;
+  unsigned long long* err;  // [2], zeroed by the caller
+};
+cudaError_t launch_check_traces(const CheckArgs& a, int sm_count, cudaStream_t s);
 
 // The TTL-grid policy class, for which the P <= 32 replay has a specialised path: program
 // FCFS; EVICT, or FIXED with T_thresh = CT_ALWAYS (pin for t_pin); no DRAM tier; eager expiry
@@ -68,44 +90,48 @@ int replay_occupancy(int ns, bool growth, int mode, int warps_per_block, int sme
 
 struct FitArgs {
   const int32_t* dur;
-  int64_t n_chunks;              // work items: chunks of <= ch samples inside one tool segment
-  int64_t ch;
-  int64_t tool_off[CT_MAX_TOOLS + 1];
-  int64_t chunk_off[CT_MAX_TOOLS + 1];  // first chunk index of each tool
+  const uint8_t* tool_u8;          // unsorted pairs layout: tool id per sample (else NULL)
+  int64_t n;                       // pairs layout: sample count
+  int64_t seg_lo[CT_MAX_TOOLS];    // CSR: physical sample range [seg_lo, seg_hi) of tool f
+  int64_t seg_hi[CT_MAX_TOOLS];
+  int64_t voff[CT_MAX_TOOLS + 1];  // CSR: prefix of the segment lengths (virtual order)
+  int64_t ch;                      // max samples per histogram piece (32-bit bin bound)
   int F, K;
-  int64_t step;          // grid step (µs)
-  uint64_t step_magic;   // ceil(2^64 / step) for the bucket quotient (per-warp kernels)
-  uint32_t div_m, div_sh, div_add;  // floor(x / step) for 32-bit x (CTA kernels, step >= 2)
+  int64_t step;                    // grid step (µs)
+  uint32_t div_m, div_sh, div_add; // floor(x / step) for 32-bit x (step >= 2)
   int64_t b_us;
-  int stages;  // TMA ring depth (TMA-staged variant)
-  unsigned long long* hcnt;  // [(F+1) * (K+1)] bucket counts, row F pooled over tools
-  unsigned long long* hsum;  // [(F+1) * (K+1)] bucket sums (buckets < K)
-  unsigned long long* stat;  // [(F+1) * 6]: n, s1, s2 limbs (32-bit limb sums in u64 slots)
+  unsigned long long* acc;         // accumulator, fit_acc_words(F, K) words
+  unsigned long long* zero;        // FUSED: zero this buffer (the next call's accumulator)
+  int64_t zero_words;
 };
 
 struct ScanArgs {
-  const unsigned long long* hcnt;
-  const unsigned long long* hsum;
-  const unsigned long long* stat;
+  const unsigned long long* acc;
   int F, K, J;
   ct_cost_params cost;
   ct_estimator_params est;
   int64_t* ttl_argmax;
   int64_t* ttl_paper;
   int64_t* stats_out;
+  int64_t* n_invalid;
 };
 
-// Kernel variant, launch shape and shared memory of the histogram pass for grid size K and
-// clamp b (ttl_fit.cu: CT_FIT_VARIANT overrides the default for experiments).
+// Accumulator words: (F+1)(K+1) bucket counts | (F+1)(K+1) bucket sums | (F+1) x 6 statistic
+// limbs {n, sum t~, l0..l3 of sum t~^2} | 1 count of samples outside [0, 2^31).
+int64_t fit_acc_words(int F, int K);
+
+// Shape of the histogram pass: lane replicas of the CTA histogram (32, or 16 when (K+1) x 256 B
+// exceeds shared memory), dynamic shared memory; pairs = unsorted (dur, u8 tool) layout.
 struct FitPlan {
-  int v, threads, smem, repl, stages;
-  bool cta;     // CTA-shared lane-indexed histogram (work items are CTA-level)
-  bool ranges;  // one contiguous sample range per CTA, pieces of <= ch samples
+  bool pairs, ok;
+  int lr, smem;
 };
-FitPlan fit_plan(int K, int64_t b_us);
-int fit_hist_occupancy(const FitPlan& p);  // resident CTAs per SM
-cudaError_t launch_fit_hist(const FitArgs& a, const FitPlan& p, int grid, cudaStream_t s);
-cudaError_t launch_fit_scan(const ScanArgs& a, cudaStream_t s);
+FitPlan fit_plan(int K, int F, bool pairs);
+int fit_hist_occupancy(const FitArgs& a, const FitPlan& p, bool fused);  // CTAs per SM
+// fused: cooperative launch, histogram + grid barrier + finish (ct_fit_ttl, CSR layout)
+cudaError_t launch_fit_hist(const FitArgs& a, const ScanArgs& s, const FitPlan& p, int grid,
+                            bool fused, cudaStream_t st);
+cudaError_t launch_fit_finish(const ScanArgs& s, cudaStream_t st);
 
 // On-device trace synthesis (synth.cu).  Device scratch is owned by the context.
 struct SynthLaunch {
@@ -126,6 +152,16 @@ struct SynthLaunch {
 // Runs the three passes; synchronises `st` after the count pass and skips the write pass when
 // the total (returned in *total_host) exceeds turns_cap.
 cudaError_t launch_synth(const SynthLaunch& L, int sm_count, cudaStream_t st, int64_t* total_host);
+
+// Estimator calls (estimator.cu): device batches and the host references (same helpers).
+cudaError_t launch_bernstein(const ct_stat_row* rows, int64_t n, const ct_estimator_params& e,
+                             int64_t* out, int sm_count, cudaStream_t s);
+cudaError_t launch_calc_ttl(const ct_stat_row* g, const ct_stat_row* f, const int64_t* n_done,
+                            const int64_t* turns_done, int64_t n, const ct_estimator_params& e,
+                            int64_t* out, int sm_count, cudaStream_t s);
+int64_t bernstein_row(const ct_stat_row& r, const ct_estimator_params& e);
+int64_t calc_ttl_row(const ct_stat_row& g, const ct_stat_row& f, const ct_estimator_params& e,
+                     int64_t n_done, int64_t turns_done);
 
 // Sets the thread-local message ct_last_error() returns (api.cu); host code in other files.
 void set_last_error(const char* msg);

@@ -190,13 +190,7 @@ __device__ __forceinline__ void replay_one_w32(const ReplayArgs& a, int64_t r, S
     if (lane == v) { gblk = 0; dblk = keep; pin = false; texp = CT_INF64; }
   };
 
-#ifdef CT_DEBUG_LOOPS
-  int64_t dbg_loops = 0, dbg_sched = 0, dbg_macro = 0, dbg_mid = 0;
-#endif
   for (;;) {
-#ifdef CT_DEBUG_LOOPS
-    ++dbg_loops;
-#endif
     // ---- next event (R1, R3) --------------------------------------------------------------
     // With an iteration in flight nothing can be scheduled before its end (R2), so every
     // program event up to iter_end is applied in one pass at the boundary, each program's own
@@ -337,15 +331,9 @@ __device__ __forceinline__ void replay_one_w32(const ReplayArgs& a, int64_t r, S
         }
       }
     }
-#ifdef CT_DEBUG_LOOPS
-    if (in_flight) ++dbg_mid;
-#endif
     if (in_flight) continue;  // mid-iteration: events only mutate Q / stats / pins (R2)
 
     // ---- scheduling point (R3) --------------------------------------------------------------
-#ifdef CT_DEBUG_LOOPS
-    ++dbg_sched;
-#endif
     // (a) STEP reading: release expired pins of programs not waiting
     if (!eager) {
       uint32_t m = __ballot_sync(FULL_MASK, pin && st == S_TOOL && texp <= now);
@@ -480,9 +468,6 @@ __device__ __forceinline__ void replay_one_w32(const ReplayArgs& a, int64_t r, S
         const int64_t te = warp_min64_redux(min(tev, texp));
         k = FAST ? macro_iters32(mfin - n_it, te - now, dur1, (uint32_t)d, rd_cur)
                  : macro_iters(mfin - n_it, te - now, dur1, d, rd_cur);
-#ifdef CT_DEBUG_LOOPS
-        ++dbg_macro;
-#endif
       }
       const int64_t dur = dur1 + (k - 1) * d;
       if (n_it + k > E.max_iters) { status = CT_R_EVENT_BUDGET; break; }
@@ -549,12 +534,6 @@ __device__ __forceinline__ void replay_one_w32(const ReplayArgs& a, int64_t r, S
       o.pin_expiries = av[ACC_EXP];
       o.victims = av[ACC_VICT];
       o.reloads = av[ACC_RELOAD];
-#ifdef CT_DEBUG_LOOPS
-      o.reloads = dbg_loops;
-      o.victims = dbg_sched;
-      o.pin_hits = dbg_macro;
-      o.recompute_tokens = dbg_mid;
-#endif
     } else {
       int64_t* w = (int64_t*)&o;
 #pragma unroll
@@ -2198,11 +2177,23 @@ __device__ __forceinline__ bool replay_one_ns32(const ReplayArgs& a, int64_t r,
 // class; 4 every policy in the program-FCFS class with 32-bit times (replay_one_ns32), replicas
 // that reach the horizon are queued for a second launch of MODE 1 over that list (from_list);
 // 5 the same for the simple class with request FCFS (fallback launch: the generic kernel).
+// A trace set that failed the on-device check (validate.cu): no record is read; the replica
+// reports CT_R_INVALID_INPUT with a zero summary and -1 per-program outputs.
+__device__ __noinline__ void write_invalid(const ReplayArgs& a, int64_t r, int lane) {
+  const int64_t ri = r - a.r_begin;
+  if (lane < 16) ((int64_t*)&a.out[ri])[lane] = lane == 0 ? CT_R_INVALID_INPUT : 0;
+  for (int p = lane; p < a.P; p += 32) {
+    if (a.jct) a.jct[ri * a.P + p] = -1;
+    if (a.bubble) a.bubble[ri * a.P + p] = -1;
+  }
+}
+
 template <int NS, int MINB, bool VLLM = false, int MODE = 0>
 __global__ void __launch_bounds__(128, MINB) replay_kernel(ReplayArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x & 31;
   unsigned char* wm = smem + (threadIdx.x >> 5) * a.smem_per_warp;
+  const bool invalid = a.err[0] != 0;
   for (;;) {
     unsigned long long idx = 0;
     if (lane == 0) idx = atomicAdd(a.counter, 1ull);
@@ -2214,6 +2205,10 @@ __global__ void __launch_bounds__(128, MINB) replay_kernel(ReplayArgs a) {
     } else {
       r = a.r_begin + (int64_t)idx;
       if (r >= a.r_end) break;
+    }
+    if (invalid) {
+      write_invalid(a, r, lane);
+      continue;
     }
     if (NS == 1 && !VLLM) {
       if (MODE == 1) {
@@ -2232,16 +2227,14 @@ __global__ void __launch_bounds__(128, MINB) replay_kernel(ReplayArgs a) {
   }
 }
 
-// P <= 32 variants differ only in the register budget (min resident CTAs of 4 warps per SM);
-// CT_REPLAY_MINB selects one for experiments, the default is the measured best.
-static int g_minb = -1;
-static int minb() {
-  if (g_minb < 0) {
-    const char* e = getenv("CT_REPLAY_MINB");
-    g_minb = e ? atoi(e) : 8;
-  }
-  return g_minb;
-}
+// P <= 32 generic kernel: register budget (min resident CTAs of 4 warps per SM); the TTL-grid
+// class kernel (MODE 1) runs at 10 (48 registers, 40 warps/SM, measured best on cfg3).
+#ifndef CT_REPLAY_MINB
+#define CT_REPLAY_MINB 8
+#endif
+#ifndef CT_REPLAY_MINB_GRID
+#define CT_REPLAY_MINB_GRID 10
+#endif
 
 #ifndef NS32_MINB
 #define NS32_MINB 7  // 7 CTAs of 4 warps per SM: 28 warps, <= 73 registers, 28 B SMEM per program
@@ -2265,22 +2258,10 @@ static void* pick(int ns, bool growth, int mode) {
   }
   switch (ns) {
     case 1:
-      if (mode == 1) {  // TTL-grid class: 48 registers, 40 warps/SM measured best (cfg3)
-        switch (getenv("CT_REPLAY_MINB") ? minb() : 10) {
-          case 8: return (void*)replay_kernel<1, 8, false, 1>;
-          case 12: return (void*)replay_kernel<1, 12, false, 1>;
-          case 16: return (void*)replay_kernel<1, 16, false, 1>;
-          default: return (void*)replay_kernel<1, 10, false, 1>;
-        }
-      }
+      if (mode == 1) return (void*)replay_kernel<1, CT_REPLAY_MINB_GRID, false, 1>;
       if (mode == 2) return (void*)replay_kernel<1, 8, false, 2>;
       if (mode == 3) return (void*)replay_kernel<1, 8, false, 3>;
-      switch (minb()) {
-        case 6: return (void*)replay_kernel<1, 6>;
-        case 10: return (void*)replay_kernel<1, 10>;
-        case 12: return (void*)replay_kernel<1, 12>;
-        default: return (void*)replay_kernel<1, 8>;
-      }
+      return (void*)replay_kernel<1, CT_REPLAY_MINB>;
     case 2: return mode == 4 ? (void*)replay_kernel<2, NS32_MINB, false, 4>
                  : mode == 5 ? (void*)replay_kernel<2, NS32_MINB, false, 5>
                  : mode == 1 ? (void*)replay_kernel<2, NS_PROG_MINB, false, 1> : (void*)replay_kernel<2, 1>;

@@ -32,6 +32,8 @@ def gather_summaries(summ_shard: torch.Tensor, R: int, world: int, out: torch.Te
         out = torch.empty((cap * world, summ_shard.shape[1]), dtype=summ_shard.dtype,
                           device=summ_shard.device)
     dist.all_gather_into_tensor(out, summ_shard, group=group)
+    if R % world == 0:  # equal shards: the gathered buffer is already in sweep order
+        return out[:R]
     parts = []
     for k in range(world):
         a, b = shard_range(R, k, world)

@@ -8,6 +8,7 @@ import os
 import socket
 
 import numpy as np
+import pytest
 import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
@@ -23,15 +24,15 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, q):
+def _worker(rank, world, port, q, n_rates):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     from ctgen import configs as cf
     from ctgen import traces
     from oracle import oracle as O
     tr = traces.generate(3, 8, n_bfcl=4, mix="mix", ctx_cap=8192 * 16, stream=11)
-    sw = cf.Sweep(3, cf.rate_axis(3), [8192], [cf.ttl_grid(t) for t in cf.ttl_axis(3)])
-    R = sw.n_replicas  # 27: ragged over 2 ranks
+    sw = cf.Sweep(3, cf.rate_axis(n_rates), [8192], [cf.ttl_grid(t) for t in cf.ttl_axis(3)])
+    R = sw.n_replicas  # 27: ragged over 2 ranks (reassembled); 36: equal shards (no copy)
     a, b = D.shard_range(R, rank, world)
     cap = D.shard_capacity(R, world)
     s, _ = O.simulate(tr, sw, cf.ENGINE_8B, a, b, want_jct=False)
@@ -45,11 +46,12 @@ def _worker(rank, world, port, q):
     dist.destroy_process_group()
 
 
-def test_gloo_world2_gather_equals_single_process():
+@pytest.mark.parametrize("n_rates", [3, 4])
+def test_gloo_world2_gather_equals_single_process(n_rates):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    ps = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    ps = [ctx.Process(target=_worker, args=(r, 2, port, q, n_rates)) for r in range(2)]
     for p in ps:
         p.start()
     ok = q.get(timeout=300)

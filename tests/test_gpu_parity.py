@@ -226,8 +226,8 @@ def test_jct_stats_parity(ctx):
 
 @pytest.mark.parametrize("K", [300, 512, 1024])
 def test_fit_large_grids(ctx, K):
-    """Grids whose CTA-shared histogram needs fewer TMA stages (K 300, 512) or does not fit in
-    shared memory at all (K 1024: per-warp 4-replica fallback)."""
+    """Grids of up to 899 points keep the 32-replica CTA histogram; K 1024 runs the 16-replica
+    layout (tests/test_gpu_fit.py covers the boundary)."""
     rng = np.random.default_rng(K)
     sizes = [5, 100_003, 7, 250_000, 1]
     off = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)

@@ -45,6 +45,8 @@ def test_isqrt_matches_library():
     rng = random.Random(1)
     vals = [0, 1, 2, 3, 4, 15, 16, 17, 2**62, 2**64 - 1, (2**32 - 1) ** 2, (2**32 - 1) ** 2 - 1]
     vals += [rng.randrange(2**64) for _ in range(3000)] + [rng.randrange(10**6) for _ in range(1000)]
+    vals += [2**64, 2**64 + 1, 2**128 - 1, (2**64 - 1) ** 2, (2**64 - 1) ** 2 - 1]
+    vals += [rng.randrange(2**128) for _ in range(2000)] + [rng.randrange(2**70) for _ in range(1000)]
     for v in vals:
         assert O.isqrt(v) == math.isqrt(v)
 
@@ -89,6 +91,28 @@ def test_bernstein_vs_double_formula(seed):
                         cf.lq_from_delta(delta), b)
         assert abs(B - float_bound(xs, delta, b)) <= 3.0, (xs, delta, b)
         assert B >= sum(xs) // n  # B >= mean
+
+
+def test_bernstein_vs_double_wide_samples():
+    """The square-root argument 2 v L_q / (n 2^32) exceeds 2^64 for a few samples spread over
+    [0, 2^31) with a small delta: the whole 128-bit value must enter the root.
+    Relative tolerance: the double formula itself rounds at ~2^-52 of B."""
+    rng = random.Random(77)
+    big = 0
+    for _ in range(400):
+        n = rng.choice([2, 3, 4, 7])
+        b = 2**31 - 1
+        delta = rng.choice([1e-9, 1e-7, 1e-4])
+        xs = [rng.choice([0, b, rng.randint(0, b)]) for _ in range(n)]
+        r = row(xs)
+        lq = cf.lq_from_delta(delta)
+        s2 = int(np.uint64(r[2])) + (int(np.uint64(r[3])) << 64)
+        B = O.bernstein(n, int(r[1]), s2, lq, b)
+        want = float_bound(xs, delta, b)
+        assert abs(B - want) <= 3.0 + want * 1e-13, (xs, delta, B, want)
+        var = (n * s2 - int(r[1]) ** 2) // (n * (n - 1))
+        big += (2 * var * lq) // (n << 32) >= 2**64
+    assert big > 30  # the > 2^64 region is exercised
 
 
 def test_bernstein_nonincreasing_in_n():

@@ -14,6 +14,10 @@ import torch
 
 import paper_2511_02230_b200 as ct
 from ctgen import configs as cf
+
+if os.environ.get("AB_LIB"):  # tools/ab.sh: an experimental build of the library (A/B runs)
+    from paper_2511_02230_b200 import _lib
+    _lib.LIB_PATH = os.environ["AB_LIB"]
 from ctgen import traces
 
 
@@ -26,13 +30,46 @@ def main():
         dur, off = traces.synthetic_samples_torch(log2n, 32, 1234, "cuda")
         cp = ct.cost_params(13_400_000, 200, 16, 1, 10, 50_000, 256,
                             [min(16 * 2**j, 120_000) for j in range(64)], list(range(1, 65)))
-        for i in range(3):
+        est = cf.Estimator()
+        n = 1 << log2n
+        acc = torch.zeros(ct.ct_fit_acc_words(32, 256), dtype=torch.int64, device="cuda")
+
+        def fused():
+            ct.ct_fit_ttl(ctx, dur, off, cp, est, want_stats=False)
+
+        def split():
+            ct.ct_fit_ttl_partial(ctx, dur, off, cp, est, 0, 1, acc=acc)
+            ct.ct_fit_ttl_finish(ctx, acc, 32, cp, est, want_stats=False)
+
+        for name, fn in (("fused", fused), ("partial+finish", split)):
+            for _ in range(3):
+                fn()
+            torch.cuda.synchronize()
+            reps = 20
             e0.record()
-            ct.ct_fit_ttl(ctx, dur, off, cp, cf.Estimator())
+            for _ in range(reps):
+                fn()
             e1.record()
             torch.cuda.synchronize()
-            t = e0.elapsed_time(e1) / 1e3
-            print("fit n=2^%d: %.3f ms, %.1f GB/s" % (log2n, t * 1e3, 4 * (1 << log2n) / t / 1e9))
+            t = e0.elapsed_time(e1) / 1e3 / reps
+            ctx.set_timing(True)
+            ks = []
+            for _ in range(reps):
+                fn()
+                ks.append(ctx.last_launch()["fit_hist_ms"])
+            ctx.set_timing(False)
+            k = sorted(ks)[reps // 2] / 1e3
+            print("fit %s n=2^%d: call %.1f us (%.0f GB/s), kernel median %.1f us (%.0f GB/s)" % (
+                name, log2n, t * 1e6, 4 * n / t / 1e9, k * 1e6, 4 * n / k / 1e9))
+        for _ in range(2):
+            dur.max()
+        e0.record()
+        for _ in range(20):
+            dur.max()
+        e1.record()
+        torch.cuda.synchronize()
+        t = e0.elapsed_time(e1) / 1e3 / 20
+        print("read probe (torch max): %.1f us, %.0f GB/s" % (t * 1e6, 4 * n / t / 1e9))
     else:
         name = sys.argv[2] if len(sys.argv) > 2 else "cfg3"
         seeds = int(sys.argv[3]) if len(sys.argv) > 3 else 16
