@@ -245,9 +245,11 @@ int ct_ctx_destroy(ct_ctx* ctx);
  *  - argmax mode (extension C-4): n U(k) = V_j cnt_le(k) - C_j (sum_le(k) + tau_k (n - cnt_le(k))),
  *    V_j = floor(c_pf ctx_j (a_den + a_num w_j) / a_den), C_j = c_pin ceil(ctx_j / bs); tau* is the
  *    smallest maximiser over k >= 1 with U > 0, else 0.  Tools with n_f < N take the pooled row.
- * CSR layout: ONE kernel launch (histogram pass, grid barrier, scan/argmax/CalcTTL; the context's
- * double-buffered accumulator is zeroed in-kernel for the next call).  Unsorted layout: the pairs
- * kernel then the finish kernel.  Calls on one context must be ordered on one stream.
+ * Launches: the histogram pass, then the finish kernel (scan / argmax / CalcTTL) as its
+ * programmatic dependent launch (no launch gap); no memset: the histogram pass zeroes the other
+ * half of the context's double-buffered accumulator for the next call.  Unsorted layout: the
+ * pairs kernel (after a memset) then the finish kernel.  Calls on one context must be ordered
+ * on one stream.
  * Preconditions (else CT_EINVAL): dur_us 16-B aligned; n < 2^32; grid_step_us, b < 2^31;
  * (K-1) step < 2^43; every product bounded so that the 128-bit arithmetic cannot overflow
  * (checked against n and the cost maxima).  Sample VALUES are checked on the device (n_invalid).
@@ -457,7 +459,8 @@ typedef struct {
                                1 TTL-grid class (P <= 32, 32-bit times) or program-FCFS class
                                (P > 32, 64-bit), 2 mixed, 3 simple class (P <= 32, 32-bit),
                                4 program-FCFS class (P > 32, 32-bit) + list-driven 64-bit launch,
-                               5 as 4 with request FCFS (simple class) */
+                               5 as 4 with request FCFS (simple class), 6 extended class
+                               (P <= 32, 32-bit: + DRAM tier, PLAS, InferCept) */
   int32_t reserved;
 } ct_launch_info;
 int ct_last_launch(ct_ctx* ctx, ct_launch_info* info);

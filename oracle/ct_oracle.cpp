@@ -18,7 +18,9 @@
 #include "ct_oracle.h"
 
 #include <algorithm>
+#include <cstdio>
 #include <cstring>
+#include <string>
 #include <thread>
 #include <vector>
 
@@ -245,6 +247,14 @@ struct Sim {
   int next_arr = 0;
   int status = ST_OK;
   int64_t pins_created = 0;
+  std::string* audit = nullptr;  // per-decision log, JSON lines, or NULL
+
+  void log(const char* ev, int i, const char* extra = "") {
+    if (!audit) return;
+    char b[256];
+    snprintf(b, sizeof b, "{\"t\":%lld,\"ev\":\"%s\",\"p\":%d%s}\n", (long long)now, ev, i, extra);
+    *audit += b;
+  }
   // counters
   int64_t iterations = 0, busy = 0, bubble = 0, prefill = 0, recompute = 0;
   int64_t hits = 0, expiries = 0, victims = 0, reloads = 0;
@@ -333,14 +343,22 @@ struct Sim {
       free_blk += p[i].gblk; p[i].gblk = 0;
       dram_free += p[i].dblk; p[i].dblk = 0;
       p[i].completion = now; set_state(i, DONE);
+      log("done", i);
       D += 1; turns_done += prog_nturns(i);
       return;
     }
     int64_t ttl = ttl_for(i);
     if (ttl > 0) {  // pin_request(request, TTL) only if TTL != 0
       p[i].pinned = true; p[i].expiry = ttl == INF ? INF : now + ttl; pins_created++;
+      if (audit) {
+        char x[64];
+        if (ttl == INF) snprintf(x, sizeof x, ",\"ttl\":null");
+        else snprintf(x, sizeof x, ",\"ttl\":%lld", (long long)ttl);
+        log("pin", i, x);
+      }
     } else {
       evict(i);
+      log("evict", i);
     }
     p[i].t_ret = now + tr[3];
     p[i].tool_us += tr[3];
@@ -412,6 +430,7 @@ struct Sim {
     for (int i = 0; i < P; ++i)
       if (p[i].pinned && p[i].st != QUEUED && now > p[i].expiry) {
         evict(i); p[i].pinned = false; expiries++;
+        log("unpin", i, ",\"why\":\"expiry\"");
       }
     // (a2) KV growth of the running requests (NEXT-2, R27/R28)
     if (growth()) grow_running();
@@ -441,6 +460,11 @@ struct Sim {
           for (int i = P - 1; i >= 0; --i) if (p[i].pinned && i != h) { v = i; break; }
           if (v < 0) break;
           evict(v); p[v].pinned = false; victims++;
+          if (audit) {
+            char x[48];
+            snprintf(x, sizeof x, ",\"why\":\"victim\",\"for\":%d", h);
+            log("unpin", v, x);
+          }
         }
       }
       if (need > free_blk) break;  // HOL break
@@ -452,6 +476,7 @@ struct Sim {
       bool loading = false;
       if (p[h].pinned) {
         cached = p[h].ctx; p[h].pinned = false; hits++;
+        log("unpin", h, ",\"why\":\"hit\"");
       } else if (dram_on() && p[h].dblk > 0 && p[h].dblk == ceil_div(p[h].ctx, bs)) {
         cached = p[h].ctx; loading = true;
         int64_t start = now > chan_free ? now : chan_free;
@@ -467,6 +492,12 @@ struct Sim {
       p[h].preempted = false;
       int64_t uncached = p[h].ctx + tr[0] + p[h].emitted - cached;
       prefill += uncached;
+      if (audit) {
+        char x[96];
+        snprintf(x, sizeof x, ",\"cached\":%lld,\"uncached\":%lld,\"load\":%d",
+                 (long long)cached, (long long)uncached, loading ? 1 : 0);
+        log("admit", h, x);
+      }
       unc[h] = uncached;
       if (loading) {
         set_state(h, LOADING);
@@ -566,6 +597,7 @@ struct Sim {
         for (int i = 0; i < P; ++i)
           if (p[i].st == TOOL && p[i].pinned && p[i].expiry != INF && p[i].expiry + 1 == now) {
             evict(i); p[i].pinned = false; expiries++;
+            log("unpin", i, ",\"why\":\"expiry\"");
           }
       // ToolReturn = OnRequestArrive of a seen program
       for (int i = 0; i < P; ++i)
@@ -696,6 +728,31 @@ int or_simulate(const void* progs, const int32_t* turns, int64_t n_turns, int S,
     for (auto& x : th) x.join();
   }
   return 0;
+}
+
+int or_simulate_audit(const void* progs, const int32_t* turns, int64_t n_turns, int S, int P, int F,
+                      const int64_t* gap_us, int n_rate, const int64_t* kv_blocks, int n_kv,
+                      const int64_t* policies, int n_pol, const int64_t* est, const int64_t* eng,
+                      const int64_t* fitted, int J, int64_t replica, char* buf, int64_t cap,
+                      int64_t* len, int64_t* summary) {
+  (void)n_turns;
+  if (P < 1 || S < 1 || replica < 0 || replica >= (int64_t)S * n_rate * n_kv * n_pol) return -1;
+  const int64_t r = replica;
+  const int64_t pol_i = r % n_pol, kv_i = (r / n_pol) % n_kv, rate_i = (r / ((int64_t)n_pol * n_kv)) % n_rate;
+  Sim sim;
+  sim.progs = (const uint8_t*)progs;
+  sim.turns = turns;
+  sim.P = P; sim.F = F; sim.J = J;
+  sim.gap = gap_us[rate_i]; sim.kv = kv_blocks[kv_i];
+  sim.pol = policies + 8 * pol_i;
+  sim.est = est; sim.eng = eng; sim.fitted = fitted;
+  sim.seed = (int)(r / ((int64_t)n_pol * n_kv * n_rate));
+  std::string log;
+  sim.audit = &log;
+  sim.run(summary, nullptr, nullptr);
+  *len = (int64_t)log.size();
+  if (buf && cap > 0) std::memcpy(buf, log.data(), (size_t)std::min<int64_t>(cap, *len));
+  return *len <= cap ? 0 : 1;  // 1: buffer too small (len holds the size needed)
 }
 
 int or_jct_stats(const int64_t* summary, int64_t n_replicas, int n_cells, int64_t* out) {

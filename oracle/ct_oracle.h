@@ -64,6 +64,15 @@ int or_simulate(const void* progs, const int32_t* turns, int64_t n_turns,
                 int64_t r_begin, int64_t r_end, int n_threads,
                 int64_t* summary, int64_t* jct, int64_t* bubble);
 
+/* One replica with the per-decision audit log of SPEC.md:433 (pin / unpin with the reason
+ * hit | expiry | victim / evict / admit / done, each with its µs timestamp) as JSON lines in buf.
+ * Returns 0, 1 if cap < *len (the log is truncated; *len is its full size), <0 on bad input. */
+int or_simulate_audit(const void* progs, const int32_t* turns, int64_t n_turns, int S, int P, int F,
+                      const int64_t* gap_us, int n_rate, const int64_t* kv_blocks, int n_kv,
+                      const int64_t* policies, int n_pol, const int64_t* est, const int64_t* eng,
+                      const int64_t* fitted, int J, int64_t replica, char* buf, int64_t cap,
+                      int64_t* len, int64_t* summary);
+
 /* Per sweep cell sums over seeds (cells = rate x kv x policy). out: int64[8] per cell. */
 int or_jct_stats(const int64_t* summary, int64_t n_replicas, int n_cells, int64_t* out);
 

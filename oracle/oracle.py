@@ -60,6 +60,9 @@ def lib():
         _lib.or_simulate.restype = C.c_int
         _lib.or_simulate.argtypes = [p, p, i64, C.c_int, C.c_int, C.c_int, p, C.c_int, p, C.c_int,
                                      p, C.c_int, p, p, p, C.c_int, i64, i64, C.c_int, p, p, p]
+        _lib.or_simulate_audit.restype = C.c_int
+        _lib.or_simulate_audit.argtypes = [p, p, i64, C.c_int, C.c_int, C.c_int, p, C.c_int, p,
+                                           C.c_int, p, C.c_int, p, p, p, C.c_int, i64, p, i64, p, p]
         _lib.or_jct_stats.restype = C.c_int
         _lib.or_jct_stats.argtypes = [p, i64, C.c_int, p]
     return _lib
@@ -172,6 +175,37 @@ def simulate(trace, sweep, engine, r_begin: int = 0, r_end: int | None = None,
     if rc != 0:
         raise ValueError("or_simulate rejected its input (%d)" % rc)
     return (summ, jct, bub) if want_bubble else (summ, jct)
+
+
+def audit(trace, sweep, engine, replica: int):
+    """Per-decision audit log of one replica: (summary int64[16], [records])."""
+    import json
+    progs = np.ascontiguousarray(trace.programs)
+    turns = np.ascontiguousarray(trace.turns, dtype=np.int32)
+    gap, kv = _i64(sweep.gap_us), _i64(sweep.kv_blocks)
+    pol, est = _i64(sweep.policy_array()), _i64(sweep.estimator.as_array())
+    eng = _i64(engine.as_array() if hasattr(engine, "as_array") else engine)
+    if sweep.fitted is not None:
+        fitted = _i64(sweep.fitted)
+        J = int(fitted.shape[1])
+    else:
+        fitted, J = np.zeros((trace.n_tools, 1), np.int64), 1
+    summ = np.zeros(16, np.int64)
+    n = C.c_int64(0)
+    cap = 1 << 16
+    while True:
+        buf = C.create_string_buffer(cap)
+        rc = lib().or_simulate_audit(_ptr(progs), _ptr(turns), turns.shape[0], trace.n_seeds,
+                                     trace.n_programs, trace.n_tools, _ptr(gap), len(gap), _ptr(kv),
+                                     len(kv), _ptr(pol), len(sweep.policies), _ptr(est), _ptr(eng),
+                                     _ptr(fitted), J, int(replica), buf, cap, C.byref(n), _ptr(summ))
+        if rc < 0:
+            raise ValueError("or_simulate_audit rejected its input (%d)" % rc)
+        if rc == 0:
+            break
+        cap = int(n.value) + 1
+    text = buf.raw[: n.value].decode()
+    return summ, [json.loads(l) for l in text.splitlines() if l]
 
 
 def jct_stats(summary: np.ndarray, n_cells: int) -> np.ndarray:

@@ -323,9 +323,13 @@ int ct_simulate_batch_ex(ct_ctx* c, const ct_trace_set* tr, const ct_sweep* sw,
   int n_simple32 = 0;
   if (a.d32)
     for (size_t i = 0; i < n_pol; ++i) n_simple32 += ct::simple_policy(sw->policies[i], E) ? 1 : 0;
+  int n_ext32 = 0;
+  if (a.d32)
+    for (size_t i = 0; i < n_pol; ++i) n_ext32 += ct::ext_policy(sw->policies[i], E) ? 1 : 0;
   const int mode = growth    ? 0
                    : ns == 1 ? (n_fast == (int)n_pol       ? 1
                                 : n_simple32 == (int)n_pol ? 3
+                                : n_ext32 == (int)n_pol    ? 6
                                 : n_simple32 > 0           ? 2
                                                            : 0)
                              : (n_prog == (int)n_pol ? 1 : 0);
@@ -587,10 +591,10 @@ int fit_prepare(ct_ctx* c, const ct_samples* sm, const ct_cost_params* cp,
   return CT_OK;
 }
 
-int fit_grid(ct_ctx* c, const ct::FitArgs& fa, const ct::FitPlan& plan, bool fused) {
-  const int key = plan.smem * 8 + (plan.pairs ? 4 : 0) + (fused ? 2 : 0) + (fa.b_us < (1ll << 26) ? 1 : 0);
+int fit_grid(ct_ctx* c, const ct::FitArgs& fa, const ct::FitPlan& plan) {
+  const int key = plan.smem * 8 + (plan.pairs ? 4 : 0) + (fa.b_us < (1ll << 26) ? 1 : 0);
   if (c->fit_occ_key != key || c->fit_occ_step1 != (fa.step == 1)) {
-    c->fit_occ = ct::fit_hist_occupancy(fa, plan, fused);
+    c->fit_occ = ct::fit_hist_occupancy(fa, plan);
     c->fit_occ_key = key;
     c->fit_occ_step1 = fa.step == 1;
   }
@@ -666,27 +670,22 @@ int ct_fit_ttl(ct_ctx* c, const ct_samples* sm, const ct_cost_params* cp,
   sa.ttl_paper = out->ttl_paper;
   sa.stats_out = out->stats;
   sa.n_invalid = out->n_invalid;
-  const bool fused = !plan.pairs;
-  if (fused) {  // the kernel zeroes the other half for the next call
+  if (!plan.pairs) {  // the histogram kernel zeroes the other half for the next call
     fa.zero = (unsigned long long*)c->fitbuf[cur ^ 1];
     fa.zero_words = W;
   }
-  const int grid = fit_grid(c, fa, plan, fused);
+  const int grid = fit_grid(c, fa, plan);
   if (grid < 1) return fail(CT_ECUDA, "fit kernel cannot be resident");
   if (c->timing) CT_CUDA(cudaEventRecord(c->ev[2], s));
-  cudaError_t e = ct::launch_fit_hist(fa, sa, plan, grid, fused, s);
+  cudaError_t e = ct::launch_fit_hist(fa, plan, grid, s);
   if (e != cudaSuccess) return cuda_fail(e, "fit launch");
-  int launches = 1;
-  if (!fused) {
-    e = ct::launch_fit_finish(sa, s);
-    if (e != cudaSuccess) return cuda_fail(e, "fit finish launch");
-    ++launches;
-  }
+  e = ct::launch_fit_finish(sa, s);
+  if (e != cudaSuccess) return cuda_fail(e, "fit finish launch");
   if (c->timing) CT_CUDA(cudaEventRecord(c->ev[3], s));
   c->fit_timed = c->timing;
-  if (fused) c->fit_clean[cur ^ 1] = W;
+  if (!plan.pairs) c->fit_clean[cur ^ 1] = W;
   c->fit_cur = cur ^ 1;
-  c->last.launches = launches;
+  c->last.launches = 2;
   return CT_OK;
 }
 
@@ -702,10 +701,10 @@ int ct_fit_ttl_partial(ct_ctx* c, const ct_samples* sm, const ct_cost_params* cp
   cudaStream_t s = (cudaStream_t)stream;
   CT_CUDA(cudaMemsetAsync(acc, 0, 8 * (size_t)ct::fit_acc_words(fa.F, fa.K), s));
   fa.acc = (unsigned long long*)acc;
-  const int grid = fit_grid(c, fa, plan, false);
+  const int grid = fit_grid(c, fa, plan);
   if (grid < 1) return fail(CT_ECUDA, "fit kernel cannot be resident");
   if (c->timing) CT_CUDA(cudaEventRecord(c->ev[2], s));
-  cudaError_t e = ct::launch_fit_hist(fa, sa, plan, grid, false, s);
+  cudaError_t e = ct::launch_fit_hist(fa, plan, grid, s);
   if (e != cudaSuccess) return cuda_fail(e, "fit launch");
   if (c->timing) CT_CUDA(cudaEventRecord(c->ev[3], s));
   c->fit_timed = c->timing;

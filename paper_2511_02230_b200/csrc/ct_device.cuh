@@ -80,9 +80,18 @@ __host__ __device__ __forceinline__ uint64_t isqrt_u128(u128_t x) {
   const double dx = (double)(uint64_t)(x >> 64) * 18446744073709551616.0 + (double)(uint64_t)x;
   const double sq = sqrt(dx);  // relative error ~2^-54: within ~2^10 of the root (>= 2^32)
   uint64_t r = sq >= 18446744073709551615.0 ? 0xffffffffffffffffull : (uint64_t)sq;
-  // one integer Newton step leaves an error below one, then exact correction
-  const u128_t nr = ((u128_t)r + x / r) >> 1;
-  r = nr > (u128_t)0xffffffffffffffffull ? 0xffffffffffffffffull : (uint64_t)nr;
+  // one Newton step on the exact residual (x - r^2) / (2 r), in double: error below a few
+  // units, then exact integer correction (no 128-bit division)
+  const u128_t r2 = (u128_t)r * r;
+  const double res = r2 > x ? -(double)(r2 - x) : (double)(x - r2);
+  const double step = res / (2.0 * (double)r);
+  if (step >= 0.0) {
+    const uint64_t up = (uint64_t)step;
+    r = up > 0xffffffffffffffffull - r ? 0xffffffffffffffffull : r + up;
+  } else {
+    const uint64_t dn = (uint64_t)(-step);
+    r = dn > r ? 0 : r - dn;
+  }
   while ((u128_t)r * r > x) --r;
   while (r < 0xffffffffffffffffull && (u128_t)(r + 1) * (r + 1) <= x) ++r;
   return r;

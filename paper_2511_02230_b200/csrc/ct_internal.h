@@ -76,6 +76,14 @@ inline __host__ __device__ bool simple_policy(const ct_policy& p, const ct_engin
          (p.dram == 0 || E.dram_blocks <= 0) && p.pause != CT_PAUSE_INFERCEPT;
 }
 
+// The extended class, for which the P <= 32 replay has a 32-bit-time path with the DRAM tier,
+// Autellix PLAS and InferCept (replay_one_t32<true, true>, MODE 6): any priority, any pause
+// action, DRAM on or off; only the alternative readings (flags) are left to the generic path.
+inline __host__ __device__ bool ext_policy(const ct_policy& p, const ct_engine_params& E) {
+  (void)E;
+  return p.flags == 0;
+}
+
 // Bytes of shared memory one replica (one warp) needs for `ns` slots per lane and F tools.
 // KV growth (NEXT-2) always runs the shared-memory path, also for P <= 32.
 int replay_smem_per_warp(int ns, int F, bool growth, int mode);
@@ -101,7 +109,7 @@ struct FitArgs {
   uint32_t div_m, div_sh, div_add; // floor(x / step) for 32-bit x (step >= 2)
   int64_t b_us;
   unsigned long long* acc;         // accumulator, fit_acc_words(F, K) words
-  unsigned long long* zero;        // FUSED: zero this buffer (the next call's accumulator)
+  unsigned long long* zero;        // zero this buffer first (the next call's accumulator) or NULL
   int64_t zero_words;
 };
 
@@ -127,10 +135,9 @@ struct FitPlan {
   int lr, smem;
 };
 FitPlan fit_plan(int K, int F, bool pairs);
-int fit_hist_occupancy(const FitArgs& a, const FitPlan& p, bool fused);  // CTAs per SM
-// fused: cooperative launch, histogram + grid barrier + finish (ct_fit_ttl, CSR layout)
-cudaError_t launch_fit_hist(const FitArgs& a, const ScanArgs& s, const FitPlan& p, int grid,
-                            bool fused, cudaStream_t st);
+int fit_hist_occupancy(const FitArgs& a, const FitPlan& p);  // CTAs per SM
+cudaError_t launch_fit_hist(const FitArgs& a, const FitPlan& p, int grid, cudaStream_t st);
+// programmatic dependent launch after the histogram pass on the same stream
 cudaError_t launch_fit_finish(const ScanArgs& s, cudaStream_t st);
 
 // On-device trace synthesis (synth.cu).  Device scratch is owned by the context.

@@ -588,10 +588,14 @@ __device__ __forceinline__ uint32_t sat32(int64_t v) {  // v >= 0
 
 // STATS = false: the TTL-grid class (fast_policy); STATS = true: program or request FCFS with
 // the estimator (simple_policy: EVICT, FIXED with a threshold, PAPER CalcTTL, FITTED), whose
-// statistic rows live in shared memory as on the 64-bit path.
-template <bool STATS>
+// statistic rows live in shared memory as on the 64-bit path.  EXT (with STATS): the extended
+// class (ext_policy: any priority, any pause action, the DRAM tier; flags 0) adds Autellix PLAS,
+// InferCept, the DRAM write-through / serialized H2D channel / async load of R18 (LOADING ->
+// READY -> joined at the next scheduling point) on the same 32-bit times.
+template <bool STATS, bool EXT = false>
 __device__ __forceinline__ bool replay_one_t32(const ReplayArgs& a, int64_t r, Stat* stats,
                                                int lane) {
+  static_assert(STATS || !EXT, "the extended class needs the estimator rows");
   const int P = a.P;
   const int64_t npol = a.n_pol, nkv = a.n_kv, nrate = a.n_rate;
   const int pol_i = (int)(r % npol);
@@ -606,7 +610,10 @@ __device__ __forceinline__ bool replay_one_t32(const ReplayArgs& a, int64_t r, S
   const int F = a.F;
   const ct_estimator_params& est = a.est;
   const bool need_stats =
-      STATS && (pause == CT_PAUSE_PAPER || (pause == CT_PAUSE_FIXED && polp->t_thresh_us != CT_ALWAYS));
+      STATS && (pause == CT_PAUSE_PAPER || (EXT && pause == CT_PAUSE_INFERCEPT) ||
+                (pause == CT_PAUSE_FIXED && polp->t_thresh_us != CT_ALWAYS));
+  const bool dram_on = EXT && polp->dram != 0 && a.eng.dram_blocks > 0;
+  const bool plas = EXT && prio == CT_PRIO_PLAS;
   if (need_stats) {
     for (int i = lane; i < 4 * (F + 1); i += 32) ((int64_t*)stats)[i] = 0;
     __syncwarp();
@@ -632,19 +639,23 @@ __device__ __forceinline__ bool replay_one_t32(const ReplayArgs& a, int64_t r, S
   const int64_t arr0 = shfl64(arr64, 0);  // programs arrive in index order: the time origin
   const uint32_t arr = live ? sat32(arr64 - arr0) : T32_INF;
   int st = S_OUT;
-  uint32_t tev = arr;      // arrival (OUT), tool return (TOOL); INF otherwise
+  uint32_t tev = arr;      // arrival (OUT), tool return (TOOL), load done (LOAD); INF otherwise
   uint32_t texp = T32_INF; // expiry + 1 while pinned in a tool call
   uint32_t req = 0;        // request arrival; JCT once done
   uint32_t fin = 0;        // iteration index at whose end the running request finishes
   int32_t ctx = 0, gblk = 0, turn = 0;
+  int32_t dblk = 0, unc = 0;  // EXT: DRAM copy blocks; uncached tokens of a loading request
+  uint32_t svc = 0;           // EXT: attained engine time (PLAS), <= now on this path
   bool pin = false;
   int4 rec = make_int4(0, 0, -1, 0);
 
   uint32_t now = 0, iter_end = 0, n_it = 0;
   bool in_flight = false;
   int32_t free_blk = (int32_t)a.kv[kv_i];
+  int32_t dfree = dram_on ? (int32_t)E.dram_blocks : 0;
+  uint32_t chan = 0;  // EXT: the H2D channel is busy until chan
   int32_t D = 0, turns_done = 0;
-  int n_run = 0;
+  int n_run = 0, n_load = 0;  // n_load counts LOADING and READY (EXT)
   int32_t kv_sum = 0;
   int64_t pf = 0;
   int status = CT_R_OK;
@@ -666,6 +677,18 @@ __device__ __forceinline__ bool replay_one_t32(const ReplayArgs& a, int64_t r, S
   int64_t base_ps = 0;
   uint32_t d_cur = 0;
   float rd_cur = 0.0f;
+  // evict(v): free its GPU blocks; DRAM write-through when the tier is on (R18).  Uniform.
+  auto evict = [&](int v) {
+    free_blk += __shfl_sync(FULL_MASK, gblk, v);
+    int32_t keep = 0;
+    if (dram_on) {
+      const uint32_t vctx = __shfl_sync(FULL_MASK, (uint32_t)ctx, v);
+      const int32_t nb = (int32_t)ceil_div_magic(vctx, bsm);
+      dfree += __shfl_sync(FULL_MASK, dblk, v);
+      if (nb > 0 && nb <= dfree) { keep = nb; dfree -= nb; }
+    }
+    if (lane == v) { gblk = 0; dblk = keep; pin = false; texp = T32_INF; }
+  };
 
   for (;;) {
     uint32_t t;
@@ -681,11 +704,20 @@ __device__ __forceinline__ bool replay_one_t32(const ReplayArgs& a, int64_t r, S
     if (__any_sync(FULL_MASK, min(tev, texp) <= now)) {
       // PinExpiry (EAGER, R4/R15) precedes the program's own tool return at the same µs (R1)
       const bool xd = texp <= now && texp <= tev;
-      const uint32_t m = __ballot_sync(FULL_MASK, xd);
+      uint32_t m = __ballot_sync(FULL_MASK, xd);
       if (m) {
         acc_add(ACC_EXP, __popc(m));
-        free_blk += (int32_t)__reduce_add_sync(FULL_MASK, xd ? (uint32_t)gblk : 0u);
-        if (xd) { gblk = 0; pin = false; texp = T32_INF; }
+        if (dram_on) {  // write-through order matters: (time, index) order
+          while (m) {
+            const uint32_t tm = __reduce_min_sync(FULL_MASK, (m >> lane) & 1u ? texp : T32_INF);
+            const int p = __ffs(__ballot_sync(FULL_MASK, ((m >> lane) & 1u) && texp == tm)) - 1;
+            m &= ~(1u << p);
+            evict(p);
+          }
+        } else {
+          free_blk += (int32_t)__reduce_add_sync(FULL_MASK, xd ? (uint32_t)gblk : 0u);
+          if (xd) { gblk = 0; pin = false; texp = T32_INF; }
+        }
       }
       const bool due = tev <= now;
       if (need_stats) {  // estimator rows: Δ_obs = dur of the finished turn's tool, clamped (R5)
@@ -723,6 +755,9 @@ __device__ __forceinline__ bool replay_one_t32(const ReplayArgs& a, int64_t r, S
         req = tev;
         tev = T32_INF;
         rec = __ldg((const int4*)a.turns + turn0);
+      } else if (EXT && due && st == S_LOAD) {  // LoadDone
+        st = S_READY;
+        tev = T32_INF;
       }
     }
 
@@ -739,9 +774,10 @@ __device__ __forceinline__ bool replay_one_t32(const ReplayArgs& a, int64_t r, S
         --n_run;
         kv_sum -= pg;
         if (lane == p) ctx += rec.x + rec.y;
-        if (pt == pn - 1) {  // last request: free its KV, the program completes
+        if (pt == pn - 1) {  // last request: free its KV (and DRAM copy), the program completes
           free_blk += pg;
-          if (lane == p) { gblk = 0; st = S_DONE; req = now - arr; }
+          if (EXT) dfree += __shfl_sync(FULL_MASK, dblk, p);
+          if (lane == p) { gblk = 0; dblk = 0; st = S_DONE; req = now - arr; }
           ++D;
           turns_done += pn;
         } else {
@@ -754,13 +790,23 @@ __device__ __forceinline__ bool replay_one_t32(const ReplayArgs& a, int64_t r, S
               ttl = calc_ttl(stats[F], stats[ptool], est, D, turns_done);  // cache measured slower here
             } else if (pause == CT_PAUSE_FITTED) {
               ttl = __ldg(&a.fitted[(int64_t)ptool * a.J + min(pt, a.J - 1)]);
+            } else if (EXT && pause == CT_PAUSE_INFERCEPT) {
+              // preserve (no TTL) iff the predicted tool time < the swap round trip
+              const int64_t pred = infercept_predict(stats[F], stats[ptool], est);
+              const uint32_t pctx = __shfl_sync(FULL_MASK, (uint32_t)ctx, p);
+              const int64_t blocks = ceil_div_magic(pctx, bsm);
+              const int64_t swap = 2 * ceil_ps_to_us((uint64_t)(blocks * E.c_h2d_ps));
+              ttl = pred < swap ? CT_INF64 : 0;
             }
           }
           if (ttl > 0) {  // pin_request only if TTL != 0
             if (lane == p) {
               pin = true;
-              texp = ttl >= (int64_t)T32_LIM ? T32_LIM : sat32((int64_t)now + ttl + 1);
+              texp = (EXT && ttl == CT_INF64) ? T32_INF  // InferCept: preserved, no expiry
+                     : ttl >= (int64_t)T32_LIM ? T32_LIM : sat32((int64_t)now + ttl + 1);
             }
+          } else if (EXT) {
+            evict(p);
           } else {  // evict
             free_blk += pg;
             if (lane == p) { gblk = 0; pin = false; texp = T32_INF; }
@@ -774,19 +820,32 @@ __device__ __forceinline__ bool replay_one_t32(const ReplayArgs& a, int64_t r, S
     // ---- scheduling point (R3) --------------------------------------------------------------
     int admitted = 0;
     bool stable = true;
-    if (__any_sync(FULL_MASK, st == S_QUEUED)) {
+    if (__any_sync(FULL_MASK, st == S_QUEUED || (EXT && st == S_READY))) {
+      if (EXT) {  // loaded requests join the batch
+        const bool join = st == S_READY;
+        const uint32_t m = __ballot_sync(FULL_MASK, join);
+        if (m) {
+          kv_sum += (int32_t)__reduce_add_sync(FULL_MASK, join ? (uint32_t)gblk : 0u);
+          pf += (int64_t)__reduce_add_sync(FULL_MASK, join ? (uint32_t)unc : 0u);
+          n_run += __popc(m);
+          n_load -= __popc(m);
+          if (join) { st = S_RUN; fin = sat32((int64_t)n_it + rec.y); }
+        }
+      }
       for (;;) {  // admit loop (victims PAPER.md:645-655)
         const uint32_t mq = __ballot_sync(FULL_MASK, st == S_QUEUED);
         if (!mq) break;
-        if (n_run >= E.max_batch) break;
+        if (n_run + n_load >= E.max_batch) break;
         int h;
         if (!STATS || prio == CT_PRIO_PROG_FCFS) {  // pinned-queued first, then queued, by index
           const uint32_t mp = __ballot_sync(FULL_MASK, st == S_QUEUED && pin);
           h = __ffs(mp ? mp : mq) - 1;
-        } else {  // REQ_FCFS (vanilla vLLM): earliest request, ties by index
+        } else {  // REQ_FCFS (vanilla vLLM): earliest request; PLAS (Autellix,
+                  // PAPER.md:207): least attained service; ties by index
           const bool q = st == S_QUEUED;
-          const uint32_t mr = __reduce_min_sync(FULL_MASK, q ? req : T32_INF);
-          h = __ffs(__ballot_sync(FULL_MASK, q && req == mr)) - 1;
+          const uint32_t key = plas ? svc : req;
+          const uint32_t mr = __reduce_min_sync(FULL_MASK, q ? key : T32_INF);
+          h = __ffs(__ballot_sync(FULL_MASK, q && key == mr)) - 1;
         }
         const int32_t hctx = __shfl_sync(FULL_MASK, ctx, h);
         const int32_t hg = __shfl_sync(FULL_MASK, gblk, h);
@@ -798,8 +857,12 @@ __device__ __forceinline__ bool replay_one_t32(const ReplayArgs& a, int64_t r, S
             const uint32_t mv = __ballot_sync(FULL_MASK, pin && lane != h);
             if (!mv) break;
             const int v = 31 - __clz(mv);
-            free_blk += __shfl_sync(FULL_MASK, gblk, v);
-            if (lane == v) { gblk = 0; pin = false; texp = T32_INF; }
+            if (EXT) {
+              evict(v);
+            } else {
+              free_blk += __shfl_sync(FULL_MASK, gblk, v);
+              if (lane == v) { gblk = 0; pin = false; texp = T32_INF; }
+            }
             acc_add(ACC_VICT, 1);
           }
         }
@@ -811,25 +874,50 @@ __device__ __forceinline__ bool replay_one_t32(const ReplayArgs& a, int64_t r, S
         const int32_t ng = hg + (int32_t)need;
         acc_add(ACC_BUBBLE, (int64_t)(now - __shfl_sync(FULL_MASK, req, h)));
         const bool hp = __shfl_sync(FULL_MASK, pin ? 1 : 0, h) != 0;
-        const int64_t cached = hp ? hctx : 0;
-        if (hp) acc_add(ACC_HITS, 1);
-        else acc_add(ACC_RECOMP, hctx);
+        const int32_t hd = dram_on ? __shfl_sync(FULL_MASK, dblk, h) : 0;
+        bool loading = false;
+        uint32_t ld = 0;
+        int64_t cached;
+        if (hp) {
+          cached = hctx;
+          acc_add(ACC_HITS, 1);
+        } else if (dram_on && hd > 0 && hd == (int32_t)ceil_div_magic((uint32_t)hctx, bsm)) {
+          // the DRAM copy covers the context: load it through the serialized H2D channel
+          cached = hctx;
+          loading = true;
+          ld = sat32((int64_t)max(now, chan) + ceil_ps_to_us((uint64_t)((int64_t)hd * E.c_h2d_ps)));
+          chan = ld;
+          acc_add(ACC_RELOAD, 1);
+        } else {
+          cached = 0;
+          acc_add(ACC_RECOMP, hctx);
+        }
         const int64_t u = hctx + hnew - cached;
         acc_add(ACC_PREFILL, u);
         if (lane == h) {
           pin = false;
           texp = T32_INF;
           gblk = ng;
-          st = S_RUN;
-          fin = sat32((int64_t)n_it + rec.y);
+          if (EXT && loading) {
+            st = S_LOAD;
+            tev = ld;
+            unc = (int32_t)u;
+          } else {
+            st = S_RUN;
+            fin = sat32((int64_t)n_it + rec.y);
+          }
         }
-        ++n_run;
-        kv_sum += ng;
-        pf += u;
+        if (EXT && loading) {
+          ++n_load;
+        } else {
+          ++n_run;
+          kv_sum += ng;
+          pf += u;
+        }
         ++admitted;
       }
-      // unschedulable: the head missed with nothing running (C-5 5c)
-      if (admitted == 0 && n_run == 0 && __any_sync(FULL_MASK, st == S_QUEUED)) {
+      // unschedulable: the head missed with nothing running or loading (C-5 5c)
+      if (admitted == 0 && n_run == 0 && n_load == 0 && __any_sync(FULL_MASK, st == S_QUEUED)) {
         status = CT_R_UNSCHEDULABLE;
         break;
       }
@@ -858,6 +946,7 @@ __device__ __forceinline__ bool replay_one_t32(const ReplayArgs& a, int64_t r, S
       n_it += (uint32_t)k;
       iter_end = (uint32_t)end;
       acc_add(ACC_BUSY, dur);
+      if (plas && st == S_RUN) svc += (uint32_t)dur;  // every running request accrues the iterations
       in_flight = true;
     }
   }
@@ -2173,13 +2262,14 @@ __device__ __forceinline__ bool replay_one_ns32(const ReplayArgs& a, int64_t r,
 // MODE (default engine): P <= 32: 0 every policy generic; 1 every policy in the TTL-grid class
 // (32-bit times, fallback to the 64-bit TTL-grid path); 3 every policy in the simple class
 // (program or request FCFS, 32-bit times with the estimator, fallback to the generic path);
-// 2 mixed: simple-class replicas as in 3, the others generic.  P > 32: 0 generic, 1 every policy in the program-FCFS
+// 2 mixed: simple-class replicas as in 3, the others generic; 6 every policy in the extended class
+// (ext_policy: DRAM tier, PLAS, InferCept; 32-bit times, fallback to the generic path).  P > 32: 0 generic, 1 every policy in the program-FCFS
 // class; 4 every policy in the program-FCFS class with 32-bit times (replay_one_ns32), replicas
 // that reach the horizon are queued for a second launch of MODE 1 over that list (from_list);
 // 5 the same for the simple class with request FCFS (fallback launch: the generic kernel).
 // A trace set that failed the on-device check (validate.cu): no record is read; the replica
 // reports CT_R_INVALID_INPUT with a zero summary and -1 per-program outputs.
-__device__ __noinline__ void write_invalid(const ReplayArgs& a, int64_t r, int lane) {
+__device__ __forceinline__ void write_invalid(const ReplayArgs& a, int64_t r, int lane) {
   const int64_t ri = r - a.r_begin;
   if (lane < 16) ((int64_t*)&a.out[ri])[lane] = lane == 0 ? CT_R_INVALID_INPUT : 0;
   for (int p = lane; p < a.P; p += 32) {
@@ -2193,28 +2283,33 @@ __global__ void __launch_bounds__(128, MINB) replay_kernel(ReplayArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x & 31;
   unsigned char* wm = smem + (threadIdx.x >> 5) * a.smem_per_warp;
-  const bool invalid = a.err[0] != 0;
-  for (;;) {
+  // next replica of this warp (persistent grid over an atomic counter); false when done
+  auto next = [&](int64_t& r) -> bool {
     unsigned long long idx = 0;
     if (lane == 0) idx = atomicAdd(a.counter, 1ull);
     idx = __shfl_sync(FULL_MASK, idx, 0);
-    int64_t r;
     if (a.from_list) {  // replicas queued by a MODE 4 launch earlier on the stream
-      if (idx >= *a.fb_count) break;
+      if (idx >= *a.fb_count) return false;
       r = a.fb_list[idx];
     } else {
       r = a.r_begin + (int64_t)idx;
-      if (r >= a.r_end) break;
+      if (r >= a.r_end) return false;
     }
-    if (invalid) {
-      write_invalid(a, r, lane);
-      continue;
-    }
+    return true;
+  };
+  int64_t r;
+  if (a.err[0] != 0) {  // the trace check failed: no record is read (kept out of the main loop)
+    while (next(r)) write_invalid(a, r, lane);
+    return;
+  }
+  while (next(r)) {
     if (NS == 1 && !VLLM) {
       if (MODE == 1) {
         if (!replay_one_t32<false>(a, r, (Stat*)wm, lane)) replay_one_w32<true>(a, r, (Stat*)wm, lane);
       } else if (MODE == 3 || (MODE == 2 && simple_policy(a.pols[(int)(r % a.n_pol)], a.eng))) {
         if (!replay_one_t32<true>(a, r, (Stat*)wm, lane)) replay_one_w32<false>(a, r, (Stat*)wm, lane);
+      } else if (MODE == 6) {
+        if (!replay_one_t32<true, true>(a, r, (Stat*)wm, lane)) replay_one_w32<false>(a, r, (Stat*)wm, lane);
       } else {
         replay_one_w32<false>(a, r, (Stat*)wm, lane);
       }
@@ -2234,6 +2329,9 @@ __global__ void __launch_bounds__(128, MINB) replay_kernel(ReplayArgs a) {
 #endif
 #ifndef CT_REPLAY_MINB_GRID
 #define CT_REPLAY_MINB_GRID 10
+#endif
+#ifndef CT_REPLAY_MINB_EXT
+#define CT_REPLAY_MINB_EXT 8  // extended class (MODE 6)
 #endif
 
 #ifndef NS32_MINB
@@ -2261,6 +2359,7 @@ static void* pick(int ns, bool growth, int mode) {
       if (mode == 1) return (void*)replay_kernel<1, CT_REPLAY_MINB_GRID, false, 1>;
       if (mode == 2) return (void*)replay_kernel<1, 8, false, 2>;
       if (mode == 3) return (void*)replay_kernel<1, 8, false, 3>;
+      if (mode == 6) return (void*)replay_kernel<1, CT_REPLAY_MINB_EXT, false, 6>;
       return (void*)replay_kernel<1, CT_REPLAY_MINB>;
     case 2: return mode == 4 ? (void*)replay_kernel<2, NS32_MINB, false, 4>
                  : mode == 5 ? (void*)replay_kernel<2, NS32_MINB, false, 5>

@@ -15,26 +15,22 @@
 // (32, or 16 when K is too large for shared memory), laid out [bucket][count x LR | remainder
 // x LR] so that a warp instruction never hits one bank twice.  Each thread keeps the paper
 // statistics in registers.  Pieces are merged and flushed with integer atomics.
-// With FUSED (ct_fit_ttl, a cooperative launch) the same kernel zeroes the other half of the
-// context's double-buffered accumulator (the next call's), passes a grid barrier, and runs
-// phase 2 over the work items (tool row, group of 8 turn buckets): block prefix scan of the
-// row's buckets (cnt_le(k), sum_le(k)), n U(k) in 128-bit integers per turn bucket j
-// (extension C-4), a warp argmax with the smallest k on ties, and CalcTTL of the row
-// (PAPER.md:515-528).  One launch per call: no memset, no second kernel.
-// fit_finish_kernel runs phase 2 alone (ct_fit_ttl_finish, after a cross-rank all-reduce).
+// For ct_fit_ttl the same kernel also zeroes the other half of the context's double-buffered
+// accumulator (the next call's), so no memset precedes it.
+// fit_finish_kernel (phase 2), one warp per work item: (tool row, turn bucket j) -> the row's
+// buckets prefix-summed by a warp scan (cnt_le(k), sum_le(k)), n U(k) in 128-bit integers
+// (extension C-4), a warp argmax with the smallest k on ties; (row) -> the statistics and
+// CalcTTL.  It is a programmatic dependent launch of the histogram pass
+// (no launch gap), and runs alone in ct_fit_ttl_finish after a cross-rank all-reduce.
 // fit_pairs_kernel is the fallback for the unsorted (dur_us, u8 tool) layout (PAPER.md:444's
 // records S = {(f, t)} as they arrive): per-CTA shared bins per (tool, bucket), tool-keyed
 // shared atomics; its accumulator is finished by fit_finish_kernel.
-#include <cooperative_groups.h>
-
 #include <algorithm>
 
 #include "ct_device.cuh"
 #include "ct_internal.h"
 
 namespace ct {
-
-namespace cg = cooperative_groups;
 
 constexpr int FW = 8;         // warps per CTA (histogram and finish phases)
 constexpr int FT = 32 * FW;   // threads per CTA
@@ -90,12 +86,11 @@ struct Lane {
 // One sample d.  Bucket k = min(ceil(d / step), K); the bins keep the count and the sum of
 // r = k step - d in [0, step), so sum_k d = k step count_k - sum_k r is exact with 32-bit bins
 // (bucket K keeps only the count).  ceil(d / step) = floor(x / step), x = d + step - 1 < 2^32,
-// by the divisor's IMAD.HI plus shifts; step = 1 is the identity.  neg collects the sign bits:
-// a negative sample (outside the documented [0, 2^31)) is counted and poisons the outputs.
+// by the divisor's IMAD.HI plus shifts; step = 1 is the identity.  The caller ORs the raw words
+// of every int4 into neg: a negative sample (outside the documented [0, 2^31)) sets its sign
+// bit, is then counted exactly and voids the outputs.
 template <bool IDENT, int LR, typename S1>
-__device__ __forceinline__ void sample(const Lane& L, int32_t d, S1& s1, uint64_t& s2,
-                                       int32_t& neg) {
-  neg |= d;
+__device__ __forceinline__ void sample(const Lane& L, int32_t d, S1& s1, uint64_t& s2) {
   const uint32_t x = (uint32_t)d + L.xoff;
   uint32_t q;
   if (IDENT) {
@@ -143,24 +138,25 @@ __device__ __forceinline__ void hist_piece(const FitArgs& a, const AccView& acc,
   if (va > end) va = end;
   const int64_t vb = va + ((end - va) & ~(int64_t)3);
   if (tid < 32) {  // scalar head and tail (< 4 samples each)
-    if (beg + lane < va) sample<IDENT, LR>(L, __ldg(&a.dur[beg + lane]), s1, s2, neg);
-    if (vb + lane < end) sample<IDENT, LR>(L, __ldg(&a.dur[vb + lane]), s1, s2, neg);
+    if (beg + lane < va) { const int32_t d = __ldg(&a.dur[beg + lane]); neg |= d; sample<IDENT, LR>(L, d, s1, s2); }
+    if (vb + lane < end) { const int32_t d = __ldg(&a.dur[vb + lane]); neg |= d; sample<IDENT, LR>(L, d, s1, s2); }
   }
   const int4* v = (const int4*)(a.dur + va);
   const int64_t nv = (vb - va) >> 2;
   uint64_t q1 = 0, q2 = 0, q3 = 0;  // extra sum-of-squares accumulators (ILP)
   uint32_t s1w = 0;                  // 32-bit partial sum, flushed per 4 FU samples (b < 2^26)
   auto run4 = [&](const int4& x) {
+    neg |= (x.x | x.y) | (x.z | x.w);
     if (FAST32) {
-      sample<IDENT, LR>(L, x.x, s1w, s2, neg);
-      sample<IDENT, LR>(L, x.y, s1w, q1, neg);
-      sample<IDENT, LR>(L, x.z, s1w, q2, neg);
-      sample<IDENT, LR>(L, x.w, s1w, q3, neg);
+      sample<IDENT, LR>(L, x.x, s1w, s2);
+      sample<IDENT, LR>(L, x.y, s1w, q1);
+      sample<IDENT, LR>(L, x.z, s1w, q2);
+      sample<IDENT, LR>(L, x.w, s1w, q3);
     } else {
-      sample<IDENT, LR>(L, x.x, s1, s2, neg);
-      sample<IDENT, LR>(L, x.y, s1, q1, neg);
-      sample<IDENT, LR>(L, x.z, s1, q2, neg);
-      sample<IDENT, LR>(L, x.w, s1, q3, neg);
+      sample<IDENT, LR>(L, x.x, s1, s2);
+      sample<IDENT, LR>(L, x.y, s1, q1);
+      sample<IDENT, LR>(L, x.z, s1, q2);
+      sample<IDENT, LR>(L, x.w, s1, q3);
     }
   };
   int64_t i = tid;
@@ -273,7 +269,7 @@ __device__ __forceinline__ void hist_phase(const FitArgs& a, const AccView& acc,
 }
 
 // ---------------------------------------------------------------------------------------------
-// Phase 2: statistics row -> estimator Stat; argmax of n U(k) per turn bucket; CalcTTL.
+// Phase 2: statistics row -> estimator Stat; argmax of n U(k) per (row, turn bucket); CalcTTL.
 __device__ __forceinline__ Stat row_stat(const unsigned long long* stat, int row) {
   uint64_t v[6];
 #pragma unroll
@@ -288,84 +284,86 @@ __device__ __forceinline__ Stat row_stat(const unsigned long long* stat, int row
   return s;
 }
 
-// Work item (row, jg): turn buckets j in [8 jg, 8 jg + 8), one per warp; jg == 0 also writes the
-// row's CalcTTL offset and statistics.  Tools with fewer than N samples take the pooled row's
-// argmax (PAPER.md:492-494 ladder).  sh holds 2 K u64.
-__device__ __forceinline__ void finish_item(const ScanArgs& a, int row, int jg,
-                                            unsigned long long* sh) {
-  __shared__ unsigned long long wtot[2][FW];
-  __shared__ unsigned long long carry[2];
-  const int K = a.K, F = a.F, J = a.J;
+// V_j = floor(c_pf ctx_j (a_den + a_num w_j) / a_den) (prefill ps saved per hit, turn-weighted)
+// and C_j = c_pin ceil(ctx_j / bs) (ps per µs pinned), extension C-4.
+// (every factor is non-negative and a_den < 2^32, host-checked: an exact u128 / u64 quotient)
+__device__ __forceinline__ void cost_vc(const ct_cost_params& cp, int j, i128_t& V, i128_t& C) {
+  const u128_t num = (u128_t)(uint64_t)cp.c_pf_ps * (uint64_t)cp.ctx_tokens[j] *
+                     ((u128_t)(uint64_t)cp.a_den + (u128_t)(uint64_t)cp.a_num * (uint64_t)cp.turn_weight[j]);
+  V = (i128_t)div_u128_u64(num, (uint64_t)cp.a_den);
+  C = (i128_t)cp.c_pin_ps * ceil_div_i64(cp.ctx_tokens[j], cp.bs);
+}
+
+// One warp item of phase 2.  Items [0, (F+1) J): the argmax of n U(k) for (row, j).  The warp
+// reads the row's buckets itself in rounds of 32 consecutive buckets (lane l: bucket 32 r + l,
+// coalesced; up to FR rounds of loads in flight at once), prefix-sums each round with a warp
+// scan plus the running carry (no block barrier), and evaluates n U(k) = V_j cnt_le(k) -
+// C_j (sum_le(k) + tau_k (n - cnt_le(k))) in 128-bit integers; the smallest maximiser wins
+// (U(0) = 0: no pin).  A tool with fewer than N samples takes the pooled row's
+// argmax (PAPER.md:492-494 ladder).
+// Items [(F+1) J, (F+1) (J+1)): the row's statistics and CalcTTL.
+constexpr int FR = 8;  // rounds of bucket loads in flight (K <= 256: every round)
+
+__device__ __forceinline__ int row_argmax(const unsigned long long* hc, const unsigned long long* hs,
+                                          int K, uint64_t ntot, i128_t V, i128_t C, int64_t step,
+                                          int lane) {
+  uint64_t carry_c = 0, carry_s = 0;
+  i128_t best = 0;
+  int bk = 0;
+  for (int r0 = 0; r0 * 32 < K; r0 += FR) {
+    uint64_t xc[FR], xs[FR];
+#pragma unroll
+    for (int q = 0; q < FR; ++q) {
+      const int k = 32 * (r0 + q) + lane;
+      xc[q] = k < K ? hc[k] : 0;
+      xs[q] = k < K ? hs[k] : 0;
+    }
+#pragma unroll
+    for (int q = 0; q < FR; ++q) {
+      if (32 * (r0 + q) >= K) break;
+      uint64_t ic = xc[q], is = xs[q];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint64_t tc = __shfl_up_sync(FULL_MASK, ic, o), ts = __shfl_up_sync(FULL_MASK, is, o);
+        if (lane >= o) { ic += tc; is += ts; }
+      }
+      const uint64_t cc = carry_c + ic, cs = carry_s + is;  // cnt_le(k), sum_le(k)
+      const int k = 32 * (r0 + q) + lane;
+      if (k >= 1 && k < K) {
+        const i128_t tau = (i128_t)k * step;
+        const i128_t U = V * (i128_t)cc - C * ((i128_t)cs + tau * (i128_t)(ntot - cc));
+        if (U > best) { best = U; bk = k; }  // per lane k increases: > keeps the smallest
+      }
+      carry_c += __shfl_sync(FULL_MASK, ic, 31);
+      carry_s += __shfl_sync(FULL_MASK, is, 31);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const uint64_t lo = __shfl_xor_sync(FULL_MASK, (uint64_t)best, o);
+    const uint64_t hi = __shfl_xor_sync(FULL_MASK, (uint64_t)((u128_t)best >> 64), o);
+    const int ok = __shfl_xor_sync(FULL_MASK, bk, o);
+    const i128_t ob = (i128_t)(((u128_t)hi << 64) | lo);
+    if (ob > best || (ob == best && ok < bk)) { best = ob; bk = ok; }
+  }
+  return bk;
+}
+
+__device__ __forceinline__ void finish_warp(const ScanArgs& a, int item, int lane) {
+  const int K = a.K, F = a.F, J = a.J, K1 = K + 1;
   const AccView acc = acc_view(const_cast<unsigned long long*>(a.acc), F, K);
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const unsigned long long n_bad = *acc.invalid;
-  if (n_bad) {  // samples outside [0, 2^31): no table, sentinels everywhere (block-uniform)
-    for (int j = jg * FW + warp; lane == 0 && j < min(J, (jg + 1) * FW); j += FW)
-      a.ttl_argmax[(int64_t)row * J + j] = CT_TTL_INVALID;
-    if (tid == 0 && jg == 0) {
+  if (item >= (F + 1) * J) {  // statistics + CalcTTL of one row
+    const int row = item - (F + 1) * J;
+    if (lane != 0) return;
+    if (n_bad) {  // samples outside [0, 2^31): no table (CT_TTL_INVALID everywhere)
       a.ttl_paper[row] = CT_TTL_INVALID;
       if (a.stats_out)
         for (int q = 0; q < 4; ++q) a.stats_out[row * 4 + q] = 0;
       if (row == 0 && a.n_invalid) *a.n_invalid = (int64_t)n_bad;
+      return;
     }
-    return;
-  }
-  unsigned long long* pc = sh;      // [K] inclusive prefix of counts
-  unsigned long long* ps = sh + K;  // [K] inclusive prefix of sums
-  const Stat f = row_stat(acc.stat, row);
-  const int src = (row == F || f.n < a.est.n_min) ? F : row;
-  if (tid == 0) carry[0] = carry[1] = 0;
-  __syncthreads();
-  const int K1 = K + 1;
-  for (int base = 0; base < K; base += FT) {
-    const int b = base + tid;
-    unsigned long long c = 0, s = 0;
-    if (b < K) {
-      c = acc.hcnt[(int64_t)src * K1 + b];
-      s = acc.hsum[(int64_t)src * K1 + b];
-    }
-    unsigned long long ic = c, is = s;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const unsigned long long tc = __shfl_up_sync(FULL_MASK, ic, o), ts = __shfl_up_sync(FULL_MASK, is, o);
-      if (lane >= o) { ic += tc; is += ts; }
-    }
-    if (lane == 31) { wtot[0][warp] = ic; wtot[1][warp] = is; }
-    __syncthreads();
-    unsigned long long oc = carry[0], os = carry[1];
-    for (int w = 0; w < warp; ++w) { oc += wtot[0][w]; os += wtot[1][w]; }
-    if (b < K) { pc[b] = ic + oc; ps[b] = is + os; }
-    __syncthreads();
-    if (tid == FT - 1) { carry[0] = ic + oc; carry[1] = is + os; }
-    __syncthreads();
-  }
-  const uint64_t ntot = carry[0] + acc.hcnt[(int64_t)src * K1 + K];  // + the overflow bucket
-  const ct_cost_params& cp = a.cost;
-  const int j = jg * FW + warp;
-  if (j < J) {
-    const i128_t V = ((i128_t)cp.c_pf_ps * cp.ctx_tokens[j] *
-                      ((i128_t)cp.a_den + (i128_t)cp.a_num * cp.turn_weight[j])) / cp.a_den;
-    const i128_t C = (i128_t)cp.c_pin_ps * ceil_div_i64(cp.ctx_tokens[j], cp.bs);
-    i128_t best = 0;  // U(0) = 0: TTL 0 means no pin
-    int bk = 0;
-    for (int k = 1 + lane; k < K; k += 32) {
-      const uint64_t cc = pc[k], cs = ps[k];
-      const i128_t tau = (i128_t)k * cp.grid_step_us;
-      const i128_t U = V * (i128_t)cc - C * ((i128_t)cs + tau * (i128_t)(ntot - cc));
-      if (U > best) { best = U; bk = k; }  // k increases: strict > keeps the smallest
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const uint64_t lo = __shfl_xor_sync(FULL_MASK, (uint64_t)best, o);
-      const uint64_t hi = __shfl_xor_sync(FULL_MASK, (uint64_t)((u128_t)best >> 64), o);
-      const int ok = __shfl_xor_sync(FULL_MASK, bk, o);
-      const i128_t ob = (i128_t)(((u128_t)hi << 64) | lo);
-      if (ob > best || (ob == best && ok < bk)) { best = ob; bk = ok; }
-    }
-    if (lane == 0) a.ttl_argmax[(int64_t)row * J + j] = (int64_t)bk * cp.grid_step_us;
-  }
-  if (tid == 0 && jg == 0) {
-    const Stat g = row_stat(acc.stat, F);
+    const Stat f = row_stat(acc.stat, row), g = row_stat(acc.stat, F);
     a.ttl_paper[row] = calc_ttl(g, f, a.est, a.cost.avg_turns_den, a.cost.avg_turns_num);
     if (a.stats_out) {
       a.stats_out[row * 4 + 0] = f.n;
@@ -374,35 +372,46 @@ __device__ __forceinline__ void finish_item(const ScanArgs& a, int row, int jg,
       a.stats_out[row * 4 + 3] = (int64_t)f.s2hi;
     }
     if (row == 0 && a.n_invalid) *a.n_invalid = 0;
+    return;
   }
-  __syncthreads();  // sh and carry are reused by the next item
+  const int row = item / J, j = item % J;
+  i128_t V, C;
+  cost_vc(a.cost, j, V, C);
+  // n_f (the statistics' sample count, overflow bucket included) and the row's buckets are
+  // loaded together: a tool with n_f < N then redoes the argmax on the pooled row
+  const uint64_t n_row = acc.stat[row * 6];
+  int bk = row_argmax(acc.hcnt + (int64_t)row * K1, acc.hsum + (int64_t)row * K1, K, n_row, V, C,
+                      a.cost.grid_step_us, lane);
+  if (row != F && n_row < (uint64_t)a.est.n_min)
+    bk = row_argmax(acc.hcnt + (int64_t)F * K1, acc.hsum + (int64_t)F * K1, K, acc.stat[F * 6], V,
+                    C, a.cost.grid_step_us, lane);
+  if (lane == 0)
+    a.ttl_argmax[(int64_t)row * J + j] = n_bad ? CT_TTL_INVALID : (int64_t)bk * a.cost.grid_step_us;
 }
 
-__device__ __forceinline__ int finish_items(const ScanArgs& a) { return (a.F + 1) * ((a.J + FW - 1) / FW); }
+__device__ __forceinline__ int finish_items(const ScanArgs& a) { return (a.F + 1) * (a.J + 1); }
 
 // ---------------------------------------------------------------------------------------------
-template <bool IDENT, bool FAST32, int LR, bool FUSED>
-__global__ void __launch_bounds__(FT, 2) fit_hist_kernel(FitArgs a, ScanArgs s) {
+// The histogram pass.  It first lets the finish kernel launch (programmatic dependent launch:
+// the finish kernel's CTAs are scheduled while this grid streams and wait in
+// griddepcontrol.wait for its completion, so no launch gap sits between the two), zeroes the
+// other half of the context's double-buffered accumulator for the next call (no memset), then
+// streams its range.
+template <bool IDENT, bool FAST32, int LR>
+__global__ void __launch_bounds__(FT, 2) fit_hist_kernel(FitArgs a) {
   extern __shared__ __align__(16) uint32_t hsm[];
   __shared__ unsigned long long red[FW][3];
-  if (FUSED) {  // the next call's half of the double-buffered accumulator
-    const int64_t nt = (int64_t)gridDim.x * FT;
-    for (int64_t i = (int64_t)blockIdx.x * FT + threadIdx.x; i < a.zero_words; i += nt) a.zero[i] = 0;
-  }
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  const int64_t nt = (int64_t)gridDim.x * FT;
+  for (int64_t i = (int64_t)blockIdx.x * FT + threadIdx.x; i < a.zero_words; i += nt) a.zero[i] = 0;
   const AccView acc = acc_view(a.acc, a.F, a.K);
   hist_phase<IDENT, FAST32, LR>(a, acc, hsm, red);
-  if (FUSED) {
-    __threadfence();
-    cg::this_grid().sync();
-    const int items = finish_items(s), jgs = (s.J + FW - 1) / FW;
-    for (int it = blockIdx.x; it < items; it += gridDim.x)
-      finish_item(s, it / jgs, it % jgs, (unsigned long long*)hsm);
-  }
 }
 
 __global__ void __launch_bounds__(FT) fit_finish_kernel(ScanArgs s) {
-  extern __shared__ __align__(16) unsigned long long fsh[];
-  finish_item(s, blockIdx.x, blockIdx.y, fsh);
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // the histogram grid is complete
+  const int it = blockIdx.x * FW + (threadIdx.x >> 5);
+  if (it < finish_items(s)) finish_warp(s, it, threadIdx.x & 31);
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -498,50 +507,46 @@ __global__ void __launch_bounds__(FT) fit_pairs_kernel(FitArgs a) {
 }
 
 // ---------------------------------------------------------------------------------------------
-template <bool FUSED>
 static void* hist_fn(bool ident, bool fast32, int lr) {
   if (lr == 32) {
-    if (ident) return fast32 ? (void*)fit_hist_kernel<true, true, 32, FUSED> : (void*)fit_hist_kernel<true, false, 32, FUSED>;
-    return fast32 ? (void*)fit_hist_kernel<false, true, 32, FUSED> : (void*)fit_hist_kernel<false, false, 32, FUSED>;
+    if (ident) return fast32 ? (void*)fit_hist_kernel<true, true, 32> : (void*)fit_hist_kernel<true, false, 32>;
+    return fast32 ? (void*)fit_hist_kernel<false, true, 32> : (void*)fit_hist_kernel<false, false, 32>;
   }
-  if (ident) return fast32 ? (void*)fit_hist_kernel<true, true, 16, FUSED> : (void*)fit_hist_kernel<true, false, 16, FUSED>;
-  return fast32 ? (void*)fit_hist_kernel<false, true, 16, FUSED> : (void*)fit_hist_kernel<false, false, 16, FUSED>;
+  if (ident) return fast32 ? (void*)fit_hist_kernel<true, true, 16> : (void*)fit_hist_kernel<true, false, 16>;
+  return fast32 ? (void*)fit_hist_kernel<false, true, 16> : (void*)fit_hist_kernel<false, false, 16>;
 }
 
-static void* pick_hist(const FitArgs& a, const FitPlan& p, bool fused) {
-  const bool ident = a.step == 1, fast32 = a.b_us < (1ll << 26);
-  return fused ? hist_fn<true>(ident, fast32, p.lr) : hist_fn<false>(ident, fast32, p.lr);
+static void* pick_hist(const FitArgs& a, const FitPlan& p) {
+  return p.pairs ? (void*)fit_pairs_kernel : hist_fn(a.step == 1, a.b_us < (1ll << 26), p.lr);
 }
 
-int fit_hist_occupancy(const FitArgs& a, const FitPlan& p, bool fused) {
-  void* k = p.pairs ? (void*)fit_pairs_kernel : pick_hist(a, p, fused);
+int fit_hist_occupancy(const FitArgs& a, const FitPlan& p) {
+  void* k = pick_hist(a, p);
   if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, p.smem) != cudaSuccess) return 0;
   int nb = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k, FT, p.smem);
   return nb;
 }
 
-cudaError_t launch_fit_hist(const FitArgs& a, const ScanArgs& s, const FitPlan& p, int grid,
-                            bool fused, cudaStream_t st) {
-  if (p.pairs) {
-    void* args[] = {(void*)&a};
-    return cudaLaunchKernel((void*)fit_pairs_kernel, dim3(grid), dim3(FT), args, p.smem, st);
-  }
-  void* k = pick_hist(a, p, fused);
-  void* args[] = {(void*)&a, (void*)&s};
-  if (fused) return cudaLaunchCooperativeKernel(k, dim3(grid), dim3(FT), args, p.smem, st);
-  return cudaLaunchKernel(k, dim3(grid), dim3(FT), args, p.smem, st);
+cudaError_t launch_fit_hist(const FitArgs& a, const FitPlan& p, int grid, cudaStream_t st) {
+  void* args[] = {(void*)&a};
+  return cudaLaunchKernel(pick_hist(a, p), dim3(grid), dim3(FT), args, p.smem, st);
 }
 
+// The finish kernel as a programmatic dependent launch of the histogram pass before it on the
+// stream (its griddepcontrol.wait orders it after that grid's completion and memory flush).
 cudaError_t launch_fit_finish(const ScanArgs& s, cudaStream_t st) {
-  const int smem = 16 * s.K;
-  if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(fit_finish_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-  }
-  const dim3 grid(s.F + 1, (s.J + FW - 1) / FW);
-  fit_finish_kernel<<<grid, FT, smem, st>>>(s);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(((s.F + 1) * (s.J + 1) + FW - 1) / FW);
+  cfg.blockDim = dim3(FT);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, fit_finish_kernel, s);
 }
 
 }  // namespace ct

@@ -6,6 +6,7 @@ slots-per-lane variant (P <= 32, 64, 128, 256), ragged tails, edge cases, and â€
 launch configuration bench.py times â€” sampled replicas of the full BASELINE configs.
 """
 import random
+from dataclasses import replace
 
 import numpy as np
 import pytest
@@ -264,7 +265,7 @@ def test_fit_estimator_extremes(ctx, case):
 
 
 @pytest.mark.parametrize("kind", ["grid", "prog"])
-@pytest.mark.parametrize("P", [1, 17, 32, 33, 70, 130])
+@pytest.mark.parametrize("P", [1, 17, 32, 33, 70, 100, 130, 180, 200, 256])
 def test_ttl_grid_32bit_horizon(ctx, P, kind):
     """TTL-grid-only and program-FCFS-only sweeps run the 32-bit-time kernels (P <= 32: MODE 1 / 3;
     P > 32: MODE 4 plus the list-driven 64-bit launch).  Long inter-arrival gaps (up to 2^30 Âµs),
@@ -296,7 +297,7 @@ def test_ttl_grid_32bit_horizon(ctx, P, kind):
         li = ctx.last_launch()  # the specialised 32-bit kernel ran (DESIGN.md Â§8 MODE)
         assert li["kernel_mode"] == ((4 if kind == "grid" else 5) if P > 32 else
                                      1 if kind == "grid" else 3), li
-        assert li["launches"] == (2 if P > 32 else 1)
+        assert li["launches"] == (2 if P > 32 else 1) + 1  # + the trace check
         R = sw.n_replicas  # a shard: fallback replicas are indexed relative to replica_begin
         s, j = ct.ct_simulate_batch(ctx, ct.DeviceTrace(tr), sw, eng, R // 3, 2 * R // 3, jct=True)
         torch.cuda.synchronize()
@@ -308,3 +309,60 @@ def test_ttl_grid_32bit_horizon(ctx, P, kind):
         span = max(span, int(np.max(os_[:, 7])))
         budget |= bool(np.any(os_[:, 0] == 2))
     assert budget and (P == 1 or span > 2**32)  # both the fallback and EVENT_BUDGET were exercised
+
+
+EXT_POLICIES = [cf.VLLM, cf.VLLM_LMCACHE, cf.Policy(cf.PRIO_PROG_FCFS, cf.PAUSE_EVICT, dram=1),
+                cf.Policy(cf.PRIO_PROG_FCFS, cf.PAUSE_PAPER, dram=1),
+                cf.Policy(cf.PRIO_PROG_FCFS, cf.PAUSE_FITTED, dram=1), cf.AUTELLIX, cf.INFERCEPT,
+                cf.Policy(cf.PRIO_PLAS, cf.PAUSE_PAPER, dram=1),
+                cf.Policy(cf.PRIO_PLAS, cf.PAUSE_INFERCEPT, dram=0),
+                cf.Policy(cf.PRIO_PROG_FCFS, cf.PAUSE_INFERCEPT, dram=1),
+                cf.Policy(cf.PRIO_PROG_FCFS, cf.PAUSE_FIXED, dram=1, t_pin_us=2_000_000),
+                cf.Policy(cf.PRIO_REQ_FCFS, cf.PAUSE_FIXED, dram=1, t_pin_us=5_000_000,
+                          t_thresh_us=1_000_000)]
+
+
+@pytest.mark.parametrize("P", [1, 7, 17, 32])
+def test_extended_class_32bit(ctx, P):
+    """Sweeps whose policies are all in the extended class (DRAM tier, PLAS, InferCept; flags 0)
+    run the 32-bit P <= 32 kernel (MODE 6) with the 64-bit fallback past the 2^32 Âµs horizon
+    (long gaps, a slow engine, slow H2D loads) and EVENT_BUDGET replicas: byte equality."""
+    import paper_2511_02230_b200 as ct
+    n_seeds = 4
+    tr = traces.generate(n_seeds, P, n_bfcl=P // 2, mix="mix", ctx_cap=1500 * 16, stream=60 + P)
+    fitted = np.tile(np.array([[0, 200_000, 3_000_000, 1 << 40]], np.int64), (tr.n_tools, 1))
+    gaps = [1 << 20, 300_000_000, (1 << 30) - 1]
+    engines = [cf.Engine(**{**cf.ENGINE_8B.__dict__, "dram_blocks": 30 * P}),
+               cf.Engine(**{**cf.ENGINE_8B.__dict__, "dram_blocks": 3000, "c_h2d_ps": 4 * 10**11}),
+               cf.Engine(**{**cf.ENGINE_8B.__dict__, "c0_ps": 4 * 10**11, "dram_blocks": 500}),
+               cf.Engine(**{**cf.ENGINE_8B.__dict__, "dram_blocks": 800,
+                            "max_iters": 2000 if P == 1 else 20000})]
+    reloads = 0
+    for eng in engines:
+        sw = cf.Sweep(n_seeds, gaps, [1600, 4096], EXT_POLICIES, fitted=fitted)
+        s, j = ct.ct_simulate_batch(ctx, ct.DeviceTrace(tr), sw, eng, jct=True)
+        torch.cuda.synchronize()
+        os_, oj = O.simulate(tr, sw, eng, n_threads=8)
+        assert_same(s.cpu().numpy(), j.cpu().numpy(), os_, oj)
+        assert ctx.last_launch()["kernel_mode"] == 6
+        reloads += int(os_[:, 15].sum())
+    assert reloads > 0  # DRAM reloads happened
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_random_tiny_extended_class(ctx, seed):
+    rng = random.Random(2000 + seed)
+    tr = random_tiny_set(rng, 300)
+    eng = cf.Engine(c0_ps=rng.randint(1, 3 * 10**6), c_pf_ps=rng.choice([0, 5 * 10**5, 10**6]),
+                    c_kv_ps=rng.choice([0, 10**4, 2 * 10**5]), c_h2d_ps=rng.randint(1, 2 * 10**6),
+                    bs=rng.choice([1, 2, 4]), max_batch=rng.choice([1, 2, 256]),
+                    dram_blocks=rng.randint(0, 12), max_iters=rng.choice([10**6, 40]))
+    est = cf.Estimator(b_us=rng.choice([5, 40]), t_def_us=rng.randint(1, 40), n_min=rng.randint(1, 3),
+                       a_num=rng.randint(0, 2), a_den=rng.choice([1, 3]), ttl_max_us=rng.choice([0, 25]))
+    fitted = np.array([[rng.randint(0, 30) for _ in range(3)] for _ in range(2)], np.int64)
+    pols = [replace(p, flags=0) for p in random_policies(rng, 8)] + [cf.AUTELLIX]
+    sw = cf.Sweep(300, [1 << 20, 3 << 19], [6, 11, 18], pols, est, fitted)
+    gs, gj = gpu_run(ctx, tr, sw, eng)
+    assert ctx.last_launch()["kernel_mode"] == 6
+    os_, oj = O.simulate(tr, sw, eng, n_threads=8)
+    assert_same(gs, gj, os_, oj)

@@ -1,6 +1,7 @@
 """Write profiles/ncu_constants.json entries from an ncu report (bench.py roofline inputs).
 
 usage: python tools/ncu_constants.py replay <report> <workload_name> <replica_turns>
+       python tools/ncu_constants.py replay-auto <report> <cfgN> <log of the captured run>
        python tools/ncu_constants.py fit <report> <samples>
 """
 import csv, io, json, os, subprocess, sys
@@ -29,6 +30,15 @@ def main():
     d = rows[0]
     dram = num(d, "dram__bytes_read.sum") * scale(units["dram__bytes_read.sum"]) + \
         num(d, "dram__bytes_write.sum") * scale(units["dram__bytes_write.sum"])
+    if kind == "replay-auto":  # replica-turns from the captured run's own log line
+        sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+        from ctgen import configs as cf
+        w = {"cfg2": cf.config2, "cfg3": cf.config3, "cfg4": cf.config4, "cfg5": cf.config5}[sys.argv[3]]()
+        import re
+        txt = open(sys.argv[4]).read()
+        turns = float(re.findall(r"replicas (\d+) turns", txt)[0])
+        sys.argv[3:5] = [w.name, str(turns)]
+        kind = "replay"
     if kind == "replay":
         name, turns = sys.argv[3], float(sys.argv[4])
         inst = num(d, "smsp__inst_executed.sum")

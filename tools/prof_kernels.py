@@ -80,7 +80,14 @@ def main():
             w = cf.Workload("cont", w.trace, cf.Sweep(seeds, cf.rate_axis(16), [8192], pols),
                             w.engine, "cfg3 trace, 16 program-FCFS policies")
         else:
-            w = {"cfg2": cf.config2, "cfg3": cf.config3, "cfg5": cf.config5}[name](n_seeds=seeds)
+            w = {"cfg2": cf.config2, "cfg3": cf.config3, "cfg4": cf.config4,
+                 "cfg5": cf.config5}[name](n_seeds=seeds)
+            if name == "cfg4":  # the FITTED policy replays ct_fit_ttl's table (bench's cfg4 step)
+                dur, off = traces.tool_samples(w.trace)
+                p, c = cf.CFG4_FIT, cf.cfg4_fit_cost(w.engine)
+                cp = ct.cost_params(*c[:7], p["ctx_j"], p["w_j"])
+                w.sweep.fitted = ct.ct_fit_ttl(ctx, torch.from_numpy(dur).cuda(), off, cp,
+                                               w.sweep.estimator)[0][:-1]
         dt = ct.DeviceTrace(w.trace)
         for i in range(2):
             e0.record()

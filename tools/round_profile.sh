@@ -1,29 +1,42 @@
 #!/bin/bash
-# Round measurement bundle (run under gpurun, ONE GPU).  Writes gpurun_out/rNN_*.
-# Order: ncu captures first, so the bench's roofline reads per-unit constants (warp-inst per
-# replica-turn, DRAM bytes per sample) measured on the code being benchmarked.
-R=${1:-r01}
+# Round measurement bundle (run under gpurun, ONE GPU).  Writes gpurun_out/${R}_*.
+# Order: ncu captures first, so the bench's roofline reads per-unit constants (warp-inst and
+# DRAM bytes per replica-turn, DRAM bytes per sample) measured on the code being benchmarked.
+# Replay captures are FULL-SIZE launches of each workload (outputs larger than L2), so their
+# DRAM traffic includes the summary writes.
+R=${1:-r02}
 OUT=gpurun_out
 mkdir -p $OUT
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > $OUT/${R}_gpu.txt
-ncu --set full --clock-control none --import-source on -k regex:replay_kernel -c 1 \
-    -o $OUT/${R}_replay_cfg3 python tools/prof_kernels.py replay cfg3 16 > $OUT/${R}_ncu_replay.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:fit_hist -s 1 -c 1 \
+cap() {  # cap NAME WORKLOAD SEEDS
+  ncu --set full --clock-control none --import-source on -k regex:replay_kernel -c 1 \
+      -o $OUT/${R}_replay_$1 python tools/prof_kernels.py replay $2 $3 > $OUT/${R}_ncu_replay_$1.log 2>&1
+}
+cap cfg3 cfg3 256
+cap cfg2 cfg2 4096
+cap cfg4 cfg4 4096
+cap cfg5 cfg5 256
+ncu --set full --clock-control none --import-source on -k regex:fit_hist -s 3 -c 1 \
     -o $OUT/${R}_fit_hist python tools/prof_kernels.py fit 28 > $OUT/${R}_ncu_fit.log 2>&1
-python tools/ncu_constants.py replay $OUT/${R}_replay_cfg3.ncu-rep cfg3_ttl_sweep_64x64x256 29396992 > $OUT/${R}_constants.log 2>&1
-python tools/ncu_constants.py fit $OUT/${R}_fit_hist.ncu-rep 268435456 >> $OUT/${R}_constants.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:replay_kernel -c 1 \
-    -o $OUT/${R}_replay_cfg2 python tools/prof_kernels.py replay cfg2 4096 > $OUT/${R}_ncu_replay2.log 2>&1
-python tools/ncu_constants.py replay $OUT/${R}_replay_cfg2.ncu-rep cfg2_swe200x4096 18761016 >> $OUT/${R}_constants.log 2>&1
+python tools/ncu_constants.py fit $OUT/${R}_fit_hist.ncu-rep 268435456 > $OUT/${R}_constants.log 2>&1
+for w in cfg3 cfg2 cfg4 cfg5; do
+  python tools/ncu_constants.py replay-auto $OUT/${R}_replay_$w.ncu-rep $w $OUT/${R}_ncu_replay_$w.log >> $OUT/${R}_constants.log 2>&1
+done
 cp profiles/ncu_constants.json $OUT/${R}_ncu_constants.json
+python tools/summarize_ncu.py $OUT/${R}_ncu_summary $OUT/${R}_replay_cfg3.ncu-rep $OUT/${R}_replay_cfg2.ncu-rep \
+    $OUT/${R}_replay_cfg4.ncu-rep $OUT/${R}_replay_cfg5.ncu-rep $OUT/${R}_fit_hist.ncu-rep > /dev/null 2>&1
 python bench.py > $OUT/${R}_bench.log 2>&1
 tail -1 $OUT/${R}_bench.log > $OUT/${R}_bench.json
-python bench.py --workload cfg2 > $OUT/${R}_bench_cfg2.log 2>&1
-tail -1 $OUT/${R}_bench_cfg2.log > $OUT/${R}_bench_cfg2.json
-ncu --metrics gpu__time_duration.sum --clock-control none -c 40 --csv --log-file $OUT/${R}_launches.csv \
-    python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e --fit-log2n 26 > $OUT/${R}_launches_bench.log 2>&1
+for w in cfg2 cfg4 cfg5; do
+  python bench.py --workload $w --no-fit-bandwidth > $OUT/${R}_bench_$w.log 2>&1
+  tail -1 $OUT/${R}_bench_$w.log > $OUT/${R}_bench_$w.json
+done
+python bench.py --impl reference --steps 3 --warmup 1 > $OUT/${R}_bench_reference.log 2>&1
+tail -1 $OUT/${R}_bench_reference.log > $OUT/${R}_bench_reference.json
+ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv --log-file $OUT/${R}_launches.csv \
+    python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e --no-fit-bandwidth > $OUT/${R}_launches_bench.log 2>&1
 for t in memcheck racecheck synccheck initcheck; do
   echo "== $t" >> $OUT/${R}_sanitizer.txt
-  timeout 600 compute-sanitizer --tool $t python tools/sanitize.py 2>&1 | grep -E "SUMMARY|sanitize run" >> $OUT/${R}_sanitizer.txt
+  timeout 900 compute-sanitizer --tool $t python tools/sanitize.py 2>&1 | grep -E "SUMMARY|sanitize run" >> $OUT/${R}_sanitizer.txt
 done
 ls -la $OUT
