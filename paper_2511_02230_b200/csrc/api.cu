@@ -37,7 +37,6 @@ struct ct_ctx {
   size_t syn_cap = 0;
   ct_launch_info last{};
   int fit_occ = 0, fit_occ_key = -1;
-  bool fit_occ_step1 = false;
   bool timing = false;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};  // replay start/end, fit start/end
   bool replay_timed = false, fit_timed = false;
@@ -592,11 +591,11 @@ int fit_prepare(ct_ctx* c, const ct_samples* sm, const ct_cost_params* cp,
 }
 
 int fit_grid(ct_ctx* c, const ct::FitArgs& fa, const ct::FitPlan& plan) {
-  const int key = plan.smem * 8 + (plan.pairs ? 4 : 0) + (fa.b_us < (1ll << 26) ? 1 : 0);
-  if (c->fit_occ_key != key || c->fit_occ_step1 != (fa.step == 1)) {
+  const int dv = fa.step == 1 ? 0 : fa.div_add ? 2 : 1;  // the kernel instantiation
+  const int key = (plan.smem * 8 + (plan.pairs ? 4 : 0) + (fa.b_us < (1ll << 26) ? 1 : 0)) * 4 + dv;
+  if (c->fit_occ_key != key) {
     c->fit_occ = ct::fit_hist_occupancy(fa, plan);
     c->fit_occ_key = key;
-    c->fit_occ_step1 = fa.step == 1;
   }
   return c->sm_count * c->fit_occ;
 }

@@ -152,7 +152,21 @@ __host__ __device__ __forceinline__ int64_t bernstein(const Stat& s, uint64_t lq
   const int64_t n = s.n;
   const double rn = 1.0 / (double)n;           // n < 2^31 (validated): exact conversion
   const double rnsh = rn * 2.3283064365386963e-10;  // 2^-32: exact scaling
-  const int64_t mu = (int64_t)div_u128_r((u128_t)(uint64_t)s.s1, (uint64_t)n, rn);
+  // floor(s1 / n) with 64-bit operands (s1 < 2^63): double estimate, one 64-bit correction
+  int64_t mu;
+  {
+    const uint64_t num = (uint64_t)s.s1, den = (uint64_t)n;
+    const double est = (double)num * rn;
+    if (est < 1125899906842624.0) {  // 2^50: the estimate is within one of the quotient
+      uint64_t q = (uint64_t)est;
+      const uint64_t prod = q * den;   // <= num + den < 2^64
+      if (prod > num) q -= 1;
+      else if (num - prod >= den) q += 1;
+      mu = (int64_t)q;
+    } else {
+      mu = (int64_t)(num / den);
+    }
+  }
   u128_t v = 0;
   if (n >= 2) {
     u128_t s2 = ((u128_t)s.s2hi << 64) | s.s2lo;
@@ -172,9 +186,17 @@ __host__ __device__ __forceinline__ int64_t calc_ttl(const Stat& g, const Stat& 
                                             const ct_estimator_params& e, int64_t n_done,
                                             int64_t turns_done) {
   int64_t B;
-  if (g.n < e.n_min) B = e.t_default_us;
-  else if (f.n >= e.n_min) B = bernstein(f, e.lq, e.b_us);
-  else B = bernstein(g, e.lq, e.b_us);
+  if (g.n < e.n_min) {
+    B = e.t_default_us;
+  } else {  // one inlined bound on the selected row (tool if |S_f| >= N, else global)
+    const bool tool = f.n >= e.n_min;
+    Stat s;
+    s.n = tool ? f.n : g.n;
+    s.s1 = tool ? f.s1 : g.s1;
+    s.s2lo = tool ? f.s2lo : g.s2lo;
+    s.s2hi = tool ? f.s2hi : g.s2hi;
+    B = bernstein(s, e.lq, e.b_us);
+  }
   if (B < 1) B = 1;
   const u128_t T2 = (u128_t)(uint64_t)e.t_default_us * (uint64_t)e.t_default_us;  // < 2^80
   u128_t ttl;

@@ -86,18 +86,21 @@ struct Lane {
 // One sample d.  Bucket k = min(ceil(d / step), K); the bins keep the count and the sum of
 // r = k step - d in [0, step), so sum_k d = k step count_k - sum_k r is exact with 32-bit bins
 // (bucket K keeps only the count).  ceil(d / step) = floor(x / step), x = d + step - 1 < 2^32,
-// by the divisor's IMAD.HI plus shifts; step = 1 is the identity.  The caller ORs the raw words
+// by the divisor's IMAD.HI plus shifts (DV: 0 identity for step 1, 1 multiply-high + shift,
+// 2 the add variant; a compile-time choice, so no per-sample select).  The caller ORs the raw words
 // of every int4 into neg: a negative sample (outside the documented [0, 2^31)) sets its sign
 // bit, is then counted exactly and voids the outputs.
-template <bool IDENT, int LR, typename S1>
+template <int DV, int LR, typename S1>
 __device__ __forceinline__ void sample(const Lane& L, int32_t d, S1& s1, uint64_t& s2) {
   const uint32_t x = (uint32_t)d + L.xoff;
   uint32_t q;
-  if (IDENT) {
+  if (DV == 0) {  // step 1: the identity
     q = x;
-  } else {
+  } else if (DV == 1) {  // multiply-high and shift
+    q = __umulhi(x, L.dm) >> L.dsh;
+  } else {  // the add variant of the divisor
     const uint32_t t = __umulhi(x, L.dm);
-    q = L.dadd ? ((((x - t) >> 1) + t) >> L.dsh) : (t >> L.dsh);
+    q = (((x - t) >> 1) + t) >> L.dsh;
   }
   const uint32_t b = min(q, L.K);
   const uint32_t addr = L.base + b * (8 * LR);
@@ -123,7 +126,7 @@ __device__ __forceinline__ Lane make_lane(const FitArgs& a, uint32_t* hsm, int l
 
 // One work piece: samples [beg, end) of one tool -> zeroed CTA histogram -> flush into the
 // tool's row and the pooled row F of the accumulator.
-template <bool IDENT, bool FAST32, int LR>
+template <int DV, bool FAST32, int LR>
 __device__ __forceinline__ void hist_piece(const FitArgs& a, const AccView& acc, const Lane& L,
                                            uint32_t* hsm, unsigned long long (*red)[3], int tool,
                                            int64_t beg, int64_t end) {
@@ -138,8 +141,8 @@ __device__ __forceinline__ void hist_piece(const FitArgs& a, const AccView& acc,
   if (va > end) va = end;
   const int64_t vb = va + ((end - va) & ~(int64_t)3);
   if (tid < 32) {  // scalar head and tail (< 4 samples each)
-    if (beg + lane < va) { const int32_t d = __ldg(&a.dur[beg + lane]); neg |= d; sample<IDENT, LR>(L, d, s1, s2); }
-    if (vb + lane < end) { const int32_t d = __ldg(&a.dur[vb + lane]); neg |= d; sample<IDENT, LR>(L, d, s1, s2); }
+    if (beg + lane < va) { const int32_t d = __ldg(&a.dur[beg + lane]); neg |= d; sample<DV, LR>(L, d, s1, s2); }
+    if (vb + lane < end) { const int32_t d = __ldg(&a.dur[vb + lane]); neg |= d; sample<DV, LR>(L, d, s1, s2); }
   }
   const int4* v = (const int4*)(a.dur + va);
   const int64_t nv = (vb - va) >> 2;
@@ -148,15 +151,15 @@ __device__ __forceinline__ void hist_piece(const FitArgs& a, const AccView& acc,
   auto run4 = [&](const int4& x) {
     neg |= (x.x | x.y) | (x.z | x.w);
     if (FAST32) {
-      sample<IDENT, LR>(L, x.x, s1w, s2);
-      sample<IDENT, LR>(L, x.y, s1w, q1);
-      sample<IDENT, LR>(L, x.z, s1w, q2);
-      sample<IDENT, LR>(L, x.w, s1w, q3);
+      sample<DV, LR>(L, x.x, s1w, s2);
+      sample<DV, LR>(L, x.y, s1w, q1);
+      sample<DV, LR>(L, x.z, s1w, q2);
+      sample<DV, LR>(L, x.w, s1w, q3);
     } else {
-      sample<IDENT, LR>(L, x.x, s1, s2);
-      sample<IDENT, LR>(L, x.y, s1, q1);
-      sample<IDENT, LR>(L, x.z, s1, q2);
-      sample<IDENT, LR>(L, x.w, s1, q3);
+      sample<DV, LR>(L, x.x, s1, s2);
+      sample<DV, LR>(L, x.y, s1, q1);
+      sample<DV, LR>(L, x.z, s1, q2);
+      sample<DV, LR>(L, x.w, s1, q3);
     }
   };
   int64_t i = tid;
@@ -240,7 +243,7 @@ __device__ __forceinline__ void hist_piece(const FitArgs& a, const AccView& acc,
 // (segment f = physical samples [seg_lo[f], seg_hi[f]), virtual offset voff[f]); boundaries are
 // 4-aligned in the virtual order (equal to the physical one for a whole CSR array, where only
 // tool boundaries have scalar heads/tails).  A CTA zeroes and flushes its histogram about once.
-template <bool IDENT, bool FAST32, int LR>
+template <int DV, bool FAST32, int LR>
 __device__ __forceinline__ void hist_phase(const FitArgs& a, const AccView& acc, uint32_t* hsm,
                                            unsigned long long (*red)[3]) {
   const Lane L = make_lane(a, hsm, LR);
@@ -261,7 +264,7 @@ __device__ __forceinline__ void hist_phase(const FitArgs& a, const AccView& acc,
     const int64_t p1 = a.seg_lo[tool] + (vend - a.voff[tool]);
     while (p0 < p1) {
       const int64_t e = min(p1, p0 + a.ch);
-      hist_piece<IDENT, FAST32, LR>(a, acc, L, hsm, red, tool, p0, e);
+      hist_piece<DV, FAST32, LR>(a, acc, L, hsm, red, tool, p0, e);
       p0 = e;
     }
     lo = vend;
@@ -294,49 +297,80 @@ __device__ __forceinline__ void cost_vc(const ct_cost_params& cp, int j, i128_t&
   C = (i128_t)cp.c_pin_ps * ceil_div_i64(cp.ctx_tokens[j], cp.bs);
 }
 
-// One warp item of phase 2.  Items [0, (F+1) J): the argmax of n U(k) for (row, j).  The warp
-// reads the row's buckets itself in rounds of 32 consecutive buckets (lane l: bucket 32 r + l,
-// coalesced; up to FR rounds of loads in flight at once), prefix-sums each round with a warp
-// scan plus the running carry (no block barrier), and evaluates n U(k) = V_j cnt_le(k) -
-// C_j (sum_le(k) + tau_k (n - cnt_le(k))) in 128-bit integers; the smallest maximiser wins
-// (U(0) = 0: no pin).  A tool with fewer than N samples takes the pooled row's
-// argmax (PAPER.md:492-494 ladder).
-// Items [(F+1) J, (F+1) (J+1)): the row's statistics and CalcTTL.
-constexpr int FR = 8;  // rounds of bucket loads in flight (K <= 256: every round)
+// Phase 2, one CTA per (tool row, group of FW turn buckets), plus CTAs for the statistics and
+// CalcTTL of every row (one thread per row).  In an argmax CTA warp w first
+// prefix-sums bucket rounds w, w + FW, ... (round q = buckets 32 q .. 32 q + 31, coalesced
+// loads, a warp scan each); the round totals through shared memory give every bucket's
+// cnt_le(k), sum_le(k), kept in shared memory.  Then warp w takes turn bucket j = FW jg + w and
+// evaluates n U(k) = V_j cnt_le(k) - C_j (sum_le(k) + tau_k (n - cnt_le(k))) in 128-bit
+// integers over every k (lane-strided), keeps the smallest maximiser (U(0) = 0: no pin,
+// PAPER.md:633), and one warp reduction gives tau*.  A tool with fewer than N samples takes the
+// pooled row's argmax (PAPER.md:492-494 ladder).
+constexpr int MAX_ROUNDS = (CT_MAX_K + 31) / 32;
 
-__device__ __forceinline__ int row_argmax(const unsigned long long* hc, const unsigned long long* hs,
-                                          int K, uint64_t ntot, i128_t V, i128_t C, int64_t step,
-                                          int lane) {
-  uint64_t carry_c = 0, carry_s = 0;
-  i128_t best = 0;
-  int bk = 0;
-  for (int r0 = 0; r0 * 32 < K; r0 += FR) {
-    uint64_t xc[FR], xs[FR];
+__device__ __forceinline__ void argmax_cta(const ScanArgs& a, int row, int jg, unsigned long long* pre) {
+  __shared__ unsigned long long tot[2][MAX_ROUNDS];
+  const int K = a.K, F = a.F, J = a.J, K1 = K + 1;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const AccView acc = acc_view(const_cast<unsigned long long*>(a.acc), F, K);
+  const unsigned long long n_bad = *acc.invalid;
+  const uint64_t n_row = acc.stat[row * 6];
+  const int src = (row != F && n_row < (uint64_t)a.est.n_min) ? F : row;
+  const int j = jg * FW + warp;
+  i128_t V = 0, C = 0;
+  if (j < J) cost_vc(a.cost, j, V, C);
+  const unsigned long long* hc = acc.hcnt + (int64_t)src * K1;
+  const unsigned long long* hs = acc.hsum + (int64_t)src * K1;
+  const int rounds = (K + 31) >> 5;
+  constexpr int RW = MAX_ROUNDS / FW;  // rounds per warp at most
+  uint64_t ic[RW], is[RW];
 #pragma unroll
-    for (int q = 0; q < FR; ++q) {
-      const int k = 32 * (r0 + q) + lane;
-      xc[q] = k < K ? hc[k] : 0;
-      xs[q] = k < K ? hs[k] : 0;
-    }
+  for (int i = 0; i < RW; ++i) {  // loads of every round of this warp in flight together
+    const int k = 32 * (warp + FW * i) + lane;
+    ic[i] = k < K ? hc[k] : 0;
+    is[i] = k < K ? hs[k] : 0;
+  }
+  const uint64_t over = hc[K];
 #pragma unroll
-    for (int q = 0; q < FR; ++q) {
-      if (32 * (r0 + q) >= K) break;
-      uint64_t ic = xc[q], is = xs[q];
+  for (int i = 0; i < RW; ++i) {
+    const int q = warp + FW * i;
+    if (q < rounds) {
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
-        const uint64_t tc = __shfl_up_sync(FULL_MASK, ic, o), ts = __shfl_up_sync(FULL_MASK, is, o);
-        if (lane >= o) { ic += tc; is += ts; }
+        const uint64_t tc = __shfl_up_sync(FULL_MASK, ic[i], o), ts = __shfl_up_sync(FULL_MASK, is[i], o);
+        if (lane >= o) { ic[i] += tc; is[i] += ts; }
       }
-      const uint64_t cc = carry_c + ic, cs = carry_s + is;  // cnt_le(k), sum_le(k)
-      const int k = 32 * (r0 + q) + lane;
-      if (k >= 1 && k < K) {
-        const i128_t tau = (i128_t)k * step;
-        const i128_t U = V * (i128_t)cc - C * ((i128_t)cs + tau * (i128_t)(ntot - cc));
-        if (U > best) { best = U; bk = k; }  // per lane k increases: > keeps the smallest
-      }
-      carry_c += __shfl_sync(FULL_MASK, ic, 31);
-      carry_s += __shfl_sync(FULL_MASK, is, 31);
+      if (lane == 31) { tot[0][q] = ic[i]; tot[1][q] = is[i]; }
     }
+  }
+  __syncthreads();
+  uint64_t carry_c = 0, carry_s = 0;
+  int done = 0;
+#pragma unroll
+  for (int i = 0; i < RW; ++i) {
+    const int q = warp + FW * i;
+    if (q < rounds) {
+      for (; done < q; ++done) { carry_c += tot[0][done]; carry_s += tot[1][done]; }
+      const int k = 32 * q + lane;
+      if (k < K) {
+        pre[2 * k] = carry_c + ic[i];      // cnt_le(k)
+        pre[2 * k + 1] = carry_s + is[i];  // sum_le(k)
+      }
+    }
+  }
+  uint64_t ntot = over;
+  for (int q = 0; q < rounds; ++q) ntot += tot[0][q];
+  __syncthreads();
+  if (j >= J) return;
+  const int64_t step = a.cost.grid_step_us;
+  i128_t best = 0;
+  int bk = 0;
+  for (int k = lane; k < K; k += 32) {
+    if (k == 0) continue;
+    const uint64_t cc = pre[2 * k], cs = pre[2 * k + 1];
+    const i128_t tau = (i128_t)k * step;
+    const i128_t U = V * (i128_t)cc - C * ((i128_t)cs + tau * (i128_t)(ntot - cc));
+    if (U > best) { best = U; bk = k; }  // k increases per lane: > keeps the smallest
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -346,50 +380,31 @@ __device__ __forceinline__ int row_argmax(const unsigned long long* hc, const un
     const i128_t ob = (i128_t)(((u128_t)hi << 64) | lo);
     if (ob > best || (ob == best && ok < bk)) { best = ob; bk = ok; }
   }
-  return bk;
+  if (lane == 0) a.ttl_argmax[(int64_t)row * J + j] = n_bad ? CT_TTL_INVALID : (int64_t)bk * step;
 }
 
-__device__ __forceinline__ void finish_warp(const ScanArgs& a, int item, int lane) {
-  const int K = a.K, F = a.F, J = a.J, K1 = K + 1;
-  const AccView acc = acc_view(const_cast<unsigned long long*>(a.acc), F, K);
+__device__ __forceinline__ void ttl_row(const ScanArgs& a, int row) {
+  const AccView acc = acc_view(const_cast<unsigned long long*>(a.acc), a.F, a.K);
   const unsigned long long n_bad = *acc.invalid;
-  if (item >= (F + 1) * J) {  // statistics + CalcTTL of one row
-    const int row = item - (F + 1) * J;
-    if (lane != 0) return;
-    if (n_bad) {  // samples outside [0, 2^31): no table (CT_TTL_INVALID everywhere)
-      a.ttl_paper[row] = CT_TTL_INVALID;
-      if (a.stats_out)
-        for (int q = 0; q < 4; ++q) a.stats_out[row * 4 + q] = 0;
-      if (row == 0 && a.n_invalid) *a.n_invalid = (int64_t)n_bad;
-      return;
-    }
-    const Stat f = row_stat(acc.stat, row), g = row_stat(acc.stat, F);
-    a.ttl_paper[row] = calc_ttl(g, f, a.est, a.cost.avg_turns_den, a.cost.avg_turns_num);
-    if (a.stats_out) {
-      a.stats_out[row * 4 + 0] = f.n;
-      a.stats_out[row * 4 + 1] = f.s1;
-      a.stats_out[row * 4 + 2] = (int64_t)f.s2lo;
-      a.stats_out[row * 4 + 3] = (int64_t)f.s2hi;
-    }
-    if (row == 0 && a.n_invalid) *a.n_invalid = 0;
+  if (n_bad) {  // samples outside [0, 2^31): no table (CT_TTL_INVALID everywhere)
+    a.ttl_paper[row] = CT_TTL_INVALID;
+    if (a.stats_out)
+      for (int q = 0; q < 4; ++q) a.stats_out[row * 4 + q] = 0;
+    if (row == 0 && a.n_invalid) *a.n_invalid = (int64_t)n_bad;
     return;
   }
-  const int row = item / J, j = item % J;
-  i128_t V, C;
-  cost_vc(a.cost, j, V, C);
-  // n_f (the statistics' sample count, overflow bucket included) and the row's buckets are
-  // loaded together: a tool with n_f < N then redoes the argmax on the pooled row
-  const uint64_t n_row = acc.stat[row * 6];
-  int bk = row_argmax(acc.hcnt + (int64_t)row * K1, acc.hsum + (int64_t)row * K1, K, n_row, V, C,
-                      a.cost.grid_step_us, lane);
-  if (row != F && n_row < (uint64_t)a.est.n_min)
-    bk = row_argmax(acc.hcnt + (int64_t)F * K1, acc.hsum + (int64_t)F * K1, K, acc.stat[F * 6], V,
-                    C, a.cost.grid_step_us, lane);
-  if (lane == 0)
-    a.ttl_argmax[(int64_t)row * J + j] = n_bad ? CT_TTL_INVALID : (int64_t)bk * a.cost.grid_step_us;
+  const Stat f = row_stat(acc.stat, row), g = row_stat(acc.stat, a.F);
+  a.ttl_paper[row] = calc_ttl(g, f, a.est, a.cost.avg_turns_den, a.cost.avg_turns_num);
+  if (a.stats_out) {
+    a.stats_out[row * 4 + 0] = f.n;
+    a.stats_out[row * 4 + 1] = f.s1;
+    a.stats_out[row * 4 + 2] = (int64_t)f.s2lo;
+    a.stats_out[row * 4 + 3] = (int64_t)f.s2hi;
+  }
+  if (row == 0 && a.n_invalid) *a.n_invalid = 0;
 }
 
-__device__ __forceinline__ int finish_items(const ScanArgs& a) { return (a.F + 1) * (a.J + 1); }
+__host__ __device__ __forceinline__ int finish_argmax_ctas(int F, int J) { return (F + 1) * ((J + FW - 1) / FW); }
 
 // ---------------------------------------------------------------------------------------------
 // The histogram pass.  It first lets the finish kernel launch (programmatic dependent launch:
@@ -397,7 +412,7 @@ __device__ __forceinline__ int finish_items(const ScanArgs& a) { return (a.F + 1
 // griddepcontrol.wait for its completion, so no launch gap sits between the two), zeroes the
 // other half of the context's double-buffered accumulator for the next call (no memset), then
 // streams its range.
-template <bool IDENT, bool FAST32, int LR>
+template <int DV, bool FAST32, int LR>
 __global__ void __launch_bounds__(FT, 2) fit_hist_kernel(FitArgs a) {
   extern __shared__ __align__(16) uint32_t hsm[];
   __shared__ unsigned long long red[FW][3];
@@ -405,13 +420,20 @@ __global__ void __launch_bounds__(FT, 2) fit_hist_kernel(FitArgs a) {
   const int64_t nt = (int64_t)gridDim.x * FT;
   for (int64_t i = (int64_t)blockIdx.x * FT + threadIdx.x; i < a.zero_words; i += nt) a.zero[i] = 0;
   const AccView acc = acc_view(a.acc, a.F, a.K);
-  hist_phase<IDENT, FAST32, LR>(a, acc, hsm, red);
+  hist_phase<DV, FAST32, LR>(a, acc, hsm, red);
 }
 
 __global__ void __launch_bounds__(FT) fit_finish_kernel(ScanArgs s) {
+  extern __shared__ __align__(16) unsigned long long pre[];  // [K][2] cnt_le, sum_le
   asm volatile("griddepcontrol.wait;" ::: "memory");  // the histogram grid is complete
-  const int it = blockIdx.x * FW + (threadIdx.x >> 5);
-  if (it < finish_items(s)) finish_warp(s, it, threadIdx.x & 31);
+  const int na = finish_argmax_ctas(s.F, s.J);
+  if ((int)blockIdx.x < na) {
+    const int jgs = (s.J + FW - 1) / FW;
+    argmax_cta(s, blockIdx.x / jgs, blockIdx.x % jgs, pre);
+  } else {
+    const int row = ((int)blockIdx.x - na) * FT + threadIdx.x;
+    if (row <= s.F) ttl_row(s, row);
+  }
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -507,17 +529,19 @@ __global__ void __launch_bounds__(FT) fit_pairs_kernel(FitArgs a) {
 }
 
 // ---------------------------------------------------------------------------------------------
-static void* hist_fn(bool ident, bool fast32, int lr) {
-  if (lr == 32) {
-    if (ident) return fast32 ? (void*)fit_hist_kernel<true, true, 32> : (void*)fit_hist_kernel<true, false, 32>;
-    return fast32 ? (void*)fit_hist_kernel<false, true, 32> : (void*)fit_hist_kernel<false, false, 32>;
-  }
-  if (ident) return fast32 ? (void*)fit_hist_kernel<true, true, 16> : (void*)fit_hist_kernel<true, false, 16>;
-  return fast32 ? (void*)fit_hist_kernel<false, true, 16> : (void*)fit_hist_kernel<false, false, 16>;
+template <int DV>
+static void* hist_fn_dv(bool fast32, int lr) {
+  if (lr == 32) return fast32 ? (void*)fit_hist_kernel<DV, true, 32> : (void*)fit_hist_kernel<DV, false, 32>;
+  return fast32 ? (void*)fit_hist_kernel<DV, true, 16> : (void*)fit_hist_kernel<DV, false, 16>;
+}
+
+static void* hist_fn(int dv, bool fast32, int lr) {
+  return dv == 0 ? hist_fn_dv<0>(fast32, lr) : dv == 1 ? hist_fn_dv<1>(fast32, lr) : hist_fn_dv<2>(fast32, lr);
 }
 
 static void* pick_hist(const FitArgs& a, const FitPlan& p) {
-  return p.pairs ? (void*)fit_pairs_kernel : hist_fn(a.step == 1, a.b_us < (1ll << 26), p.lr);
+  const int dv = a.step == 1 ? 0 : a.div_add ? 2 : 1;
+  return p.pairs ? (void*)fit_pairs_kernel : hist_fn(dv, a.b_us < (1ll << 26), p.lr);
 }
 
 int fit_hist_occupancy(const FitArgs& a, const FitPlan& p) {
@@ -536,10 +560,15 @@ cudaError_t launch_fit_hist(const FitArgs& a, const FitPlan& p, int grid, cudaSt
 // The finish kernel as a programmatic dependent launch of the histogram pass before it on the
 // stream (its griddepcontrol.wait orders it after that grid's completion and memory flush).
 cudaError_t launch_fit_finish(const ScanArgs& s, cudaStream_t st) {
+  if (16 * s.K > 48 * 1024) {
+    const cudaError_t e =
+        cudaFuncSetAttribute(fit_finish_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 16 * s.K);
+    if (e != cudaSuccess) return e;
+  }
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(((s.F + 1) * (s.J + 1) + FW - 1) / FW);
+  cfg.gridDim = dim3(finish_argmax_ctas(s.F, s.J) + (s.F + 1 + FT - 1) / FT);
   cfg.blockDim = dim3(FT);
-  cfg.dynamicSmemBytes = 0;
+  cfg.dynamicSmemBytes = 16 * (size_t)s.K;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;

@@ -1,0 +1,7 @@
+python tools/prof_kernels.py fit 28 > gpurun_out/g12_fit.txt 2>&1
+python tools/prof_kernels.py fit 28 >> gpurun_out/g12_fit.txt 2>&1
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/g12_fit_launches.csv python tools/prof_kernels.py fit 28 > /dev/null 2>&1
+python -m pytest tests/test_gpu_fit.py tests/test_estimator_abi.py -m gpu -q > gpurun_out/g12_pytest.txt 2>&1; echo rc=$? >> gpurun_out/g12_pytest.txt
+python -m pytest tests/test_gpu_parity.py -m gpu -q -k fit >> gpurun_out/g12_pytest.txt 2>&1; echo rc=$? >> gpurun_out/g12_pytest.txt
+python -m pytest tests/test_gpu_fullsize.py -m gpu -q -k "fit_full or cfg4 or cfg2" >> gpurun_out/g12_pytest.txt 2>&1; echo rc=$? >> gpurun_out/g12_pytest.txt
+python tools/prof_kernels.py replay cfg2 4096 > gpurun_out/g12_cfg2.txt 2>&1
