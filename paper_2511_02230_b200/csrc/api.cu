@@ -313,6 +313,14 @@ int ct_simulate_batch_ex(ct_ctx* c, const ct_trace_set* tr, const ct_sweep* sw,
   for (size_t i = 0; i < n_kv; ++i) kv_max = std::max<int64_t>(kv_max, sw->kv_blocks[i]);
   const i128 d_max = ((i128)E.c0_ps + (i128)E.c_kv_ps * E.bs * kv_max + 999999) / 1000000;
   a.d32 = d_max < ((i128)1 << 31) ? 1 : 0;
+  {  // 32-bit iteration duration when c_kv bs max(kv) + 1e6 < 2^32 (replay.cu iter_us_kv32)
+    const i128 u = (i128)E.c_kv_ps * E.bs;
+    const i128 q = ((i128)E.c0_ps + 999999) / 1000000;
+    a.kv32 = (u * kv_max + 1000000 < ((i128)1 << 32) && q < ((i128)1 << 31)) ? 1 : 0;
+    a.kv_unit = a.kv32 ? (uint32_t)u : 0;
+    a.c0q = a.kv32 ? (uint32_t)q : 0;
+    a.c0r = a.kv32 ? (uint32_t)(q * 1000000 - E.c0_ps) : 0;
+  }
   int n_fast = 0;
   if (a.d32)
     for (size_t i = 0; i < n_pol; ++i) n_fast += ct::fast_policy(sw->policies[i], E) ? 1 : 0;

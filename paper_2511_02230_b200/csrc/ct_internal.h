@@ -31,6 +31,9 @@ struct ReplayArgs {
   int64_t* fb_list;   // MODE 4: replicas handed to the 64-bit kernel (horizon, bubble output)
   unsigned long long* fb_count;
   const unsigned long long* err;  // trace check result (validate.cu): err[0] != 0 = invalid input
+  int kv32;            // c_kv bs max(kv) + 1e6 < 2^32: 32-bit iteration duration (iter_us_kv32)
+  uint32_t kv_unit;    // c_kv bs (ps per resident block)
+  uint32_t c0q, c0r;   // c0 = c0q 1e6 - c0r, 0 <= c0r < 1e6
 };
 
 // Trace-set check (validate.cu).  Bits of err[0]:

@@ -579,6 +579,18 @@ __device__ __forceinline__ int64_t calc_ttl_cached(const Stat* stats, TtlCache* 
   return ttl;
 }
 
+// Duration (µs) of a no-prefill iteration with kv resident blocks, ceil((c0 + c_kv bs kv) / 1e6),
+// for the 32-bit kernels.  When c_kv bs max(kv) + 1e6 < 2^32 (host-checked, ReplayArgs.kv32)
+// it is c0q + ceil((c_kv bs kv - c0r) / 1e6) (0 when that is negative) with c0 = c0q 1e6 - c0r,
+// 0 <= c0r < 1e6: one 32-bit constant division instead of the 64-bit one.
+__device__ __forceinline__ uint32_t iter_us_kv32(const ReplayArgs& a, uint32_t kv) {
+  if (a.kv32) {
+    const uint32_t x = a.kv_unit * kv;
+    return a.c0q + (x > a.c0r ? (x - a.c0r + 999999u) / 1000000u : 0u);
+  }
+  return (uint32_t)ceil_ps_to_us((uint64_t)(a.eng.c0_ps + a.eng.c_kv_ps * a.eng.bs * (int64_t)kv));
+}
+
 constexpr uint32_t T32_INF = 0xFFFFFFFFu;
 constexpr uint32_t T32_LIM = 0xFFFFFFF0u;
 
@@ -674,7 +686,6 @@ __device__ __forceinline__ bool replay_one_t32(const ReplayArgs& a, int64_t r, S
   // iteration budget as a 32-bit bound (n_it < 2^32 on this path)
   const uint32_t it_cap = E.max_iters >= (int64_t)T32_INF ? T32_INF : (uint32_t)E.max_iters;
   int32_t kv_at = -1;
-  int64_t base_ps = 0;
   uint32_t d_cur = 0;
   float rd_cur = 0.0f;
   // evict(v): free its GPU blocks; DRAM write-through when the tier is on (R18).  Uniform.
@@ -926,11 +937,12 @@ __device__ __forceinline__ bool replay_one_t32(const ReplayArgs& a, int64_t r, S
     if (n_run > 0) {
       if (kv_sum != kv_at) {
         kv_at = kv_sum;
-        base_ps = E.c0_ps + E.c_kv_ps * E.bs * kv_sum;
-        d_cur = (uint32_t)ceil_ps_to_us((uint64_t)base_ps);  // < 2^31 (host-checked)
+        d_cur = iter_us_kv32(a, (uint32_t)kv_sum);  // < 2^31 (host-checked)
         rd_cur = rcp_approx((float)d_cur);  // estimate only: macro_iters32 corrects
       }
-      const int64_t dur1 = pf > 0 ? ceil_ps_to_us((uint64_t)(base_ps + E.c_pf_ps * pf)) : d_cur;
+      const int64_t dur1 = pf > 0 ? ceil_ps_to_us((uint64_t)(E.c0_ps + E.c_kv_ps * E.bs * kv_sum +
+                                                             E.c_pf_ps * pf))
+                                  : d_cur;
       pf = 0;
       int64_t k = 1;
       if (stable) {
@@ -1918,7 +1930,7 @@ __device__ __forceinline__ bool replay_one_ns32(const ReplayArgs& a, int64_t r,
   int n_run = 0;
   int64_t kv_sum = 0, pf = 0;
   int status = CT_R_OK;
-  int64_t kv_at = -1, base_ps = 0;
+  int64_t kv_at = -1;
   uint32_t d_cur = 0;
   float rd_cur = 0.0f;
   int64_t accv = 0;  // lane k holds summary counter k (ACC_*)
@@ -2155,11 +2167,12 @@ __device__ __forceinline__ bool replay_one_ns32(const ReplayArgs& a, int64_t r,
     if (n_run > 0) {
       if (kv_sum != kv_at) {
         kv_at = kv_sum;
-        base_ps = E.c0_ps + E.c_kv_ps * bs * kv_sum;
-        d_cur = (uint32_t)ceil_ps_to_us((uint64_t)base_ps);  // < 2^31 (host-checked)
+        d_cur = iter_us_kv32(a, (uint32_t)kv_sum);  // < 2^31 (host-checked)
         rd_cur = rcp_approx((float)d_cur);  // estimate only: macro_iters32 corrects
       }
-      const int64_t dur1 = pf > 0 ? ceil_ps_to_us((uint64_t)(base_ps + E.c_pf_ps * pf)) : d_cur;
+      const int64_t dur1 = pf > 0 ? ceil_ps_to_us((uint64_t)(E.c0_ps + E.c_kv_ps * bs * kv_sum +
+                                                             E.c_pf_ps * pf))
+                                  : d_cur;
       pf = 0;
       int64_t k = 1;
       if (stable) {
@@ -2331,7 +2344,7 @@ __global__ void __launch_bounds__(128, MINB) replay_kernel(ReplayArgs a) {
 #define CT_REPLAY_MINB_GRID 10
 #endif
 #ifndef CT_REPLAY_MINB_EXT
-#define CT_REPLAY_MINB_EXT 8  // extended class (MODE 6)
+#define CT_REPLAY_MINB_EXT 7  // extended class (MODE 6): 72 registers, 28 warps/SM, measured best (cfg4)
 #endif
 
 #ifndef NS32_MINB
