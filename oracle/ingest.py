@@ -221,10 +221,13 @@ def load_trace_jsonl(path: str, fmt: str = "auto", ctx_window: int = 0, known_to
             raise TraceError(ln, "program_id duplicate")
         ids.add(key)
         at = rec.get("arrival_time_s")
-        if not _is_num(at) or _us(at) < 0 or _us(at) >= 2**62:
+        # arrivals replay as recorded at gap 2^20 (R34): the replay needs arr_q * gap < 2^62
+        if not _is_num(at) or _us(at) < 0 or _us(at) >= 2**42:
             raise TraceError(ln, "arrival_time_s")
         turns = rec.get("turns")
         if not isinstance(turns, list) or not turns:
+            raise TraceError(ln, "turns")
+        if len(turns) > 65536:  # CT_MAX_TURNS
             raise TraceError(ln, "turns")
         out, cum = [], 0
         for k, tv in enumerate(turns):
@@ -237,6 +240,8 @@ def load_trace_jsonl(path: str, fmt: str = "auto", ctx_window: int = 0, known_to
             if not _is_int(dec) or not 1 <= dec < 2**31:
                 raise TraceError(ln, "decode_tokens")
             cum += nw + dec
+            if cum > 2**30:  # CT_MAX_CONTEXT
+                raise TraceError(ln, "context above 2^30 tokens")
             if ctx_window > 0 and cum > ctx_window:
                 raise TraceError(ln, "context window")
             if last:

@@ -320,6 +320,9 @@ int ct_simulate_batch_ex(ct_ctx* c, const ct_trace_set* tr, const ct_sweep* sw,
     a.kv_unit = a.kv32 ? (uint32_t)u : 0;
     a.c0q = a.kv32 ? (uint32_t)q : 0;
     a.c0r = a.kv32 ? (uint32_t)(q * 1000000 - E.c0_ps) : 0;
+    a.pf_q = (uint32_t)(E.c_pf_ps / 1000000);  // c_pf < 2^40: pf_q < 2^20
+    a.pf_r = (uint32_t)(E.c_pf_ps % 1000000);
+    a.pf32 = a.pf_r == 0 ? 0x7fffffffu : (uint32_t)(((1ull << 32) - 1000001ull) / a.pf_r);
   }
   int n_fast = 0;
   if (a.d32)

@@ -34,6 +34,8 @@ struct ReplayArgs {
   int kv32;            // c_kv bs max(kv) + 1e6 < 2^32: 32-bit iteration duration (iter_us_kv32)
   uint32_t kv_unit;    // c_kv bs (ps per resident block)
   uint32_t c0q, c0r;   // c0 = c0q 1e6 - c0r, 0 <= c0r < 1e6
+  uint32_t pf_q, pf_r; // c_pf = pf_q 1e6 + pf_r, 0 <= pf_r < 1e6
+  uint32_t pf32;       // prefills below pf32 tokens take the 32-bit path (pf_r pf + 1e6 < 2^32)
 };
 
 // Trace-set check (validate.cu).  Bits of err[0]:

@@ -518,11 +518,15 @@ int ct_load_trace_jsonl(const char* path, int32_t format, int64_t ctx_window, ch
       const JVal* at = rec.get("arrival_time_s");
       LProg pr;
       pr.line = ln;
-      if (!at || at->k != JVal::NUM || !decimal_to_us(at->s, pr.arr) || pr.arr < 0)
+      // arr_q = arrival µs replays at gap_us = 2^20, so arrivals stay below 2^42 µs
+      // (ct_simulate_batch: arr_q x gap < 2^62)
+      if (!at || at->k != JVal::NUM || !decimal_to_us(at->s, pr.arr) || pr.arr < 0 ||
+          pr.arr >= (1ll << 42))
         return fail_line(counts, ln, "arrival_time_s: missing, negative or out of range");
       const JVal* ts = rec.get("turns");
       if (!ts || ts->k != JVal::ARR || ts->a.empty())
         return fail_line(counts, ln, "turns: missing, not a list or empty");
+      if (ts->a.size() > CT_MAX_TURNS) return fail_line(counts, ln, "turns: more than CT_MAX_TURNS");
       int64_t cum = 0;
       for (size_t k = 0; k < ts->a.size(); ++k) {
         const JVal& tv = ts->a[k];
@@ -538,6 +542,8 @@ int ct_load_trace_jsonl(const char* path, int32_t format, int64_t ctx_window, ch
         if (!f || !json_int(*f, 1, kI32, x)) return fail_line(counts, ln, tk + "decode_tokens: missing or not an integer >= 1");
         t.dec = (int32_t)x;
         cum += (int64_t)t.nw + t.dec;
+        if (cum > CT_MAX_CONTEXT)
+          return fail_line(counts, ln, tk + "new_prompt_tokens: total context above CT_MAX_CONTEXT");
         if (ctx_window > 0 && cum > ctx_window)
           return fail_line(counts, ln, tk + "new_prompt_tokens: cumulative context exceeds the context window");
         const JVal* tn = tv.get("tool_name");

@@ -582,13 +582,31 @@ __device__ __forceinline__ int64_t calc_ttl_cached(const Stat* stats, TtlCache* 
 // Duration (µs) of a no-prefill iteration with kv resident blocks, ceil((c0 + c_kv bs kv) / 1e6),
 // for the 32-bit kernels.  When c_kv bs max(kv) + 1e6 < 2^32 (host-checked, ReplayArgs.kv32)
 // it is c0q + ceil((c_kv bs kv - c0r) / 1e6) (0 when that is negative) with c0 = c0q 1e6 - c0r,
-// 0 <= c0r < 1e6: one 32-bit constant division instead of the 64-bit one.
-__device__ __forceinline__ uint32_t iter_us_kv32(const ReplayArgs& a, uint32_t kv) {
+// 0 <= c0r < 1e6: one 32-bit constant division instead of the 64-bit one.  *rb receives
+// d 1e6 - (c0 + c_kv bs kv), in [0, 1e6), for iter_us_prefill.
+__device__ __forceinline__ uint32_t iter_us_kv32(const ReplayArgs& a, uint32_t kv, uint32_t* rb) {
   if (a.kv32) {
     const uint32_t x = a.kv_unit * kv;
-    return a.c0q + (x > a.c0r ? (x - a.c0r + 999999u) / 1000000u : 0u);
+    const uint32_t e = x > a.c0r ? (x - a.c0r + 999999u) / 1000000u : 0u;
+    *rb = e * 1000000u + a.c0r - x;
+    return a.c0q + e;
   }
+  *rb = 0;
   return (uint32_t)ceil_ps_to_us((uint64_t)(a.eng.c0_ps + a.eng.c_kv_ps * a.eng.bs * (int64_t)kv));
+}
+
+// Duration (µs) of an iteration that also prefills pf tokens: ceil((c0 + c_kv bs kv + c_pf pf)
+// / 1e6).  With c_pf = pfq 1e6 + pfr and d, rb from iter_us_kv32 it is d + pfq pf +
+// ceil((pfr pf - rb) / 1e6) (0 when negative), one 32-bit division while pfr pf + 1e6 < 2^32
+// (pf < a.pf32); otherwise the 64-bit sum.
+__device__ __forceinline__ int64_t iter_us_prefill(const ReplayArgs& a, uint32_t d, uint32_t rb,
+                                                   uint32_t kv, int64_t pf) {
+  if (a.kv32 && pf < (int64_t)a.pf32) {
+    const uint32_t y = a.pf_r * (uint32_t)pf;
+    return (int64_t)d + (int64_t)a.pf_q * pf + (y > rb ? (y - rb + 999999u) / 1000000u : 0u);
+  }
+  return ceil_ps_to_us((uint64_t)(a.eng.c0_ps + a.eng.c_kv_ps * a.eng.bs * (int64_t)kv +
+                                  a.eng.c_pf_ps * pf));
 }
 
 constexpr uint32_t T32_INF = 0xFFFFFFFFu;
@@ -686,7 +704,7 @@ __device__ __forceinline__ bool replay_one_t32(const ReplayArgs& a, int64_t r, S
   // iteration budget as a 32-bit bound (n_it < 2^32 on this path)
   const uint32_t it_cap = E.max_iters >= (int64_t)T32_INF ? T32_INF : (uint32_t)E.max_iters;
   int32_t kv_at = -1;
-  uint32_t d_cur = 0;
+  uint32_t d_cur = 0, rb_cur = 0;
   float rd_cur = 0.0f;
   // evict(v): free its GPU blocks; DRAM write-through when the tier is on (R18).  Uniform.
   auto evict = [&](int v) {
@@ -937,12 +955,14 @@ __device__ __forceinline__ bool replay_one_t32(const ReplayArgs& a, int64_t r, S
     if (n_run > 0) {
       if (kv_sum != kv_at) {
         kv_at = kv_sum;
-        d_cur = iter_us_kv32(a, (uint32_t)kv_sum);  // < 2^31 (host-checked)
+        d_cur = iter_us_kv32(a, (uint32_t)kv_sum, &rb_cur);  // < 2^31 (host-checked)
         rd_cur = rcp_approx((float)d_cur);  // estimate only: macro_iters32 corrects
       }
-      const int64_t dur1 = pf > 0 ? ceil_ps_to_us((uint64_t)(E.c0_ps + E.c_kv_ps * E.bs * kv_sum +
-                                                             E.c_pf_ps * pf))
-                                  : d_cur;
+      // the TTL-grid kernel (48 registers) measured faster with the plain 64-bit sum
+      const int64_t dur1 =
+          pf <= 0 ? d_cur
+          : STATS ? iter_us_prefill(a, d_cur, rb_cur, (uint32_t)kv_sum, pf)
+                  : ceil_ps_to_us((uint64_t)(E.c0_ps + E.c_kv_ps * E.bs * kv_sum + E.c_pf_ps * pf));
       pf = 0;
       int64_t k = 1;
       if (stable) {
@@ -1931,7 +1951,7 @@ __device__ __forceinline__ bool replay_one_ns32(const ReplayArgs& a, int64_t r,
   int64_t kv_sum = 0, pf = 0;
   int status = CT_R_OK;
   int64_t kv_at = -1;
-  uint32_t d_cur = 0;
+  uint32_t d_cur = 0, rb_cur = 0;
   float rd_cur = 0.0f;
   int64_t accv = 0;  // lane k holds summary counter k (ACC_*)
   auto acc_add = [&](int k, int64_t v) {
@@ -2167,12 +2187,10 @@ __device__ __forceinline__ bool replay_one_ns32(const ReplayArgs& a, int64_t r,
     if (n_run > 0) {
       if (kv_sum != kv_at) {
         kv_at = kv_sum;
-        d_cur = iter_us_kv32(a, (uint32_t)kv_sum);  // < 2^31 (host-checked)
+        d_cur = iter_us_kv32(a, (uint32_t)kv_sum, &rb_cur);  // < 2^31 (host-checked)
         rd_cur = rcp_approx((float)d_cur);  // estimate only: macro_iters32 corrects
       }
-      const int64_t dur1 = pf > 0 ? ceil_ps_to_us((uint64_t)(E.c0_ps + E.c_kv_ps * bs * kv_sum +
-                                                             E.c_pf_ps * pf))
-                                  : d_cur;
+      const int64_t dur1 = pf > 0 ? iter_us_prefill(a, d_cur, rb_cur, (uint32_t)kv_sum, pf) : d_cur;
       pf = 0;
       int64_t k = 1;
       if (stable) {

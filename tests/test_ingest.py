@@ -224,6 +224,25 @@ def test_load_errors_and_tool_table(ct, tmp_path):
         ct.ct_load_trace_jsonl(write(tmp_path, many))
 
 
+def test_load_enforces_the_replay_bounds(ct, tmp_path):
+    """Arrivals replay as recorded at gap_us = 2^20 (R34), so the replay's arr_q * gap < 2^62
+    means arrivals below 2^42 µs; a program's total context is at most 2^30 tokens
+    (CT_MAX_CONTEXT).  The product and the oracle accept and reject the same files."""
+    def rec(arr_us, new=10):
+        return ('{"program_id": 1, "arrival_time_s": %d.%06d, "turns": [{"new_prompt_tokens": %d, '
+                '"decode_tokens": 1}]}' % (arr_us // 10**6, arr_us % 10**6, new))
+    ok = write(tmp_path, [rec(2**42 - 1)])
+    tr, _, _ = ct.ct_load_trace_jsonl(ok)
+    assert int(tr.programs["arr_q"][0]) == 2**42 - 1
+    assert OI.load_trace_jsonl(ok)[0][0][0] == 2**42 - 1
+    for bad in ([rec(2**42)], [rec(0, new=2**30)]):
+        path = write(tmp_path, bad)
+        with pytest.raises(Exception):
+            ct.ct_load_trace_jsonl(path)
+        with pytest.raises(OI.TraceError):
+            OI.load_trace_jsonl(path)
+
+
 @pytest.mark.gpu
 def test_replay_of_a_loaded_trace_matches_oracle(ct, tmp_path):
     """A JSONL trace loaded by the product replays on the GPU exactly as the oracle replays the
