@@ -1,17 +1,19 @@
 """Build libcontinuum.so in-tree for sm_100a (nvcc cross-compiles without a GPU)."""
 from __future__ import annotations
 
+import concurrent.futures
 import glob
 import os
 import subprocess
 import sys
+import tempfile
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 SO = os.path.join(HERE, "libcontinuum.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-std=c++17", "-O3", "-lineinfo", "-gencode", "arch=compute_100a,code=sm_100a",
-         "-Xcompiler", "-fPIC", "-shared"]
+         "-Xcompiler", "-fPIC"]
 
 
 def sources() -> list[str]:
@@ -31,14 +33,30 @@ def up_to_date() -> bool:
     return all(os.path.getmtime(d) <= t for d in deps())
 
 
+def compile_link(srcs: list[str], out: str, extra: list[str] = (), verbose: bool = False) -> None:
+    """nvcc -c every source in parallel (one translation unit per kernel family), then link."""
+    with tempfile.TemporaryDirectory() as tmp:
+        objs, cmds = [], []
+        for src in srcs:
+            obj = os.path.join(tmp, os.path.basename(src) + ".o")
+            objs.append(obj)
+            cmd = [NVCC, *FLAGS, *extra, "-I", os.path.join(ROOT, "include"), "-c", "-o", obj, src]
+            if verbose:
+                cmd.insert(1, "-Xptxas=-v")
+                print(" ".join(cmd), file=sys.stderr)
+            cmds.append(cmd)
+        with concurrent.futures.ThreadPoolExecutor(max(1, os.cpu_count() or 1)) as ex:
+            for rc, cmd in zip(ex.map(subprocess.call, cmds), cmds):
+                if rc != 0:
+                    raise subprocess.CalledProcessError(rc, cmd)
+        subprocess.check_call([NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a",
+                               "-o", out, *objs])
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and up_to_date():
         return SO
-    cmd = [NVCC, *FLAGS, "-I", os.path.join(ROOT, "include"), "-o", SO + ".tmp", *sources()]
-    if verbose:
-        cmd.insert(1, "-Xptxas=-v")
-        print(" ".join(cmd), file=sys.stderr)
-    subprocess.check_call(cmd)
+    compile_link(sources(), SO + ".tmp", verbose=verbose)
     os.replace(SO + ".tmp", SO)
     return SO
 

@@ -32,8 +32,7 @@ def main():
             open(path, "w").write(s.replace(old, new))
         out = os.path.join(ROOT, "tools", "var_%s.so" % name)
         srcs = sorted(os.path.join(src, x) for x in os.listdir(src) if x.endswith((".cu", ".cpp")))
-        subprocess.check_call([B.NVCC, *B.FLAGS, *defs, "-I", os.path.join(ROOT, "include"),
-                               "-o", out, *srcs])
+        B.compile_link(srcs, out, extra=defs)
         print(out)
 
 

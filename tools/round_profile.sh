@@ -25,6 +25,13 @@ done
 cp profiles/ncu_constants.json $OUT/${R}_ncu_constants.json
 python tools/summarize_ncu.py $OUT/${R}_ncu_summary $OUT/${R}_replay_cfg3.ncu-rep $OUT/${R}_replay_cfg2.ncu-rep \
     $OUT/${R}_replay_cfg4.ncu-rep $OUT/${R}_replay_cfg5.ncu-rep $OUT/${R}_fit_hist.ncu-rep > /dev/null 2>&1
+# per-source-line instruction / stall tables, then park the big reports outside gpurun_out/
+# (the copy-back is capped at 64 MiB)
+for w in cfg3 cfg2 cfg4 cfg5; do
+  python tools/ncu_src_lines.py $OUT/${R}_replay_$w.ncu-rep 60 > $OUT/${R}_srclines_$w.txt 2>&1
+done
+python tools/ncu_src_lines.py $OUT/${R}_fit_hist.ncu-rep 40 > $OUT/${R}_srclines_fit.txt 2>&1
+mkdir -p /tmp/ncu_reps && mv $OUT/${R}_replay_*.ncu-rep /tmp/ncu_reps/
 python bench.py > $OUT/${R}_bench.log 2>&1
 tail -1 $OUT/${R}_bench.log > $OUT/${R}_bench.json
 for w in cfg2 cfg4 cfg5; do
