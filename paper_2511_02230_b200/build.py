@@ -22,7 +22,7 @@ def sources() -> list[str]:
 
 
 def deps() -> list[str]:
-    return sources() + sorted(glob.glob(os.path.join(HERE, "csrc", "*.h*"))) + \
+    return sources() + sorted(glob.glob(os.path.join(HERE, "csrc", "*.h")) + glob.glob(os.path.join(HERE, "csrc", "*.cuh"))) + \
         [os.path.join(ROOT, "include", "continuum.h")]
 
 

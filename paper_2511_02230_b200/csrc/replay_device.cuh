@@ -603,6 +603,24 @@ __device__ __forceinline__ int64_t iter_us_prefill(const ReplayArgs& a, uint32_t
 constexpr uint32_t T32_INF = 0xFFFFFFFFu;
 constexpr uint32_t T32_LIM = 0xFFFFFFF0u;
 
+// Macro-step on 32-bit times (replay_one_t32): the first iteration ends at end1; the result is
+// the number j of further iterations of d µs (all identical, no finish before the m1-th), the
+// smallest j <= m1 with end1 + j d >= te (the next external event; T32_INF = none), i.e.
+// min(m1, ceil((te - end1) / d)), 0 when te <= end1.  Same value as macro_iters32 - 1.  Past
+// the test g <= m1 d the quotient is at most m1 (a request's decode tokens), so the float
+// estimate is within one of it and the two integer corrections make it exact.
+__device__ __forceinline__ uint32_t extra_iters32(uint32_t m1, uint32_t te, uint32_t end1,
+                                                  uint32_t d, float rd) {
+  if (te == T32_INF) return m1;
+  if (te <= end1) return 0;
+  const uint32_t g = te - end1;
+  if ((uint64_t)m1 * d < g) return m1;
+  uint32_t c = (uint32_t)((float)g * rd);
+  while ((uint64_t)c * d < g) ++c;
+  while (c > 0 && (uint64_t)(c - 1) * d >= g) --c;
+  return c;
+}
+
 __device__ __forceinline__ uint32_t sat32(int64_t v) {  // v >= 0
   return v >= (int64_t)T32_LIM ? T32_LIM : (uint32_t)v;
 }
@@ -789,7 +807,41 @@ __device__ __forceinline__ bool replay_one_t32(const ReplayArgs& a, int64_t r, S
     }
 
     // IterationEnd: members whose last token was emitted finish, in index order (C-6)
-    if (in_flight && iter_end == now) {
+    if (!STATS && in_flight && iter_end == now) {
+      // TTL-grid class: every finish takes the same pause action (pin for ttl_fixed, or evict)
+      // and touches only its own program and order-free sums, so the finishing lanes apply
+      // it in parallel; D and turns_done are counted once at the end
+      in_flight = false;
+      const bool f = st == S_RUN && fin == n_it;
+      const uint32_t m = __ballot_sync(FULL_MASK, f);
+      if (m) {
+        const bool last = turn == nturns - 1;
+        const bool rel = last || ttl_fixed <= 0;  // the blocks return to the pool
+        n_run -= __popc(m);
+        kv_sum -= (int32_t)__reduce_add_sync(FULL_MASK, f ? (uint32_t)gblk : 0u);
+        free_blk += (int32_t)__reduce_add_sync(FULL_MASK, f && rel ? (uint32_t)gblk : 0u);
+        if (f) {
+          ctx += rec.x + rec.y;
+          if (last) {
+            gblk = 0;
+            st = S_DONE;
+            req = now - arr;
+          } else {
+            if (ttl_fixed > 0) {  // pin_request only if TTL != 0
+              pin = true;
+              texp = ttl_fixed >= (int64_t)T32_LIM ? T32_LIM : sat32((int64_t)now + ttl_fixed + 1);
+            } else {
+              gblk = 0;
+              pin = false;
+              texp = T32_INF;
+            }
+            tev = sat32((int64_t)now + rec.w);
+            st = S_TOOL;
+          }
+        }
+      }
+    }
+    if (STATS && in_flight && iter_end == now) {
       in_flight = false;
       uint32_t m = __ballot_sync(FULL_MASK, st == S_RUN && fin == n_it);
       while (m) {
@@ -958,29 +1010,32 @@ __device__ __forceinline__ bool replay_one_t32(const ReplayArgs& a, int64_t r, S
         d_cur = iter_us_kv32(a, (uint32_t)kv_sum, &rb_cur);  // < 2^31 (host-checked)
         rd_cur = rcp_approx((float)d_cur);  // estimate only: macro_iters32 corrects
       }
-      // the TTL-grid kernel (48 registers) measured faster with the plain 64-bit sum
-      const int64_t dur1 =
-          pf <= 0 ? d_cur
-          : STATS ? iter_us_prefill(a, d_cur, rb_cur, (uint32_t)kv_sum, pf)
-                  : ceil_ps_to_us((uint64_t)(E.c0_ps + E.c_kv_ps * E.bs * kv_sum + E.c_pf_ps * pf));
+      const int64_t dur1 = pf <= 0 ? d_cur : iter_us_prefill(a, d_cur, rb_cur, (uint32_t)kv_sum, pf);
       pf = 0;
-      int64_t k = 1;
+      // every end below is checked against the 32-bit horizon (else: the 64-bit path replays
+      // the replica), so the macro-step is computed on 32-bit times
+      if (dur1 >= (int64_t)(T32_LIM - now)) return false;
+      const uint32_t end1 = now + (uint32_t)dur1;
+      uint32_t kk = 0;  // iterations of d_cur after the first one
       if (stable) {
         const uint32_t mfin = __reduce_min_sync(FULL_MASK, st == S_RUN ? fin : T32_INF);
         const uint32_t te = __reduce_min_sync(FULL_MASK, qleft ? min(tev, texp) : tev);
-        k = macro_iters32((int64_t)(mfin - n_it), te == T32_INF ? CT_INF64 : (int64_t)te - now,
-                          dur1, d_cur, rd_cur);
+        kk = extra_iters32(mfin - n_it - 1, te, end1, d_cur, rd_cur);
       }
-      const int64_t dur = dur1 + (k - 1) * (int64_t)d_cur;
-      if ((uint64_t)n_it + (uint64_t)k > it_cap) { status = CT_R_EVENT_BUDGET; break; }
-      const int64_t end = (int64_t)now + dur;
-      if (end >= (int64_t)T32_LIM) return false;  // beyond the 32-bit horizon
-      n_it += (uint32_t)k;
+      const uint64_t end = (uint64_t)end1 + (uint64_t)kk * d_cur;
+      if ((uint64_t)n_it + kk + 1 > it_cap) { status = CT_R_EVENT_BUDGET; break; }
+      if (end >= T32_LIM) return false;  // beyond the 32-bit horizon
+      const uint32_t dur = (uint32_t)end - now;
+      n_it += kk + 1;
       iter_end = (uint32_t)end;
       acc_add(ACC_BUSY, dur);
-      if (plas && st == S_RUN) svc += (uint32_t)dur;  // every running request accrues the iterations
+      if (plas && st == S_RUN) svc += dur;  // every running request accrues the iterations
       in_flight = true;
     }
+  }
+  if (!STATS) {
+    D = __popc(__ballot_sync(FULL_MASK, st == S_DONE));
+    turns_done = (int32_t)__reduce_add_sync(FULL_MASK, st == S_DONE ? (uint32_t)nturns : 0u);
   }
   if (status == CT_R_OK && D != P) status = CT_R_UNSCHEDULABLE;
 
