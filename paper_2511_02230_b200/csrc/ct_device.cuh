@@ -65,6 +65,14 @@ __device__ __forceinline__ uint32_t ceil_div_magic(uint32_t x, const DivMagic& m
   return (uint32_t)(p >> 32) + y * m.ident;
 }
 
+// The generic quotients (a 128-bit quotient of 2^50 or more, a 64-bit one of 2^50 or more) are
+// cold paths.  OL = true (the 32 < P <= 256 kernels, whose estimator sits in a large loop)
+// calls one out-of-line copy of each, keeping the long division sequences out of the hot
+// instruction footprint (measured: cfg2 +3 %); the P <= 32 kernels keep them inline (a call
+// there measured 2-5 % slower: register pressure around the call).
+static __host__ __device__ __noinline__ u128_t div_u128_slow(u128_t num, u128_t den) { return num / den; }
+static __host__ __device__ __noinline__ uint64_t div_u64_slow(uint64_t num, uint64_t den) { return num / den; }
+
 // floor(sqrt(x)) exactly: double estimate, then integer correction.
 // floor(sqrt(x)) for x < 2^128 exactly (the argument of the Bernstein square root can exceed
 // 2^64 for small n, wide samples and a small delta): double estimate, integer correction.
@@ -113,6 +121,7 @@ __host__ __device__ __forceinline__ uint64_t isqrt_u64(uint64_t x) {
 // scaling, so several quotients by one divisor share one double division.  rden then adds at
 // most two roundings and the product one, for six in all: the relative error stays below
 // 2^-50.4, and the estimate is still within one of any quotient below 2^50.
+template <bool OL = false>
 __host__ __device__ __forceinline__ u128_t div_u128_r(u128_t num, uint64_t den, double rden) {
   const double dn = (double)(uint64_t)(num >> 64) * 18446744073709551616.0 + (double)(uint64_t)num;
   const double est = dn * rden;
@@ -123,9 +132,10 @@ __host__ __device__ __forceinline__ u128_t div_u128_r(u128_t num, uint64_t den, 
     else if (num - prod >= den) q += 1;
     return q;
   }
-  return num / den;
+  return OL ? div_u128_slow(num, den) : num / den;
 }
 
+template <bool OL = false>
 __host__ __device__ __forceinline__ u128_t div_u128_u64(u128_t num, uint64_t den) {
   const double dn = (double)(uint64_t)(num >> 64) * 18446744073709551616.0 + (double)(uint64_t)num;
   const double est = dn / (double)den;
@@ -136,7 +146,7 @@ __host__ __device__ __forceinline__ u128_t div_u128_u64(u128_t num, uint64_t den
     else if (num - prod >= den) q += 1;
     return q;
   }
-  return num / den;
+  return OL ? div_u128_slow(num, den) : num / den;
 }
 
 struct Stat {  // one estimator row: n, sum t~, sum t~^2 (128-bit as lo/hi)
@@ -148,6 +158,7 @@ struct Stat {  // one estimator row: n, sum t~, sum t~^2 (128-bit as lo/hi)
 // floor(s1/n) + isqrt(floor(2 v L_q / (n 2^32))) + floor(3 b L_q / (n 2^32)),
 // v = floor((n s2 - s1^2) / (n (n-1))) for n >= 2, else 0.
 // The three quotients by n and by n 2^32 share one reciprocal of n.
+template <bool OL = false>
 __host__ __device__ __forceinline__ int64_t bernstein(const Stat& s, uint64_t lq, int64_t b_us) {
   const int64_t n = s.n;
   const double rn = 1.0 / (double)n;           // n < 2^31 (validated): exact conversion
@@ -164,7 +175,7 @@ __host__ __device__ __forceinline__ int64_t bernstein(const Stat& s, uint64_t lq
       else if (num - prod >= den) q += 1;
       mu = (int64_t)q;
     } else {
-      mu = (int64_t)(num / den);
+      mu = OL ? (int64_t)div_u64_slow(num, den) : (int64_t)(num / den);
     }
   }
   u128_t v = 0;
@@ -172,16 +183,17 @@ __host__ __device__ __forceinline__ int64_t bernstein(const Stat& s, uint64_t lq
     u128_t s2 = ((u128_t)s.s2hi << 64) | s.s2lo;
     u128_t num = (u128_t)(uint64_t)n * s2 - (u128_t)(uint64_t)s.s1 * (uint64_t)s.s1;
     uint64_t den = (uint64_t)n * (uint64_t)(n - 1);  // n < 2^31 (validated)
-    v = div_u128_u64(num, den);
+    v = div_u128_u64<OL>(num, den);
   }
   uint64_t nsh = (uint64_t)n << 32;
-  u128_t a2 = div_u128_r((u128_t)2 * v * lq, nsh, rnsh);
+  u128_t a2 = div_u128_r<OL>((u128_t)2 * v * lq, nsh, rnsh);
   uint64_t t2 = isqrt_u128(a2);
-  u128_t t3 = div_u128_r((u128_t)3 * (uint64_t)b_us * lq, nsh, rnsh);
+  u128_t t3 = div_u128_r<OL>((u128_t)3 * (uint64_t)b_us * lq, nsh, rnsh);
   return mu + (int64_t)t2 + (int64_t)t3;
 }
 
 // 𝓑(r,f) then CalcTTL offset, readings R7/R8/R36.
+template <bool OL = false>
 __host__ __device__ __forceinline__ int64_t calc_ttl(const Stat& g, const Stat& f,
                                             const ct_estimator_params& e, int64_t n_done,
                                             int64_t turns_done) {
@@ -195,7 +207,7 @@ __host__ __device__ __forceinline__ int64_t calc_ttl(const Stat& g, const Stat& 
     s.s1 = tool ? f.s1 : g.s1;
     s.s2lo = tool ? f.s2lo : g.s2lo;
     s.s2hi = tool ? f.s2hi : g.s2hi;
-    B = bernstein(s, e.lq, e.b_us);
+    B = bernstein<OL>(s, e.lq, e.b_us);
   }
   if (B < 1) B = 1;
   const u128_t T2 = (u128_t)(uint64_t)e.t_default_us * (uint64_t)e.t_default_us;  // < 2^80
@@ -204,9 +216,10 @@ __host__ __device__ __forceinline__ int64_t calc_ttl(const Stat& g, const Stat& 
     u128_t num = T2 * ((u128_t)(uint64_t)n_done * (uint64_t)e.a_den +
                        (u128_t)(uint64_t)e.a_num * (uint64_t)turns_done);
     u128_t den = (u128_t)(uint64_t)B * (uint64_t)n_done * (uint64_t)e.a_den;
-    ttl = (den >> 64) == 0 ? div_u128_u64(num, (uint64_t)den) : num / den;
+    ttl = (den >> 64) == 0 ? div_u128_u64<OL>(num, (uint64_t)den)
+                           : OL ? div_u128_slow(num, den) : num / den;
   } else {
-    ttl = div_u128_u64(T2, (uint64_t)B);
+    ttl = div_u128_u64<OL>(T2, (uint64_t)B);
   }
   if (e.ttl_max_us > 0 && ttl > (u128_t)(uint64_t)e.ttl_max_us) ttl = (uint64_t)e.ttl_max_us;
   if (ttl >= (u128_t)CT_TTL_SAT) ttl = CT_TTL_SAT - 1;  // reading R36

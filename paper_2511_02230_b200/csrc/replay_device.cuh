@@ -560,13 +560,15 @@ __device__ __forceinline__ int64_t calc_ttl_cached(const Stat* stats, TtlCache* 
                                                    int f, const ct_estimator_params& est,
                                                    int32_t D, int32_t turns_done, int lane) {
   const int64_t nf = stats[f].n;
-  if (nf < est.n_min) return calc_ttl(stats[F], stats[f], est, D, turns_done);
+  const bool keyed = nf >= est.n_min;
   const uint64_t key = ((uint64_t)nf << 32) | (uint32_t)D;
-  if (tcache[f].key == key) return tcache[f].ttl;
-  const int64_t ttl = calc_ttl(stats[F], stats[f], est, D, turns_done);
-  __syncwarp();
-  if (lane == 0) { tcache[f].key = key; tcache[f].ttl = ttl; }
-  __syncwarp();
+  if (keyed && tcache[f].key == key) return tcache[f].ttl;
+  const int64_t ttl = calc_ttl<true>(stats[F], stats[f], est, D, turns_done);  // one inlined copy
+  if (keyed) {
+    __syncwarp();
+    if (lane == 0) { tcache[f].key = key; tcache[f].ttl = ttl; }
+    __syncwarp();
+  }
   return ttl;
 }
 
@@ -1825,7 +1827,7 @@ __device__ __forceinline__ void replay_one_ns(const ReplayArgs& a, int64_t r, un
     // nearest rank (R20): value v with #(x < v) < rank <= #(x <= v)
     const int r50 = (50 * P + 99) / 100, r99 = (99 * P + 99) / 100;
     int64_t c50 = CT_INF64, c99 = CT_INF64;
-#pragma unroll
+#pragma unroll 1
     for (int s = 0; s < NS; ++s) {
       const int p = lane + 32 * s;
       if (p < P) {
@@ -2280,10 +2282,11 @@ __device__ __forceinline__ bool replay_one_ns32(const ReplayArgs& a, int64_t r,
     }
     jsum = (int64_t)warp_sum_u64((uint64_t)ls);
     jmax = __reduce_max_sync(FULL_MASK, lm);
-    // nearest rank (R20): value v with #(x < v) < rank <= #(x <= v)
+    // nearest rank (R20): value v with #(x < v) < rank <= #(x <= v); once per replica, so
+    // kept rolled (instruction footprint)
     const int r50 = (50 * P + 99) / 100, r99 = (99 * P + 99) / 100;
     uint32_t c50 = T32_INF, c99 = T32_INF;
-#pragma unroll
+#pragma unroll 1
     for (int s = 0; s < NS; ++s) {
       const int p = lane + 32 * s;
       if (p < P) {
