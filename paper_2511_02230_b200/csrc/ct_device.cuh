@@ -188,7 +188,23 @@ __host__ __device__ __forceinline__ int64_t bernstein(const Stat& s, uint64_t lq
   uint64_t nsh = (uint64_t)n << 32;
   u128_t a2 = div_u128_r<OL>((u128_t)2 * v * lq, nsh, rnsh);
   uint64_t t2 = isqrt_u128(a2);
-  u128_t t3 = div_u128_r<OL>((u128_t)3 * (uint64_t)b_us * lq, nsh, rnsh);
+  // floor(3 b L_q / (n 2^32)) = floor(floor(3 b L_q / 2^32) / n): a 64-bit numerator below
+  // 3 2^48 (b, L_q < 2^40, host-checked), loop-invariant in the replay; its quotient by n as mu
+  uint64_t t3;
+  {
+    const uint64_t num = (uint64_t)(((u128_t)3 * (uint64_t)b_us * lq) >> 32);
+    const uint64_t den = (uint64_t)n;
+    const double est = (double)num * rn;
+    if (est < 1125899906842624.0) {  // 2^50
+      uint64_t q = (uint64_t)est;
+      const uint64_t prod = q * den;
+      if (prod > num) q -= 1;
+      else if (num - prod >= den) q += 1;
+      t3 = q;
+    } else {
+      t3 = OL ? div_u64_slow(num, den) : num / den;
+    }
+  }
   return mu + (int64_t)t2 + (int64_t)t3;
 }
 

@@ -2249,20 +2249,21 @@ __device__ __forceinline__ bool replay_one_ns32(const ReplayArgs& a, int64_t r,
       }
       const int64_t dur1 = pf > 0 ? iter_us_prefill(a, d_cur, rb_cur, (uint32_t)kv_sum, pf) : d_cur;
       pf = 0;
-      int64_t k = 1;
+      // 32-bit macro-step as in replay_one_t32 (every end is checked against the horizon)
+      if (dur1 >= (int64_t)(T32_LIM - now)) return false;
+      const uint32_t end1 = now + (uint32_t)dur1;
+      uint32_t kk = 0;
       if (stable) {
         const uint32_t mfin = __reduce_min_sync(FULL_MASK, fmin);
         const uint32_t te = min(__reduce_min_sync(FULL_MASK, qleft ? min(lev, lexp) : lev), t_arr);
-        k = macro_iters32((int64_t)(mfin - n_it), te == T32_INF ? CT_INF64 : (int64_t)te - now,
-                          dur1, d_cur, rd_cur);
+        kk = extra_iters32(mfin - n_it - 1, te, end1, d_cur, rd_cur);
       }
-      const int64_t dur = dur1 + (k - 1) * (int64_t)d_cur;
-      if ((uint64_t)n_it + (uint64_t)k > it_cap) { status = CT_R_EVENT_BUDGET; break; }
-      const int64_t end = (int64_t)now + dur;
-      if (end >= (int64_t)T32_LIM) return false;  // beyond the 32-bit horizon
-      n_it += (uint32_t)k;
+      const uint64_t end = (uint64_t)end1 + (uint64_t)kk * d_cur;
+      if ((uint64_t)n_it + kk + 1 > it_cap) { status = CT_R_EVENT_BUDGET; break; }
+      if (end >= T32_LIM) return false;  // beyond the 32-bit horizon
+      n_it += kk + 1;
       iter_end = (uint32_t)end;
-      acc_add(ACC_BUSY, dur);
+      acc_add(ACC_BUSY, (int64_t)((uint32_t)end - now));
       in_flight = true;
     }
   }
