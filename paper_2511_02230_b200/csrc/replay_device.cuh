@@ -623,6 +623,11 @@ __device__ __forceinline__ uint32_t extra_iters32(uint32_t m1, uint32_t te, uint
   return c;
 }
 
+// min(t + x, T32_LIM) for a time t < T32_LIM and a duration x >= 0, in 32-bit arithmetic
+__device__ __forceinline__ uint32_t add_sat32(uint32_t t, uint32_t x) {
+  return x >= T32_LIM - t ? T32_LIM : t + x;
+}
+
 __device__ __forceinline__ uint32_t sat32(int64_t v) {  // v >= 0
   return v >= (int64_t)T32_LIM ? T32_LIM : (uint32_t)v;
 }
@@ -648,6 +653,8 @@ __device__ __forceinline__ bool replay_one_t32(const ReplayArgs& a, int64_t r, S
   const int pause = polp->pause;
   const int prio = polp->priority;  // STATS: program or request FCFS (simple_policy)
   const int64_t ttl_fixed = pause == CT_PAUSE_FIXED ? polp->t_pin_us : 0;
+  // expiry offset ttl + 1 of a FIXED pin, saturated at the horizon (ttl < CT_TTL_SAT)
+  const uint32_t ttl1 = ttl_fixed >= (int64_t)T32_LIM ? T32_LIM : (uint32_t)ttl_fixed + 1;
   const int F = a.F;
   const ct_estimator_params& est = a.est;
   const bool need_stats =
@@ -703,11 +710,16 @@ __device__ __forceinline__ bool replay_one_t32(const ReplayArgs& a, int64_t r, S
   // summary counters (ACC_*): with the estimator, lane k holds counter k in one register; the
   // TTL-grid class accumulates the warp-uniform values in every lane (uniform registers),
   // measured 5 % faster there and 5 % slower with the estimator's register pressure
+  // (TTL-grid class: the time and count counters, ACC_BUSY onward, are 32-bit: busy time lies
+  // within the replica's span, below the 32-bit horizon, and each count is below 2^31)
   int64_t accv = 0;
   int64_t A[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  uint32_t A32[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   auto acc_add = [&](int k, int64_t v) {
     if (STATS) {
       if (lane == k) accv += v;
+    } else if (k >= ACC_BUSY) {
+      A32[k] += (uint32_t)v;
     } else {
       A[k] += v;
     }
@@ -831,13 +843,13 @@ __device__ __forceinline__ bool replay_one_t32(const ReplayArgs& a, int64_t r, S
           } else {
             if (ttl_fixed > 0) {  // pin_request only if TTL != 0
               pin = true;
-              texp = ttl_fixed >= (int64_t)T32_LIM ? T32_LIM : sat32((int64_t)now + ttl_fixed + 1);
+              texp = add_sat32(now, ttl1);
             } else {
               gblk = 0;
               pin = false;
               texp = T32_INF;
             }
-            tev = sat32((int64_t)now + rec.w);
+            tev = add_sat32(now, (uint32_t)rec.w);
             st = S_TOOL;
           }
         }
@@ -987,7 +999,7 @@ __device__ __forceinline__ bool replay_one_t32(const ReplayArgs& a, int64_t r, S
             unc = (int32_t)u;
           } else {
             st = S_RUN;
-            fin = sat32((int64_t)n_it + rec.y);
+            fin = STATS ? sat32((int64_t)n_it + rec.y) : add_sat32(n_it, (uint32_t)rec.y);
           }
         }
         if (EXT && loading) {
@@ -1025,7 +1037,10 @@ __device__ __forceinline__ bool replay_one_t32(const ReplayArgs& a, int64_t r, S
         kk = extra_iters32(mfin - n_it - 1, te, end1, d_cur, rd_cur);
       }
       const uint64_t end = (uint64_t)end1 + (uint64_t)kk * d_cur;
-      if ((uint64_t)n_it + kk + 1 > it_cap) { status = CT_R_EVENT_BUDGET; break; }
+      if (STATS ? (uint64_t)n_it + kk + 1 > it_cap : kk >= it_cap - n_it) {  // n_it + kk + 1 > it_cap
+        status = CT_R_EVENT_BUDGET;
+        break;
+      }
       if (end >= T32_LIM) return false;  // beyond the 32-bit horizon
       const uint32_t dur = (uint32_t)end - now;
       n_it += kk + 1;
@@ -1062,7 +1077,7 @@ __device__ __forceinline__ bool replay_one_t32(const ReplayArgs& a, int64_t r, S
   }
   int64_t av[8];
 #pragma unroll
-  for (int k = 0; k < 8; ++k) av[k] = STATS ? shfl64(accv, k) : A[k];
+  for (int k = 0; k < 8; ++k) av[k] = STATS ? shfl64(accv, k) : k >= ACC_BUSY ? (int64_t)A32[k] : A[k];
   if (lane == 0) {
     ct_replica_summary o;
     if (status == CT_R_OK) {
