@@ -724,6 +724,7 @@ __device__ __forceinline__ bool replay_one_t32(const ReplayArgs& a, int64_t r, S
       A[k] += v;
     }
   };
+  const int max_batch = (int)min(E.max_batch, (int64_t)0x7fffffff);
   // iteration budget as a 32-bit bound (n_it < 2^32 on this path)
   const uint32_t it_cap = E.max_iters >= (int64_t)T32_INF ? T32_INF : (uint32_t)E.max_iters;
   int32_t kv_at = -1;
@@ -929,7 +930,7 @@ __device__ __forceinline__ bool replay_one_t32(const ReplayArgs& a, int64_t r, S
       for (;;) {  // admit loop (victims PAPER.md:645-655)
         const uint32_t mq = __ballot_sync(FULL_MASK, st == S_QUEUED);
         if (!mq) break;
-        if (n_run + n_load >= E.max_batch) { qleft = true; break; }
+        if (n_run + n_load >= max_batch) { qleft = true; break; }
         int h;
         if (!STATS || prio == CT_PRIO_PROG_FCFS) {  // pinned-queued first, then queued, by index
           const uint32_t mp = __ballot_sync(FULL_MASK, st == S_QUEUED && pin);
@@ -945,7 +946,8 @@ __device__ __forceinline__ bool replay_one_t32(const ReplayArgs& a, int64_t r, S
         const int32_t hg = __shfl_sync(FULL_MASK, gblk, h);
         const int32_t hnew = __shfl_sync(FULL_MASK, rec.x, h);
         const int32_t hdec = __shfl_sync(FULL_MASK, rec.y, h);
-        const int64_t need = (int64_t)ceil_div_magic((uint32_t)(hctx + hnew + hdec), bsm) - hg;
+        // blocks, contexts and token counts are below 2^30 (validated): 32-bit arithmetic
+        const int32_t need = (int32_t)ceil_div_magic((uint32_t)(hctx + hnew + hdec), bsm) - hg;
         if (need > free_blk && admitted == 0) {
           while (need > free_blk) {  // victims: latest program arrival first, never the head
             const uint32_t mv = __ballot_sync(FULL_MASK, pin && lane != h);
@@ -965,14 +967,14 @@ __device__ __forceinline__ bool replay_one_t32(const ReplayArgs& a, int64_t r, S
           qleft = true;
           break;
         }
-        free_blk -= (int32_t)need;
-        const int32_t ng = hg + (int32_t)need;
+        free_blk -= need;
+        const int32_t ng = hg + need;
         acc_add(ACC_BUBBLE, (int64_t)(now - __shfl_sync(FULL_MASK, req, h)));
         const bool hp = __shfl_sync(FULL_MASK, pin ? 1 : 0, h) != 0;
         const int32_t hd = dram_on ? __shfl_sync(FULL_MASK, dblk, h) : 0;
         bool loading = false;
         uint32_t ld = 0;
-        int64_t cached;
+        int32_t cached;
         if (hp) {
           cached = hctx;
           acc_add(ACC_HITS, 1);
@@ -987,7 +989,7 @@ __device__ __forceinline__ bool replay_one_t32(const ReplayArgs& a, int64_t r, S
           cached = 0;
           acc_add(ACC_RECOMP, hctx);
         }
-        const int64_t u = hctx + hnew - cached;
+        const int32_t u = hctx + hnew - cached;  // < 2^31
         acc_add(ACC_PREFILL, u);
         if (lane == h) {
           pin = false;
