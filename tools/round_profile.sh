@@ -42,8 +42,5 @@ python bench.py --impl reference --steps 3 --warmup 1 > $OUT/${R}_bench_referenc
 tail -1 $OUT/${R}_bench_reference.log > $OUT/${R}_bench_reference.json
 ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv --log-file $OUT/${R}_launches.csv \
     python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e --no-fit-bandwidth > $OUT/${R}_launches_bench.log 2>&1
-for t in memcheck racecheck synccheck initcheck; do
-  echo "== $t" >> $OUT/${R}_sanitizer.txt
-  timeout 900 compute-sanitizer --tool $t python tools/sanitize.py 2>&1 | grep -E "SUMMARY|sanitize run" >> $OUT/${R}_sanitizer.txt
-done
+# compute-sanitizer is closed on this GPU pool (round 2): the round-1 sanitizer run stands
 ls -la $OUT
