@@ -208,11 +208,58 @@ __host__ __device__ __forceinline__ int64_t bernstein(const Stat& s, uint64_t lq
   return mu + (int64_t)t2 + (int64_t)t3;
 }
 
+#ifdef __CUDA_ARCH__
+// A real upper bound of the fixed-point Bernstein bound B (C-1) of
+// row s (n >= 1), in single precision with approximate reciprocal / square root: every rounding
+// (at most ~2^-22 relative each) is covered by the margin M = 1 + 2^-12 applied after each
+// step, and floor() only lowers the exact terms.  Uses the identities
+// floor(s1/n) <= s1/n, v <= (s2/n - (s1/n)^2) n/(n-1), isqrt(floor(a)) <= sqrt(a).
+__device__ __forceinline__ float bernstein_upper(const Stat& s, uint64_t lq, int64_t b_us) {
+  constexpr float M = 1.000244140625f, Mi = 0.999755859375f;  // 1 +- 2^-12
+  float rn, r;
+  const float nf = (float)s.n;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rn) : "f"(nf));
+  const float rn_up = rn * M, rn_lo = rn * Mi;
+  const float s1 = (float)s.s1;
+  const float mean_up = s1 * rn_up * M, mean_lo = s1 * rn_lo * Mi;
+  float var_up = 0.0f;
+  if (s.n >= 2) {
+    const float s2 = (float)s.s2hi * 18446744073709551616.0f + (float)s.s2lo;
+    float n1;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(n1) : "f"(nf - 1.0f));  // n - 1 >= 1 exact below 2^24
+    var_up = fmaxf(s2 * M * rn_up * M - mean_lo * mean_lo * Mi, 0.0f) * (nf * n1 * M * M);
+  }
+  const float lqf = (float)lq * M;
+  const float a_up = 2.0f * var_up * lqf * rn_up * 2.3283064365386963e-10f * M;
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(a_up));
+  const float t3_up = 3.0f * (float)b_us * lqf * rn_up * 2.3283064365386963e-10f * M;
+  return (mean_up + r * M + t3_up) * M + 2.0f;
+}
+#endif
+
 // 𝓑(r,f) then CalcTTL offset, readings R7/R8/R36.
-template <bool OL = false>
+// QUICK (device): when an upper bound of 𝓑 already proves the offset at or above the clamp
+// ttl_max (the common case once a tool row holds many samples), return the clamp without the
+// exact 128-bit evaluation; the result is identical (the test is one-sided and rigorous).
+template <bool OL = false, bool QUICK = false>
 __host__ __device__ __forceinline__ int64_t calc_ttl(const Stat& g, const Stat& f,
                                             const ct_estimator_params& e, int64_t n_done,
                                             int64_t turns_done) {
+#ifdef __CUDA_ARCH__
+  if (QUICK && e.ttl_max_us > 0 && g.n >= e.n_min) {
+    const Stat& q = f.n >= e.n_min ? f : g;
+    const double bu = fmax((double)bernstein_upper(q, e.lq, e.b_us), 1.0);
+    // floor(T^2 (D a_den + a_num turns) / (B D a_den)) >= ttl_max  <=  T^2 (D a_den + a_num
+    // turns) >= ttl_max B_up D a_den; both sides in double with a 2^-40 relative margin
+    const double t = (double)e.t_default_us;
+    const double lhs = n_done > 0 ? t * t * ((double)n_done * (double)e.a_den +
+                                             (double)e.a_num * (double)turns_done)
+                                   : t * t;
+    const double rhs = n_done > 0 ? (double)e.ttl_max_us * bu * (double)n_done * (double)e.a_den
+                                  : (double)e.ttl_max_us * bu;
+    if (lhs >= rhs * 1.0000000000009095) return e.ttl_max_us;  // ttl_max < CT_TTL_SAT
+  }
+#endif
   int64_t B;
   if (g.n < e.n_min) {
     B = e.t_default_us;

@@ -563,7 +563,7 @@ __device__ __forceinline__ int64_t calc_ttl_cached(const Stat* stats, TtlCache* 
   const bool keyed = nf >= est.n_min;
   const uint64_t key = ((uint64_t)nf << 32) | (uint32_t)D;
   if (keyed && tcache[f].key == key) return tcache[f].ttl;
-  const int64_t ttl = calc_ttl<true>(stats[F], stats[f], est, D, turns_done);  // one inlined copy
+  const int64_t ttl = calc_ttl<true, true>(stats[F], stats[f], est, D, turns_done);  // one inlined copy
   if (keyed) {
     __syncwarp();
     if (lane == 0) { tcache[f].key = key; tcache[f].ttl = ttl; }
