@@ -58,7 +58,8 @@ __global__ void __launch_bounds__(256) calc_ttl_kernel(const ct_stat_row* g, con
     const int64_t d = n_done[i], td = turns_done[i];
     const bool ok = row_ok(gr, e.b_us) && row_ok(fr, e.b_us) && d >= 0 && d <= CT_MAX_PROGRAMS &&
                     td >= 0 && td <= (int64_t)CT_MAX_PROGRAMS * CT_MAX_TURNS;
-    out[i] = ok ? calc_ttl(to_stat(gr), to_stat(fr), e, d, td) : CT_TTL_INVALID;
+    // the replay's CalcTTL, including its clamp shortcut (identical results to the exact path)
+    out[i] = ok ? calc_ttl<false, true>(to_stat(gr), to_stat(fr), e, d, td) : CT_TTL_INVALID;
   }
 }
 

@@ -881,7 +881,9 @@ __device__ __forceinline__ bool replay_one_t32(const ReplayArgs& a, int64_t r, S
             if (pause == CT_PAUSE_FIXED) {
               ttl = simplified_ttl(stats[F], stats[ptool], est, polp->t_pin_us, polp->t_thresh_us);
             } else if (pause == CT_PAUSE_PAPER) {
-              ttl = calc_ttl(stats[F], stats[ptool], est, D, turns_done);  // cache measured slower here
+              // exact path: the cache and the clamp shortcut both measured slower here
+              // (P <= 32: few samples per tool row, register pressure)
+              ttl = calc_ttl(stats[F], stats[ptool], est, D, turns_done);
             } else if (pause == CT_PAUSE_FITTED) {
               ttl = __ldg(&a.fitted[(int64_t)ptool * a.J + min(pt, a.J - 1)]);
             } else if (EXT && pause == CT_PAUSE_INFERCEPT) {

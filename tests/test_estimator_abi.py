@@ -8,6 +8,7 @@ examples through the device kernels.
 """
 import math
 import random
+from dataclasses import replace
 
 import numpy as np
 import pytest
@@ -131,3 +132,45 @@ def test_device_spec_examples_and_random(ct):
         assert got[i] == ct.ct_calc_ttl_ref(G[i], Fr[i], e, D[i], TD[i])
         if G[i][0] >= 1:
             assert bern[i] == ct.ct_bernstein_ref(G[i], e)
+
+
+@pytest.mark.gpu
+def test_device_calc_ttl_clamp_shortcut_exact(ct):
+    """The device CalcTTL (the replay's helper) returns ttl_max without the exact evaluation
+    when a single-precision upper bound of the Bernstein bound proves the clamp.  It must equal
+    the exact host reference (and the oracle) everywhere, in particular with ttl_max within a
+    few µs of the unclamped value, where a too-loose or too-tight bound would show."""
+    import torch
+    ctx = ct.Context(0)
+    rng = np.random.default_rng(11)
+    L = O.lib()
+
+    def rows(rs):
+        return torch.tensor([[r[0], r[1], np.int64(np.uint64(r[2] & (2**64 - 1))),
+                              np.int64(np.uint64(r[2] >> 64))] for r in rs], dtype=torch.int64).cuda()
+
+    cases = []
+    for i in range(240):
+        b = int(rng.choice([60 * S, 2**31 - 1, 5 * S]))
+        n = int(rng.choice([1, 2, 3, 5, 17, 100, 1000, 20000]))
+        mu = float(rng.choice([1e3, 1e5, 2e6, 8e6]))
+        xs = np.minimum(rng.lognormal(np.log(mu), float(rng.choice([0.0, 0.3, 1.0, 2.0])), n), 2**31 - 1)
+        fs = stat(xs.astype(np.int64).tolist(), b)
+        gs = stat((xs.astype(np.int64).tolist() * 2)[: n + 3], b)
+        d = int(rng.integers(0, 257))
+        td = int(rng.integers(d, 50 * d + 1)) if d else 0
+        e0 = cf.Estimator(b_us=b, t_def_us=int(rng.choice([10 * S, 3 * S, 60 * S])), n_min=5,
+                          a_num=1, a_den=10, ttl_max_us=0)
+        free = ct.ct_calc_ttl_ref(gs, fs, e0, d, td)  # unclamped offset
+        assert free >= 0
+        for off in (-3, -1, 0, 1, 2) if free > 4 else (1, 2):
+            cases.append((gs, fs, d, td, e0, max(free + off, 1)))
+    for gs, fs, d, td, e0, tmax in cases:
+        e = replace(e0, ttl_max_us=tmax)
+        got = int(ct.ct_calc_ttl_batch(ctx, rows([gs]), rows([fs]), torch.tensor([d]).cuda(),
+                                       torch.tensor([td]).cuda(), e).cpu()[0])
+        want = ct.ct_calc_ttl_ref(gs, fs, e, d, td)
+        assert got == want, (gs, fs, d, td, tmax)
+        orow = lambda r: [r[0], r[1], int(np.uint64(r[2] & (2**64 - 1)).astype(np.int64)),  # noqa: E731
+                          r[2] >> 64]
+        assert want == O.calc_ttl(orow(gs), orow(fs), e.as_array(), d, td)
