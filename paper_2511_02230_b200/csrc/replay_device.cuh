@@ -1930,7 +1930,7 @@ __device__ __forceinline__ bool replay_one_ns32(const ReplayArgs& a, int64_t r,
   uint32_t* fin = req + PM;        // finishing iteration while running, INF otherwise
   int32_t* ctx = (int32_t*)(fin + PM);
   int32_t* gblk = ctx + PM;
-  int32_t* turn = gblk + PM;
+  int32_t* tix = gblk + PM;        // index of the program's current turn record in a.turns
   Stat* stats = (Stat*)(wm + ((28 * PM + 15) & ~15));
   TtlCache* tcache = (TtlCache*)(wm + ((28 * PM + 15) & ~15) + ((32 * (a.F + 1) + 48 + 15) & ~15));
 
@@ -1966,7 +1966,7 @@ __device__ __forceinline__ bool replay_one_ns32(const ReplayArgs& a, int64_t r,
     fin[p] = T32_INF;
     ctx[p] = 0;
     gblk[p] = 0;
-    turn[p] = 0;
+    tix[p] = p < a.P ? a.progs[seed * a.P + p].turn0 : 0;
   }
   if (need_stats)
     for (int i = lane; i < 4 * (F + 1); i += 32) ((int64_t*)stats)[i] = 0;
@@ -1978,7 +1978,8 @@ __device__ __forceinline__ bool replay_one_ns32(const ReplayArgs& a, int64_t r,
   uint32_t lev = T32_INF, lexp = T32_INF, fmin = T32_INF;  // cached minima over this lane's slots
   auto own = [&](int p) { return lane == (p & 31); };
   auto bit = [&](int p) { return 1u << (p >> 5); };
-  auto turn_rec = [&](int p, int t) -> int4 { return __ldg(&a.turns[prog[p].turn0 + t]); };
+  // current turn record: one shared-memory index, then the record (no dependent program load)
+  auto rec_of = [&](int p) -> int4 { return __ldg(&a.turns[tix[p]]); };
   const int64_t arr0 = (prog[0].arr_q * gap) >> 20;  // programs arrive in index order: origin
   auto arrival = [&](int i) -> uint32_t { return sat32(((prog[i].arr_q * gap) >> 20) - arr0); };
   auto for_each_set = [&](uint32_t m, auto&& fn) {
@@ -2081,7 +2082,7 @@ __device__ __forceinline__ bool replay_one_ns32(const ReplayArgs& a, int64_t r,
       const uint32_t mret = md & tb;
       if (need_stats) {
         for_each_set(mret, [&](int p) {  // estimator rows: Δ_obs = dur of the finished turn (R5)
-          const int4 tr = turn_rec(p, turn[p]);
+          const int4 tr = rec_of(p);
           const int64_t x = min((int64_t)tr.w, est.b_us);
           const uint64_t x2 = (uint64_t)x * (uint64_t)x;
           if (lane == 0) {
@@ -2105,7 +2106,7 @@ __device__ __forceinline__ bool replay_one_ns32(const ReplayArgs& a, int64_t r,
         for (int s = 0; s < NS; ++s) {
           const int p = lane + 32 * s;
           if ((mret >> s) & 1u) {
-            turn[p] += 1;
+            tix[p] += 1;
             req[p] = tev[p];  // the event's own instant
             tev[p] = T32_INF;
             if (texp[p] != T32_INF) { texp[p] = T32_INF; rescan_e = true; }  // retained pin
@@ -2137,8 +2138,10 @@ __device__ __forceinline__ bool replay_one_ns32(const ReplayArgs& a, int64_t r,
       }
       for_each_set(mf, [&](int p) {
         // OnRequestFinish
-        const int tp = turn[p];
-        const int4 tr = turn_rec(p, tp);
+        const int tx = tix[p];
+        const int4 tr = __ldg(&a.turns[tx]);
+        const ct_program pr = prog[p];  // issued beside the record load
+        const int tp = tx - pr.turn0;
         const int nctx = ctx[p] + tr.x + tr.y;
         const int64_t g = gblk[p];
         --n_run;
@@ -2146,11 +2149,11 @@ __device__ __forceinline__ bool replay_one_ns32(const ReplayArgs& a, int64_t r,
         __syncwarp();
         if (own(p)) { rb &= ~bit(p); fin[p] = T32_INF; ctx[p] = nctx; }
         __syncwarp();
-        const int nt = prog[p].nturns;
+        const int nt = pr.nturns;
         if (tp == nt - 1) {  // last request: free its KV, the program completes
           free_blk += g;
           __syncwarp();
-          if (own(p)) { gblk[p] = 0; req[p] = now - arrival(p); }
+          if (own(p)) { gblk[p] = 0; req[p] = now - sat32(((pr.arr_q * gap) >> 20) - arr0); }
           ++D;
           turns_done += nt;
           __syncwarp();
@@ -2207,7 +2210,7 @@ __device__ __forceinline__ bool replay_one_ns32(const ReplayArgs& a, int64_t r,
           const uint32_t mk = __reduce_min_sync(FULL_MASK, bk);
           h = (int)__reduce_min_sync(FULL_MASK, (uint32_t)(bk == mk ? bp : 0x7fffffff));
         }
-        const int4 tr = turn_rec(h, turn[h]);
+        const int4 tr = rec_of(h);
         const int64_t hctx = ctx[h];
         const int64_t hg = gblk[h];
         const int64_t need = (int64_t)ceil_div_magic((uint32_t)(hctx + tr.x + tr.y), bsm) - hg;
