@@ -328,8 +328,8 @@ def fit_bandwidth(ctx, ct, cf, log2n, dev, peaks, consts):
     tr = consts.get("fit_dram_bytes_per_sample")
     return {"bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s", "frac": gbs / peak,
             "traffic": tr * n if tr else None,
-            "kernel": "fit_hist_kernel<FUSED> (histogram + grid barrier + scan/argmax/CalcTTL, "
-                      "one cooperative launch; CUDA events inside the library)",
+            "kernel": "fit_hist_kernel (the histogram pass; fit_finish_kernel follows as a "
+                      "programmatic dependent launch; CUDA events inside the library)",
             "samples": n, "bytes_per_sample": 4, "ms_per_launch": t * 1e3,
             "call_ms": t_call * 1e3, "call_gbs": 4.0 * n / t_call / 1e9,
             "call_frac": 4.0 * n / t_call / 1e9 / peak,
