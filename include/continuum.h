@@ -460,7 +460,9 @@ typedef struct {
                                (P > 32, 64-bit), 2 mixed, 3 simple class (P <= 32, 32-bit),
                                4 program-FCFS class (P > 32, 32-bit) + list-driven 64-bit launch,
                                5 as 4 with request FCFS (simple class), 6 extended class
-                               (P <= 32, 32-bit: + DRAM tier, PLAS, InferCept) */
+                               (P <= 32, 32-bit: + DRAM tier, PLAS, InferCept); 10 + m: two
+                               launches over policy subsets, MODE 1 for the TTL-grid policies
+                               and MODE m (2, 3 or 6) for the others */
   int32_t reserved;
 } ct_launch_info;
 int ct_last_launch(ct_ctx* ctx, ct_launch_info* info);

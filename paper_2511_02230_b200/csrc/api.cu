@@ -252,13 +252,23 @@ int ct_simulate_batch_ex(ct_ctx* c, const ct_trace_set* tr, const ct_sweep* sw,
 
   // device copy of the sweep axes
   const size_t n_gap = sw->n_rates, n_kv = sw->n_kv, n_pol = sw->n_policies;
-  const size_t bytes = 8 * (n_gap + n_kv) + sizeof(ct_policy) * n_pol;
+  // axes: gaps, KV budgets, policies, then the policy order of a split launch (TTL-grid class
+  // first, ascending indices within each part)
+  const size_t bytes = 8 * (n_gap + n_kv) + sizeof(ct_policy) * n_pol + 4 * n_pol;
   int rc = ensure(&c->axes, &c->axes_cap, bytes);
   if (rc) return rc;
   std::vector<unsigned char> hb(bytes);
   std::memcpy(hb.data(), sw->gap_us, 8 * n_gap);
   std::memcpy(hb.data() + 8 * n_gap, sw->kv_blocks, 8 * n_kv);
   std::memcpy(hb.data() + 8 * (n_gap + n_kv), sw->policies, sizeof(ct_policy) * n_pol);
+  {
+    int* order = (int*)(hb.data() + 8 * (n_gap + n_kv) + sizeof(ct_policy) * n_pol);
+    int k = 0;
+    for (size_t i = 0; i < n_pol; ++i)
+      if (ct::fast_policy(sw->policies[i], E)) order[k++] = (int)i;
+    for (size_t i = 0; i < n_pol; ++i)
+      if (!ct::fast_policy(sw->policies[i], E)) order[k++] = (int)i;
+  }
   CT_CUDA(cudaMemcpyAsync(c->axes, hb.data(), bytes, cudaMemcpyHostToDevice, s));
   // counter block: [0] replica counter, [1] fallback list count, [2] fallback counter,
   // [4..5] trace check result
@@ -301,6 +311,10 @@ int ct_simulate_batch_ex(ct_ctx* c, const ct_trace_set* tr, const ct_sweep* sw,
   a.out = out;
   a.jct = jct;
   a.bubble = outs->bubble_us;
+  a.sel = nullptr;
+  a.n_sel = 0;
+  a.blk0 = 0;
+  a.sel_total = 0;
   a.counter = c->counter;
   a.err = c->counter + 4;
   a.bs_magic = E.bs == 1 ? 0
@@ -365,9 +379,38 @@ int ct_simulate_batch_ex(ct_ctx* c, const ct_trace_set* tr, const ct_sweep* sw,
   if (occ < 1) return fail(CT_ECUDA, "replay kernel cannot be resident (smem %d)", smem);
   const int64_t need_blocks = (re - rb + wpb - 1) / wpb;
   const int grid = (int)std::min<int64_t>((int64_t)c->sm_count * occ, need_blocks);
+  // P <= 32 sweeps that mix TTL-grid policies with other 32-bit classes: two launches over
+  // policy subsets (ReplayArgs.sel), the TTL-grid kernel (MODE 1, no estimator, 10 CTAs/SM)
+  // for the replicas of those policies and the estimator / extended kernel for the rest
+  const int64_t nblk = (re - 1) / (int64_t)n_pol - rb / (int64_t)n_pol + 1;
+  const bool split = ns == 1 && !growth && !a.bubble && n_fast > 0 && n_fast < (int)n_pol &&
+                     (mode == 2 || mode == 3 || mode == 6) && nblk * (int64_t)n_pol < (1ll << 31);
+  a.blk0 = rb / (int64_t)n_pol;
   if (c->timing) CT_CUDA(cudaEventRecord(c->ev[0], s));
-  cudaError_t e = ct::launch_replay(a, ns, growth, mode1, wpb, grid, s);
-  if (e != cudaSuccess) return cuda_fail(e, "replay launch");
+  cudaError_t e;
+  if (split) {
+    const int* order = (const int*)(a.pols + n_pol);
+    ct::ReplayArgs g = a;
+    g.sel = order;
+    g.n_sel = n_fast;
+    g.sel_total = nblk * n_fast;
+    const int occg = ct::replay_occupancy(1, false, 1, wpb, smem);
+    if (occg < 1) return fail(CT_ECUDA, "replay kernel cannot be resident (smem %d)", smem);
+    const int gridg = (int)std::min<int64_t>((int64_t)c->sm_count * occg, (nblk * n_fast + wpb - 1) / wpb);
+    e = ct::launch_replay(g, 1, false, 1, wpb, gridg, s);
+    if (e != cudaSuccess) return cuda_fail(e, "replay launch (TTL-grid part)");
+    a.sel = order + n_fast;
+    a.n_sel = (int)n_pol - n_fast;
+    a.sel_total = nblk * a.n_sel;
+    a.counter = c->counter + 3;
+    const int grido = (int)std::min<int64_t>((int64_t)c->sm_count * occ,
+                                             (nblk * a.n_sel + wpb - 1) / wpb);
+    e = ct::launch_replay(a, 1, false, mode1, wpb, grido, s);
+    if (e != cudaSuccess) return cuda_fail(e, "replay launch");
+  } else {
+    e = ct::launch_replay(a, ns, growth, mode1, wpb, grid, s);
+    if (e != cudaSuccess) return cuda_fail(e, "replay launch");
+  }
   if (ns32) {
     ct::ReplayArgs b = a;
     b.from_list = 1;
@@ -387,8 +430,8 @@ int ct_simulate_batch_ex(ct_ctx* c, const ct_trace_set* tr, const ct_sweep* sw,
   c->last.warps_per_block = wpb;
   c->last.slots_per_lane = ns;
   c->last.smem_per_block = smem;
-  c->last.launches = (ns32 ? 2 : 1) + 1;  // + the trace check
-  c->last.kernel_mode = mode1;
+  c->last.launches = (ns32 || split ? 2 : 1) + 1;  // + the trace check
+  c->last.kernel_mode = split ? 10 + mode1 : mode1;
   return CT_OK;
 }
 

@@ -36,6 +36,10 @@ struct ReplayArgs {
   uint32_t c0q, c0r;   // c0 = c0q 1e6 - c0r, 0 <= c0r < 1e6
   uint32_t pf_q, pf_r; // c_pf = pf_q 1e6 + pf_r, 0 <= pf_r < 1e6
   uint32_t pf32;       // prefills below pf32 tokens take the 32-bit path (pf_r pf + 1e6 < 2^32)
+  const int* sel;      // policy subset of this launch (ascending indices) or NULL: every policy
+  int n_sel;
+  int64_t blk0;        // first block of n_pol replicas touched by [r_begin, r_end)
+  int64_t sel_total;   // blocks x n_sel (< 2^31)
 };
 
 // Trace-set check (validate.cu).  Bits of err[0]:

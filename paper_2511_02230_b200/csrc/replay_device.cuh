@@ -2397,17 +2397,25 @@ __global__ void __launch_bounds__(128, MINB) replay_kernel(ReplayArgs a) {
   unsigned char* wm = smem + (threadIdx.x >> 5) * a.smem_per_warp;
   // next replica of this warp (persistent grid over an atomic counter); false when done
   auto next = [&](int64_t& r) -> bool {
-    unsigned long long idx = 0;
-    if (lane == 0) idx = atomicAdd(a.counter, 1ull);
-    idx = __shfl_sync(FULL_MASK, idx, 0);
-    if (a.from_list) {  // replicas queued by a MODE 4 launch earlier on the stream
-      if (idx >= *a.fb_count) return false;
-      r = a.fb_list[idx];
-    } else {
-      r = a.r_begin + (int64_t)idx;
-      if (r >= a.r_end) return false;
+    for (;;) {
+      unsigned long long idx = 0;
+      if (lane == 0) idx = atomicAdd(a.counter, 1ull);
+      idx = __shfl_sync(FULL_MASK, idx, 0);
+      if (a.from_list) {  // replicas queued by a MODE 4 launch earlier on the stream
+        if (idx >= *a.fb_count) return false;
+        r = a.fb_list[idx];
+      } else if (a.n_sel > 0) {  // the replicas of the launch's policy subset in [r_begin, r_end)
+        // (32-bit quotient: the host splits only when blocks x n_sel < 2^31)
+        if (idx >= (unsigned long long)a.sel_total) return false;
+        const uint32_t q = (uint32_t)idx / (uint32_t)a.n_sel;
+        r = (a.blk0 + q) * a.n_pol + a.sel[(uint32_t)idx - q * (uint32_t)a.n_sel];
+        if (r < a.r_begin || r >= a.r_end) continue;
+      } else {
+        r = a.r_begin + (int64_t)idx;
+        if (r >= a.r_end) return false;
+      }
+      return true;
     }
-    return true;
   };
   int64_t r;
   if (a.err[0] != 0) {  // the trace check failed: no record is read (kept out of the main loop)
