@@ -2017,14 +2017,15 @@ __device__ __forceinline__ bool replay_one_ns32(const ReplayArgs& a, int64_t r,
   uint32_t now = 0, iter_end = 0, n_it = 0;
   const uint32_t it_cap = E.max_iters >= (int64_t)T32_INF ? T32_INF : (uint32_t)E.max_iters;
   bool in_flight = false;
-  int64_t free_blk = a.kv[kv_i];
+  int32_t free_blk = (int32_t)a.kv[kv_i];  // blocks, contexts, tokens: below 2^30 (validated)
   int next_arr = 0;
   uint32_t t_arr = 0;  // program 0 arrives at the origin
   int32_t D = 0, turns_done = 0;
   int n_run = 0;
-  int64_t kv_sum = 0, pf = 0;
+  int32_t kv_sum = 0;
+  int64_t pf = 0;
   int status = CT_R_OK;
-  int64_t kv_at = -1;
+  int32_t kv_at = -1;
   uint32_t d_cur = 0, rb_cur = 0;
   float rd_cur = 0.0f;
   int64_t accv = 0;  // lane k holds summary counter k (ACC_*)
@@ -2143,7 +2144,7 @@ __device__ __forceinline__ bool replay_one_ns32(const ReplayArgs& a, int64_t r,
         const ct_program pr = prog[p];  // issued beside the record load
         const int tp = tx - pr.turn0;
         const int nctx = ctx[p] + tr.x + tr.y;
-        const int64_t g = gblk[p];
+        const int32_t g = gblk[p];
         --n_run;
         kv_sum -= g;
         __syncwarp();
@@ -2211,9 +2212,9 @@ __device__ __forceinline__ bool replay_one_ns32(const ReplayArgs& a, int64_t r,
           h = (int)__reduce_min_sync(FULL_MASK, (uint32_t)(bk == mk ? bp : 0x7fffffff));
         }
         const int4 tr = rec_of(h);
-        const int64_t hctx = ctx[h];
-        const int64_t hg = gblk[h];
-        const int64_t need = (int64_t)ceil_div_magic((uint32_t)(hctx + tr.x + tr.y), bsm) - hg;
+        const int32_t hctx = ctx[h];
+        const int32_t hg = gblk[h];
+        const int32_t need = (int32_t)ceil_div_magic((uint32_t)(hctx + tr.x + tr.y), bsm) - hg;
         if (need > free_blk && admitted == 0) {
           while (need > free_blk) {  // victims: latest program arrival first, never the head
             const uint32_t cand = pb & ~(own(h) ? bit(h) : 0u);
@@ -2233,10 +2234,10 @@ __device__ __forceinline__ bool replay_one_ns32(const ReplayArgs& a, int64_t r,
         }
         // issue h
         free_blk -= need;
-        const int32_t ng = (int32_t)(hg + need);
+        const int32_t ng = hg + need;
         acc_add(ACC_BUBBLE, (int64_t)(now - req[h]));
         const bool hp = (__shfl_sync(FULL_MASK, pb, h & 31) >> (h >> 5)) & 1u;
-        const int64_t cached = hp ? hctx : 0;
+        const int32_t cached = hp ? hctx : 0;
         if (hp) acc_add(ACC_HITS, 1);
         acc_add(ACC_RECOMP, hctx - cached);
         const int64_t u = hctx + tr.x - cached;
