@@ -346,8 +346,10 @@ int ct_simulate_batch_ex(ct_ctx* ctx, const ct_trace_set* traces, const ct_sweep
                          const ct_replay_outputs* out, void* stream);
 
 /* Same as ct_simulate_batch but with HOST buffers: programs/turns in traces->programs/turns are
- * host pointers, out/jct_us are host pointers.  Copies in, runs, copies out and synchronises the
- * stream before returning (end-to-end path; pinned host memory recommended). */
+ * host pointers, out/jct_us are host pointers.  Copies in, checks the records of the seeds the
+ * replica range touches on the device (ct_validate_trace_set: CT_EINVAL naming the first bad
+ * program), runs, copies out and synchronises the stream before returning (end-to-end path;
+ * pinned host memory recommended). */
 int ct_simulate_batch_host(ct_ctx* ctx, const ct_trace_set* host_traces, const ct_sweep* sweep,
                            const ct_engine_params* eng, int64_t replica_begin,
                            int64_t replica_end, ct_replica_summary* host_out,

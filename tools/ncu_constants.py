@@ -27,9 +27,10 @@ def main():
     c = json.load(open(OUT)) if os.path.exists(OUT) else {}
     kind, rep = sys.argv[1], sys.argv[2]
     rows, units = raw(rep)
-    d = rows[0]
-    dram = num(d, "dram__bytes_read.sum") * scale(units["dram__bytes_read.sum"]) + \
-        num(d, "dram__bytes_write.sum") * scale(units["dram__bytes_write.sum"])
+    # every kernel of the report: the launches of one call (a split sweep runs two replay
+    # launches; a 32 < P <= 256 sweep its list-driven fallback launch)
+    dram = sum(num(d, "dram__bytes_read.sum") * scale(units["dram__bytes_read.sum"]) +
+               num(d, "dram__bytes_write.sum") * scale(units["dram__bytes_write.sum"]) for d in rows)
     if kind == "replay-auto":  # replica-turns from the captured run's own log line
         sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
         from ctgen import configs as cf
@@ -41,7 +42,7 @@ def main():
         kind = "replay"
     if kind == "replay":
         name, turns = sys.argv[3], float(sys.argv[4])
-        inst = num(d, "smsp__inst_executed.sum")
+        inst = sum(num(d, "smsp__inst_executed.sum") for d in rows)
         c.setdefault("replay_warp_inst_per_turn", {})[name] = inst / turns
         c.setdefault("replay_dram_bytes_per_turn", {})[name] = dram / turns
         c.setdefault("source", {})["replay_" + name] = os.path.basename(rep)

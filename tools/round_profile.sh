@@ -8,14 +8,14 @@ R=${1:-r02}
 OUT=gpurun_out
 mkdir -p $OUT
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > $OUT/${R}_gpu.txt
-cap() {  # cap NAME WORKLOAD SEEDS
-  ncu --set full --clock-control none --import-source on -k regex:replay_kernel -c 1 \
+cap() {  # cap NAME WORKLOAD SEEDS [LAUNCHES of one call]
+  ncu --set full --clock-control none --import-source on -k regex:replay_kernel -c ${4:-1} \
       -o $OUT/${R}_replay_$1 python tools/prof_kernels.py replay $2 $3 > $OUT/${R}_ncu_replay_$1.log 2>&1
 }
 cap cfg3 cfg3 256
-cap cfg2 cfg2 4096
+cap cfg2 cfg2 4096 2
 cap cfg4 cfg4 4096
-cap cfg5 cfg5 256
+cap cfg5 cfg5 256 2
 ncu --set full --clock-control none --import-source on -k regex:fit_hist -s 3 -c 1 \
     -o $OUT/${R}_fit_hist python tools/prof_kernels.py fit 28 > $OUT/${R}_ncu_fit.log 2>&1
 python tools/ncu_constants.py fit $OUT/${R}_fit_hist.ncu-rep 268435456 > $OUT/${R}_constants.log 2>&1
